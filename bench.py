@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the prefill->decode KV hand-off (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric: "KV hand-off GB/s (fp16-equiv)" = the reference's 16-bit KV volume
+(2*b*s*h*2*L, costs.py:102) moved per second, whole job, with the % of the
+HBM / NVLink roofline.
+
+* N = 1: BASELINE config 2 (LLaMA-2-7B KV, 2048 tokens x batch 8): one step =
+  K1 quantise+pack of the whole [32, 2, 16384, 32, 128] fp16 KV, then K3
+  dequantise + scatter into a paged decode cache (block 16, random block
+  table).  Inputs (8.6 GB) are far larger than L2 (126 MB), so no flush.
+* N > 1 (torchrun, one process per GPU): ranks [0, N/2) are prefill, [N/2, N)
+  decode, pair i -> i + N/2 (1P1D / 2P2D / 4P4D); see transport.py.
+* --impl reference: the CPU reference path (the C restatement of the oracle,
+  oracle/kvq_oracle.c, all host threads) on a bounded sample of the same
+  workload; rank 0 only.
+
+One JSON line on rank 0.  Timing: CUDA events on the launching streams, a
+barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KV hand-off GB/s (fp16-equiv)"
+UNIT = "GB/s"
+
+# name -> (n_layers, n_kv_heads, head_dim, batch, seq)
+WORKLOADS = {
+    "cfg1_7b_512x1": (32, 32, 128, 1, 512),
+    "cfg2_7b_2048x8": (32, 32, 128, 8, 2048),
+    "cfg3_13b_2048x8": (40, 40, 128, 8, 2048),
+    "cfg4_70b_gqa_pair": (80, 8, 128, 2, 4096),  # one 4P4D pair: 8x4096 tokens / 4 pairs
+}
+BLOCK = 16
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        time.sleep(0.1)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(parts[1]), smax=float(parts[2]), util=float(parts[4]),
+                                 reasons=[n for n, v in zip(
+                                     ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                      "sw_power_cap"), parts[5:9]) if v.lower() == "active"]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        busy = [r for r in rows if r["util"] > 0] or rows
+        reasons = sorted({x for r in busy for x in r["reasons"]})
+        return {"sm_mhz": statistics.median(r["sm"] for r in busy),
+                "sm_max_mhz": max(r["smax"] for r in rows), "reasons": reasons,
+                "samples": len(busy)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference path (oracle/kvq_oracle.c) on a bounded sample
+# ---------------------------------------------------------------------------
+_CPU_LAYERS: dict = {}
+
+
+def _cpu_layer(workload, i, T, H, D):
+    """Synthetic layer i of the workload (generated once, outside timing)."""
+    from oracle import kvq_oracle as O
+    key = (workload, i % 4)
+    if key not in _CPU_LAYERS:
+        _CPU_LAYERS[key] = O.synthetic_kv(1, T, H, D, seed=i % 4)  # [1, 2, T, H, D]
+    return _CPU_LAYERS[key]
+
+
+def cpu_reference(workload: str, bits: int, group: int, budget_s: float | None = 12.0,
+                  max_layers: int | None = None):
+    """Time the C oracle (quant+pack, then dequant+scatter into a paged cache)
+    layer by layer over the workload until ``budget_s`` or ``max_layers``."""
+    import numpy as np
+    from oracle import kvq_oracle as O
+    from oracle import kvq_oracle_c as C
+    C.lib()
+    L, H, D, b, s = WORKLOADS[workload]
+    T = b * s
+    nb = (T + BLOCK - 1) // BLOCK
+    slots = O.synthetic_slots(T, BLOCK, nb, seed=0)
+    kc = np.zeros((1, nb, BLOCK, H, D), np.float16)
+    vc = np.zeros_like(kc)
+    layers = 0
+    elapsed = 0.0
+    limit = max_layers or L
+    while layers < limit:
+        kv = _cpu_layer(workload, layers, T, H, D)
+        t0 = time.perf_counter()
+        c, sc, z = C.quant_pack(kv.reshape(-1, D), bits, group)
+        C.dequant_scatter_paged(c, sc, z, slots, 1, T, H, D, group, bits, kc, vc)
+        elapsed += time.perf_counter() - t0
+        layers += 1
+        if budget_s is not None and elapsed >= budget_s:
+            break
+    fp16_bytes = layers * 2 * T * H * D * 2
+    return dict(value=fp16_bytes / elapsed / 1e9, unit=UNIT, cores=C.threads(), kind="port",
+                sample=f"{layers}/{L} layers of {workload} ({fp16_bytes / 1e9:.2f} GB fp16), "
+                       f"oracle/kvq_oracle.c quant+pack+dequant+paged-scatter, "
+                       f"{C.threads()} OpenMP threads, {elapsed:.2f} s")
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    bits, group = args.bits, args.group
+    wl = args.workload or ("cfg2_7b_2048x8" if world == 1 else default_pair_workload(world))
+    L, H, D, b, s = WORKLOADS[wl]
+    for _ in range(args.warmup):
+        cpu_reference(wl, bits, group, budget_s=None, max_layers=1)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        r = cpu_reference(wl, bits, group, budget_s=None, max_layers=args.ref_layers)
+        vals.append(r["value"])
+        secs.append(args.ref_layers * 2 * b * s * H * D * 2 / 1e9 / r["value"])
+    value = statistics.median(vals)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.median(secs), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp16->u4", "data": "synthetic",
+        "config": {"workload": wl, "bits": bits, "group": group, "block_size": BLOCK,
+                   "sample_layers_per_step": args.ref_layers},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": r["cores"],
+                         "kind": "port", "sample": r["sample"]},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def default_pair_workload(world: int) -> str:
+    return "cfg3_13b_2048x8" if world == 2 else "cfg4_70b_gqa_pair"
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def synthetic_kv_device(torch, L, T, H, D, device, seed=0):
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    kv = torch.empty((L, 2, T, H, D), dtype=torch.float16, device=device)
+    for l in range(L):  # per layer keeps the fp32 temporary small
+        kv[l].copy_(torch.randn((2, T, H, D), generator=g, device=device, dtype=torch.float32))
+    ch = torch.randperm(D, generator=torch.Generator().manual_seed(seed))[:4].to(device)
+    kv[:, 0, :, :, ch] *= 8  # K outlier channels
+    return kv
+
+
+def paged_slots(torch, T, device, slack_blocks=64, seed=0):
+    need = (T + BLOCK - 1) // BLOCK
+    nb = need + slack_blocks
+    perm = torch.randperm(nb, generator=torch.Generator().manual_seed(seed + 1))[:need]
+    t = torch.arange(T)
+    return (perm[t // BLOCK] * BLOCK + t % BLOCK).to(device), nb
+
+
+def run_local(args, torch):
+    from paper_2502_09334_b200 import KvPrecision
+    from paper_2502_09334_b200.datapath import HandoffPlan, HostHandoff, KVPlanes
+    wl = args.workload or "cfg2_7b_2048x8"
+    L, H, D, b, s = WORKLOADS[wl]
+    T = b * s
+    dev = torch.device("cuda", torch.cuda.current_device())
+    kv = synthetic_kv_device(torch, L, T, H, D, dev)
+    slots, nb = paged_slots(torch, T, dev)
+    kc = torch.zeros((L, nb, BLOCK, H, D), dtype=torch.float16, device=dev)
+    vc = torch.zeros_like(kc)
+    plan = HandoffPlan(KVPlanes.dense(kv), KVPlanes.paged(kc, vc, slots), T,
+                       KvPrecision(args.bits), args.group, mode="local", n_chunks=args.chunks)
+    lay = plan.layout
+    fp16_bytes = lay.fp16_bytes
+    for _ in range(args.warmup):
+        plan.run()
+    torch.cuda.synchronize()
+    timing = []
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(args.steps):
+            plan.run(timing)
+        end.record()
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / args.steps
+    launches_per_step = 2 * len(plan.chunks)
+    k1 = sum(e["k1"][0].elapsed_time(e["k1"][1]) for e in timing) / args.steps
+    k3 = sum(e["k3"][0].elapsed_time(e["k3"][1]) for e in timing) / args.steps
+    kernel_bytes = fp16_bytes + lay.wire_bytes  # K1 reads fp16, writes payload; K3 the reverse
+    hbm, peak_kind = peaks()
+    dom, dom_ms = ("quant_pack", k1) if k1 >= k3 else ("dequant_scatter_paged", k3)
+    achieved = kernel_bytes / (dom_ms * 1e-3) / 1e9
+    step_bytes = 2 * kernel_bytes  # algorithmic HBM bytes of the round trip
+    roof_ms = step_bytes / (hbm * 1e9) * 1e3
+    value = fp16_bytes / (ms * 1e-3) / 1e9
+
+    # e2e: the same hand-off from pinned host KV to a host paged cache
+    e2e = None
+    if not args.no_e2e:
+        kv_h = torch.empty(kv.shape, dtype=torch.float16, pin_memory=True)
+        kv_h.copy_(kv)
+        kc_h = torch.empty(kc.shape, dtype=torch.float16, pin_memory=True)
+        vc_h = torch.empty(vc.shape, dtype=torch.float16, pin_memory=True)
+        del plan
+        host = HostHandoff(kv_h, kc_h, vc_h, slots, dev, KvPrecision(args.bits), args.group,
+                           n_chunks=max(args.chunks, 8))
+        for _ in range(max(1, min(args.warmup, 3))):
+            host.run()
+        torch.cuda.synchronize()
+        n_e2e = max(1, min(args.steps, args.e2e_steps))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n_e2e):
+            host.run()
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / n_e2e
+        e2e = {"value": round(fp16_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
+               "h2d_bytes_per_step": host.h2d_bytes, "d2h_bytes_per_step": host.d2h_bytes,
+               "ms_per_step": round(e2e_ms, 3), "steps": n_e2e,
+               "path": "pinned host KV -> H2D -> K1 -> K3 -> D2H of the paged cache, "
+                       f"{len(host.chunks)} layer chunks on 3 streams"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_reference(wl, args.bits, args.group, budget_s=args.cpu_budget)
+    return dict(
+        value=value, ms=ms, workload=wl, fp16_bytes=fp16_bytes, wire_bytes=lay.wire_bytes,
+        launches=launches_per_step * args.steps, clocks=clk.summary(), e2e=e2e, cpu=cpu,
+        roofline={"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                  "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                  "frac": round(achieved / hbm, 4), "traffic": None,
+                  "algorithmic_bytes_per_launch": kernel_bytes // len(plan_chunks(args, L)),
+                  "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
+                  "step_roofline_ms": round(roof_ms, 4), "step_frac": round(roof_ms / ms, 4)},
+        extra={"n_chunks": args.chunks, "mode": "local"},
+    )
+
+
+def plan_chunks(args, L):
+    from paper_2502_09334_b200.datapath import layer_chunks
+    return layer_chunks(L, args.chunks)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
+    ap.add_argument("--bits", type=int, default=4)
+    ap.add_argument("--group", type=int, default=128)
+    ap.add_argument("--chunks", type=int, default=1)
+    ap.add_argument("--mode", default="pull", choices=["pull", "push", "copy", "nccl"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-layers", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    from paper_2502_09334_b200 import _lib
+    _lib.load()
+    if world > 1:
+        from paper_2502_09334_b200 import transport
+        transport.bench_pairs(args, torch, rank, world, emit=emit)
+        return
+    torch.cuda.set_device(0)
+    r = run_local(args, torch)
+    emit(args, r, world)
+
+
+def emit(args, r, world):
+    out = {
+        "metric": METRIC, "value": round(r["value"], 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms"], 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16->u4",
+        "data": "synthetic",
+        "config": {"workload": r["workload"], "bits": args.bits, "group": args.group,
+                   "block_size": BLOCK, "fp16_bytes_per_step": r["fp16_bytes"],
+                   "wire_bytes_per_step": r["wire_bytes"],
+                   "l2": "inputs larger than L2 (no flush)", **r.get("extra", {})},
+        "roofline": r["roofline"],
+        "cpu_baseline": r["cpu"],
+        "e2e": r["e2e"],
+        "clocks": r["clocks"],
+        "gpu_launches": r["launches"],
+    }
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,149 @@
+/*
+ * kvx.h - C-ABI of the B200 (sm_100a) prefill->decode KV hand-off library.
+ *
+ * Reference interface being replaced
+ * ----------------------------------
+ * The reference (ThunderServe planner, /root/reference/pkg) ships the hand-off
+ * only as an analytic model:
+ *   KvPrecision            pkg/src/hetplan/costs.py:18-30   (bits in {16,8,4,2})
+ *   bottleneck_link        pkg/src/hetplan/costs.py:51-65   (the P->D link)
+ *   kv_comm_cost           pkg/src/hetplan/costs.py:83-103  (alpha + 2bshN_bytesL/beta)
+ * called at the hand-off site pkg/src/hetplan/simulate.py:221-235 and in
+ * pkg/src/hetplan/orchestrate.py:369-372.  The data path it models
+ * (PAPER.md:490-493 quantise+pack -> transfer -> unpack+dequantise; NCCL
+ * async SendRecv/cudaMemcpy from prefill-side KV queues) is
+ * what these entry points implement.  The Python layer
+ * (paper_2502_09334_b200/) keeps KvPrecision / kv_comm_cost verbatim and binds
+ * these symbols with ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - The caller owns every buffer; nothing here allocates on the hot path
+ *    (kvx_malloc exists only for IPC-exportable staging buffers at setup).
+ *  - Every compute/transfer call is stream-ordered and asynchronous; `stream`
+ *    is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Return 0 on success, else a kvx/cuda error code; kvx_strerror() names it.
+ *    No exceptions cross the ABI.  Re-entrant across host threads.
+ *  - Device pointers may be local, peer-mapped (kvx_enable_peer) or
+ *    IPC-mapped (kvx_ipc_open): a quantise kernel writing into a peer buffer
+ *    is the fused quantise+NVLink-push path, a dequantise kernel reading from
+ *    a peer buffer is the fused NVLink-pull+dequantise path.
+ *
+ * Data layout (HBM)
+ *  - KV source / destination planes are paged or dense token-major:
+ *      plane(l, kv) = (kv ? v_base : k_base) + l * layer_stride    [elements]
+ *      token t of a plane lives at plane + pos(t) * n_heads * head_dim
+ *      pos(t) = slots ? slots[t] : t   (slots[t] < 0 = padding, skipped on
+ *      the decode side; vLLM flash layout [num_blocks, block_size, H, D]
+ *      has pos = block * block_size + offset).
+ *  - Packed payload, per layer l (row i = (kv*n_tokens + t)*n_heads + h):
+ *      codes  uint8 [2*T*H][head_dim*bits/8]  code k of a byte at bits
+ *             [k*bits, (k+1)*bits) (low = even element; KIVI's int32 order)
+ *      scale  fp16  [2*T*H][head_dim/group]
+ *      zero   fp16  [2*T*H][head_dim/group]
+ *    payload_layer_stride == 0: three dense arrays, layers back to back in
+ *    each.  payload_layer_stride > 0 (bytes, multiple of 16): one segment per
+ *    layer, codes/scale/zero of layer l at codes/scale/zero + l*stride -- a
+ *    range of layers is then ONE contiguous byte range (one NVLink copy or
+ *    one doorbell per layer chunk).
+ *    bits == 16 is passthrough: codes are the raw fp16 rows, no scale/zero.
+ *  - Arithmetic (bit-exact vs oracle/):
+ *      z = f16(min + 0), s = f16((max - min)/(2^bits-1) + 0)  [IEEE fp32]
+ *      q = s == 0 ? 0 : min(rint_even((x - z) * rcp_rn(s)), 2^bits-1)
+ *      x_hat = f16_rn(min(q*s + z, 65504))  (one rounding: fp16 FMA)
+ */
+#ifndef KVX_H_
+#define KVX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVX_OK 0
+/* kvx-specific codes live above the cudaError_t range. */
+#define KVX_ERR_INVALID_ARG 10001  /* ValueError on the Python side         */
+#define KVX_ERR_NO_PATH 10002      /* NoPath: no peer access between GPUs    */
+#define KVX_ERR_UNSUPPORTED 10003  /* stream memory ops etc. unavailable     */
+
+/* Library version (major*10000 + minor*100 + patch). */
+int kvx_version(void);
+
+/* Human-readable name of a return code (kvx or cudaError_t). */
+const char* kvx_strerror(int code);
+
+/* Number of CUDA devices visible (0 on a host without GPUs). */
+int kvx_device_count(int* count);
+
+/*
+ * K1: per-group asymmetric quantise + pack (prefill side).
+ * Replaces the 2*b*s*h*N_bytes*L "compress" term of kv_comm_cost
+ * (costs.py:102) with real data.  Reads n_layers*2*n_tokens*n_heads rows of
+ * head_dim fp16 from the (possibly paged: src_slots != NULL) source planes and
+ * writes the dense packed payload.  codes/scale/zero may be peer pointers
+ * (fused NVLink push).  bits in {2,4,8} (16 = passthrough copy, scale/zero
+ * ignored); group in {32,64,128} dividing head_dim; head_dim % 8 == 0.
+ */
+int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                   const int64_t* src_slots, int64_t n_layers, int64_t n_tokens, int n_heads,
+                   int head_dim, int group, int bits, void* codes, void* scale, void* zero,
+                   int64_t payload_layer_stride, void* stream);
+
+/*
+ * K3: unpack + dequantise + scatter into the decode side's paged KV cache.
+ * Replaces the ready = prefill_done + kv_delay step (simulate.py:235) with the
+ * real decode-side enrolment.  codes/scale/zero may be peer pointers (fused
+ * NVLink pull).  dst_slots[t] < 0 skips token t.  block_size is implied by the
+ * slot values (pos = block*block_size + offset).
+ */
+int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
+                              int64_t payload_layer_stride, const int64_t* dst_slots,
+                              int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                              int group, int bits, void* k_cache, void* v_cache,
+                              int64_t dst_layer_stride, void* stream);
+
+/* Packed payload sizes in bytes for n_rows rows (codes, scale, zero). */
+int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t* codes_bytes,
+                     int64_t* scale_bytes, int64_t* zero_bytes);
+
+/* ---- transport: NVLink P2P within one process --------------------------- */
+
+/* Enable peer access a->b and b->a (idempotent).  KVX_ERR_NO_PATH if the
+ * devices cannot access each other (costs.py:63-64 raises NoPath there). */
+int kvx_enable_peer(int dev_a, int dev_b);
+
+/* Copy-engine peer copy (cudaMemcpyPeerAsync): the non-fused baseline. */
+int kvx_copy_peer(void* dst, int dst_dev, const void* src, int src_dev, size_t n_bytes,
+                  void* stream);
+
+/* ---- transport: NVLink P2P across processes (one process per GPU) ------- */
+
+/* IPC-exportable device allocation (setup only, never on the hot path). */
+int kvx_malloc(void** ptr, size_t n_bytes);
+int kvx_free(void* ptr);
+int kvx_memset_async(void* ptr, int value, size_t n_bytes, void* stream);
+
+/* cudaIpcMemHandle_t export / import (64 opaque bytes). ptr must be a
+ * kvx_malloc base pointer.  kvx_ipc_open maps a peer's buffer into this
+ * process (peer access implied); kvx_ipc_close unmaps it. */
+int kvx_ipc_handle_size(void);
+int kvx_ipc_get_handle(void* ptr, void* handle_out);
+int kvx_ipc_open(const void* handle, void** ptr_out);
+int kvx_ipc_close(void* ptr);
+
+/* Stream-ordered 32-bit flags (cuStreamWriteValue32 / cuStreamWaitValue32
+ * GEQ) used as cross-GPU chunk doorbells: the producer signals after the
+ * chunk's kernel (with a memory barrier), the consumer's stream blocks in the
+ * front-end (no spinning kernel) until flag >= value.  flag may be a local,
+ * peer or IPC-mapped device address. */
+int kvx_stream_signal(void* flag, uint32_t value, void* stream);
+int kvx_stream_wait(const void* flag, uint32_t value, void* stream);
+/* 1 if stream memory operations are usable on the current device. */
+int kvx_stream_memops_supported(int* supported);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KVX_H_ */

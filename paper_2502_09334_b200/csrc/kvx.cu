@@ -1,0 +1,341 @@
+// C-ABI of the B200 KV hand-off library (see include/kvx.h for the contract).
+//
+// Host side only: argument validation, launch geometry, dispatch on
+// (bits, group), and the transport primitives (peer access, IPC mapping,
+// stream-ordered doorbells).  Device code lives in kvx_kernels.cuh.
+#include <cuda.h>  // driver API types only; entry points resolved at run time
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "../../include/kvx.h"
+#include "kvx_kernels.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerBlock = kThreads / 32;
+constexpr int kMaxDev = 64;
+
+int sm_count(int dev) {
+  static int cache[kMaxDev] = {0};
+  if (dev < 0 || dev >= kMaxDev) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+template <typename K>
+int blocks_per_sm(K kernel) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b <= 0)
+    b = 4;
+  return b;
+}
+
+// Persistent-style grid: enough warps to cover every token row once, capped at
+// the number of CTAs the SMs hold concurrently (a multiple of the SM count).
+template <typename K>
+dim3 grid_for(K kernel, int64_t n_token_rows) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int64_t full = int64_t(sm_count(dev)) * blocks_per_sm(kernel);
+  const int64_t need = (n_token_rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  int64_t g = need < full ? need : full;
+  if (g < 1) g = 1;
+  return dim3(unsigned(g));
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int valid_format(int head_dim, int group, int bits) {
+  if (head_dim <= 0 || head_dim % 8) return KVX_ERR_INVALID_ARG;
+  if (bits == 16) return KVX_OK;
+  if (bits != 2 && bits != 4 && bits != 8) return KVX_ERR_INVALID_ARG;
+  if (group != 32 && group != 64 && group != 128) return KVX_ERR_INVALID_ARG;
+  if (head_dim % group) return KVX_ERR_INVALID_ARG;
+  return KVX_OK;
+}
+
+int make_geo(kvx::Geo& g, const void* k, const void* v, int64_t layer_stride, const int64_t* slots,
+             int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim, int group, int bits,
+             int64_t payload_layer_stride) {
+  if (n_layers < 0 || n_tokens < 0 || n_heads <= 0) return KVX_ERR_INVALID_ARG;
+  const int64_t row_elems = int64_t(n_heads) * head_dim;
+  if (row_elems > (int64_t(1) << 30)) return KVX_ERR_INVALID_ARG;
+  if (n_layers > 0 && n_tokens > 0) {
+    if (!k || !v || !aligned(k, 16) || !aligned(v, 16)) return KVX_ERR_INVALID_ARG;
+    if ((layer_stride * 2) % 16) return KVX_ERR_INVALID_ARG;
+  }
+  g.k_plane = static_cast<const char*>(k);
+  g.v_plane = static_cast<const char*>(v);
+  g.layer_stride_b = layer_stride * 2;
+  g.slots = slots;
+  g.n_tokens = n_tokens;
+  g.n_token_rows = n_layers * 2 * n_tokens;
+  g.row_elems = int(row_elems);
+  g.vecs = int(row_elems / 8);
+  // Payload layer strides: dense per-array layout when payload_layer_stride == 0,
+  // else one segment per layer holding [codes | scale | zero].
+  const int64_t rows_per_layer = 2 * n_tokens * n_heads;
+  const int64_t ng = bits == 16 ? 0 : head_dim / group;
+  if (payload_layer_stride < 0) return KVX_ERR_INVALID_ARG;
+  if (payload_layer_stride == 0) {
+    g.codes_ls = rows_per_layer * head_dim * bits / 8;
+    g.meta_ls = rows_per_layer * ng * 2;
+  } else {
+    if (payload_layer_stride % 16) return KVX_ERR_INVALID_ARG;
+    g.codes_ls = payload_layer_stride;
+    g.meta_ls = payload_layer_stride;
+  }
+  return KVX_OK;
+}
+
+constexpr int kUnroll = 4;
+
+template <int BITS, int G>
+cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero, cudaStream_t s) {
+  auto k = kvx::quant_pack_kernel<BITS, G, kUnroll>;
+  k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, static_cast<uint8_t*>(codes),
+                                                      static_cast<__half*>(scale),
+                                                      static_cast<__half*>(zero));
+  return cudaGetLastError();
+}
+
+template <int BITS, int G>
+cudaError_t launch_dequant(const kvx::Geo& g, const void* codes, const void* scale,
+                           const void* zero, cudaStream_t s) {
+  auto k = kvx::dequant_scatter_kernel<BITS, G, kUnroll>;
+  k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, static_cast<const uint8_t*>(codes),
+                                                      static_cast<const __half*>(scale),
+                                                      static_cast<const __half*>(zero));
+  return cudaGetLastError();
+}
+
+template <int BITS>
+cudaError_t dispatch_quant(int group, const kvx::Geo& g, void* c, void* sc, void* z, cudaStream_t s) {
+  switch (group) {
+    case 32: return launch_quant<BITS, 32>(g, c, sc, z, s);
+    case 64: return launch_quant<BITS, 64>(g, c, sc, z, s);
+    default: return launch_quant<BITS, 128>(g, c, sc, z, s);
+  }
+}
+
+template <int BITS>
+cudaError_t dispatch_dequant(int group, const kvx::Geo& g, const void* c, const void* sc,
+                             const void* z, cudaStream_t s) {
+  switch (group) {
+    case 32: return launch_dequant<BITS, 32>(g, c, sc, z, s);
+    case 64: return launch_dequant<BITS, 64>(g, c, sc, z, s);
+    default: return launch_dequant<BITS, 128>(g, c, sc, z, s);
+  }
+}
+
+// ---- driver entry points (resolved lazily; no link-time libcuda dependency)
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_writeValue32 g_write32 = nullptr;
+PFN_waitValue32 g_wait32 = nullptr;
+std::once_flag g_drv_once;
+int g_drv_status = KVX_ERR_UNSUPPORTED;
+
+void resolve_driver() {
+  std::call_once(g_drv_once, [] {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* w = nullptr;
+    void* t = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &t, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && t) {
+      g_write32 = reinterpret_cast<PFN_writeValue32>(w);
+      g_wait32 = reinterpret_cast<PFN_waitValue32>(t);
+      g_drv_status = KVX_OK;
+    }
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int kvx_version(void) { return 100; }
+
+const char* kvx_strerror(int code) {
+  switch (code) {
+    case KVX_OK: return "ok";
+    case KVX_ERR_INVALID_ARG: return "kvx: invalid argument";
+    case KVX_ERR_NO_PATH: return "kvx: no peer path between devices";
+    case KVX_ERR_UNSUPPORTED: return "kvx: operation unsupported on this device/driver";
+    default: return cudaGetErrorString(static_cast<cudaError_t>(code));
+  }
+}
+
+int kvx_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return KVX_OK;
+}
+
+int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t* codes_bytes,
+                     int64_t* scale_bytes, int64_t* zero_bytes) {
+  int rc = valid_format(head_dim, group, bits);
+  if (rc) return rc;
+  if (n_rows < 0) return KVX_ERR_INVALID_ARG;
+  const int64_t ng = bits == 16 ? 0 : head_dim / group;
+  if (codes_bytes) *codes_bytes = n_rows * head_dim * bits / 8;
+  if (scale_bytes) *scale_bytes = n_rows * ng * 2;
+  if (zero_bytes) *zero_bytes = n_rows * ng * 2;
+  return KVX_OK;
+}
+
+int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                   const int64_t* src_slots, int64_t n_layers, int64_t n_tokens, int n_heads,
+                   int head_dim, int group, int bits, void* codes, void* scale, void* zero,
+                   int64_t payload_layer_stride, void* stream) {
+  int rc = valid_format(head_dim, group, bits);
+  if (rc) return rc;
+  kvx::Geo g;
+  rc = make_geo(g, k_src, v_src, src_layer_stride, src_slots, n_layers, n_tokens, n_heads, head_dim,
+                group, bits, payload_layer_stride);
+  if (rc) return rc;
+  if (g.n_token_rows == 0) return KVX_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (bits == 16) {
+    if (!codes || !aligned(codes, 16)) return KVX_ERR_INVALID_ARG;
+    auto k = kvx::pack16_kernel<kUnroll>;
+    k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, static_cast<uint8_t*>(codes));
+    return cudaGetLastError();
+  }
+  if (!codes || !scale || !zero || !aligned(codes, bits) || !aligned(scale, 2) || !aligned(zero, 2))
+    return KVX_ERR_INVALID_ARG;
+  switch (bits) {
+    case 2: return dispatch_quant<2>(group, g, codes, scale, zero, s);
+    case 8: return dispatch_quant<8>(group, g, codes, scale, zero, s);
+    default: return dispatch_quant<4>(group, g, codes, scale, zero, s);
+  }
+}
+
+int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
+                              int64_t payload_layer_stride, const int64_t* dst_slots,
+                              int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                              int group, int bits, void* k_cache, void* v_cache,
+                              int64_t dst_layer_stride, void* stream) {
+  int rc = valid_format(head_dim, group, bits);
+  if (rc) return rc;
+  kvx::Geo g;
+  rc = make_geo(g, k_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
+                head_dim, group, bits, payload_layer_stride);
+  if (rc) return rc;
+  if (g.n_token_rows == 0) return KVX_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (bits == 16) {
+    if (!codes || !aligned(codes, 16)) return KVX_ERR_INVALID_ARG;
+    auto k = kvx::scatter16_kernel<kUnroll>;
+    k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, static_cast<const uint8_t*>(codes));
+    return cudaGetLastError();
+  }
+  if (!codes || !scale || !zero || !aligned(codes, bits) || !aligned(scale, 2) || !aligned(zero, 2))
+    return KVX_ERR_INVALID_ARG;
+  switch (bits) {
+    case 2: return dispatch_dequant<2>(group, g, codes, scale, zero, s);
+    case 8: return dispatch_dequant<8>(group, g, codes, scale, zero, s);
+    default: return dispatch_dequant<4>(group, g, codes, scale, zero, s);
+  }
+}
+
+// ---- transport -------------------------------------------------------------
+
+int kvx_enable_peer(int a, int b) {
+  if (a == b) return KVX_OK;
+  int ab = 0, ba = 0;
+  cudaError_t e = cudaDeviceCanAccessPeer(&ab, a, b);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceCanAccessPeer(&ba, b, a);
+  if (e != cudaSuccess) return e;
+  if (!ab || !ba) return KVX_ERR_NO_PATH;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  int pairs[2][2] = {{a, b}, {b, a}};
+  for (auto& p : pairs) {
+    cudaSetDevice(p[0]);
+    e = cudaDeviceEnablePeerAccess(p[1], 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+      cudaGetLastError();
+      e = cudaSuccess;
+    }
+    if (e != cudaSuccess) break;
+  }
+  cudaSetDevice(cur);
+  return e;
+}
+
+int kvx_copy_peer(void* dst, int dst_dev, const void* src, int src_dev, size_t n, void* stream) {
+  if (n == 0) return KVX_OK;
+  return cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, n, static_cast<cudaStream_t>(stream));
+}
+
+int kvx_malloc(void** ptr, size_t n) {
+  if (!ptr) return KVX_ERR_INVALID_ARG;
+  return cudaMalloc(ptr, n ? n : 256);
+}
+
+int kvx_free(void* ptr) { return ptr ? cudaFree(ptr) : KVX_OK; }
+
+int kvx_memset_async(void* ptr, int value, size_t n, void* stream) {
+  return cudaMemsetAsync(ptr, value, n, static_cast<cudaStream_t>(stream));
+}
+
+int kvx_ipc_handle_size(void) { return int(sizeof(cudaIpcMemHandle_t)); }
+
+int kvx_ipc_get_handle(void* ptr, void* out) {
+  if (!ptr || !out) return KVX_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e != cudaSuccess) return e;
+  memcpy(out, &h, sizeof(h));
+  return KVX_OK;
+}
+
+int kvx_ipc_open(const void* handle, void** ptr_out) {
+  if (!handle || !ptr_out) return KVX_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+}
+
+int kvx_ipc_close(void* ptr) { return ptr ? cudaIpcCloseMemHandle(ptr) : KVX_OK; }
+
+int kvx_stream_memops_supported(int* supported) {
+  resolve_driver();
+  if (supported) *supported = (g_drv_status == KVX_OK);
+  return KVX_OK;
+}
+
+int kvx_stream_signal(void* flag, uint32_t value, void* stream) {
+  resolve_driver();
+  if (g_drv_status) return g_drv_status;
+  if (!flag || !aligned(flag, 4)) return KVX_ERR_INVALID_ARG;
+  CUresult r = g_write32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                         CU_STREAM_WRITE_VALUE_DEFAULT);
+  return r == CUDA_SUCCESS ? KVX_OK : KVX_ERR_UNSUPPORTED;
+}
+
+int kvx_stream_wait(const void* flag, uint32_t value, void* stream) {
+  resolve_driver();
+  if (g_drv_status) return g_drv_status;
+  if (!flag || !aligned(flag, 4)) return KVX_ERR_INVALID_ARG;
+  CUresult r = g_wait32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? KVX_OK : KVX_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

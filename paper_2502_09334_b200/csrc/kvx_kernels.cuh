@@ -1,0 +1,366 @@
+// Device code of the KV hand-off: K1 quantise+pack, K3 dequantise+paged scatter.
+//
+// Both kernels are HBM/NVLink-bandwidth kernels (no tensor cores: ~8 flops per
+// 2.53 B moved).  Work unit = one "token row": the n_heads*head_dim fp16
+// elements of one (layer, K|V, token) -- contiguous on the paged side (vLLM
+// flash layout) and contiguous in the dense packed payload.  One warp owns a
+// token row at a time (grid-stride over token rows), so slot lookups and
+// index math are paid once per 2-8 KB instead of once per element.
+//
+// Thread -> data: lane handles 16-byte vectors (8 fp16) at vector index
+// v = lane + 32*k (k < UNROLL) + 32*UNROLL*iter within the token row.  A
+// quantisation group of G elements is G/8 consecutive lanes, so group
+// min/max is a half2 hmin2 tree inside the lane plus log2(G/8) xor-shuffles.
+//
+// Format (bit-exact with oracle/, see include/kvx.h):
+//   z = f16(min + 0); s = f16((max - min)/(2^b - 1) + 0)   [IEEE fp32]
+//   q = s == 0 ? 0 : min(rint_even((x - z) * rcp_rn(s)), 2^b - 1)
+//   x_hat = f16_rn(min(q*s + z, 65504))     [single-rounding fp16 FMA]
+#pragma once
+
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace kvx {
+
+struct __align__(16) U4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ U4 ld_stream(const void* p) {
+  // Read-once data: do not allocate in L1.
+  U4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream(void* p, const U4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t h2_as_u32(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u32_as_h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t orv) {
+  // (a & mask) | orv  in one LOP3
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(mask), "r"(orv));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Codes <-> 8 elements per lane
+// ---------------------------------------------------------------------------
+template <int BITS>
+struct CodeVec;  // storage for the 8 codes of one 16-byte vector
+
+template <>
+struct CodeVec<4> {
+  using T = uint32_t;
+};
+template <>
+struct CodeVec<8> {
+  using T = uint2;
+};
+template <>
+struct CodeVec<2> {
+  using T = uint16_t;
+};
+
+// Quantise 8 fp32-exact values (given as 4 half2) with (z, inv) and pack.
+template <int BITS>
+__device__ __forceinline__ typename CodeVec<BITS>::T quant8(const U4& v, float z, float inv) {
+  constexpr uint32_t QMAX = (1u << BITS) - 1u;
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t q[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __half22float2(u32_as_h2(w[i]));
+    // t = RN(RN(x - z) * inv); rint_even(t) via the 2^23 magic add (t >= 0).
+    float t0 = __fmul_rn(__fsub_rn(f.x, z), inv);
+    float t1 = __fmul_rn(__fsub_rn(f.y, z), inv);
+    uint32_t m0 = __float_as_uint(__fadd_rn(t0, 8388608.0f)) - 0x4B000000u;
+    uint32_t m1 = __float_as_uint(__fadd_rn(t1, 8388608.0f)) - 0x4B000000u;
+    q[2 * i] = min(m0, QMAX);
+    q[2 * i + 1] = min(m1, QMAX);
+  }
+  if constexpr (BITS == 4) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r |= q[i] << (4 * i);
+    return r;
+  } else if constexpr (BITS == 8) {
+    uint2 r;
+    r.x = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+    r.y = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
+    return r;
+  } else {
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r |= q[i] << (2 * i);
+    return (uint16_t)r;
+  }
+}
+
+// Dequantise 8 codes to 8 fp16 with a single-rounding fp16 FMA.
+template <int BITS>
+__device__ __forceinline__ U4 dequant8(typename CodeVec<BITS>::T c, __half2 s2, __half2 z2) {
+  const __half2 k1024 = u32_as_h2(0x64006400u);   // (1024, 1024)
+  const __half2 kmax = u32_as_h2(0x7BFF7BFFu);    // (65504, 65504)
+  uint32_t p[4];  // half2 pairs, each holding (1024 + q_a, 1024 + q_b)
+  if constexpr (BITS == 4) {
+    // pairs (n_j, n_{j+4}) by shift+LOP3, then PRMT back to element order.
+    uint32_t a0 = lop3_and_or(c, 0x000F000Fu, 0x64006400u);        // (n0, n4)
+    uint32_t a1 = lop3_and_or(c >> 4, 0x000F000Fu, 0x64006400u);   // (n1, n5)
+    uint32_t a2 = lop3_and_or(c >> 8, 0x000F000Fu, 0x64006400u);   // (n2, n6)
+    uint32_t a3 = lop3_and_or(c >> 12, 0x000F000Fu, 0x64006400u);  // (n3, n7)
+    p[0] = prmt(a0, a1, 0x5410);  // (n0, n1)
+    p[1] = prmt(a2, a3, 0x5410);  // (n2, n3)
+    p[2] = prmt(a0, a1, 0x7632);  // (n4, n5)
+    p[3] = prmt(a2, a3, 0x7632);  // (n6, n7)
+  } else if constexpr (BITS == 8) {
+    p[0] = prmt(c.x, 0x64646464u, 0x4140);
+    p[1] = prmt(c.x, 0x64646464u, 0x4342);
+    p[2] = prmt(c.y, 0x64646464u, 0x4140);
+    p[3] = prmt(c.y, 0x64646464u, 0x4342);
+  } else {
+    uint32_t w = c;
+    w = w | (w << 14);  // element 2i at bits [2i,2i+2), element 2i+1 moved to bit 16+2i
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p[i] = lop3_and_or(w >> (4 * i), 0x00030003u, 0x64006400u);
+  }
+  U4 out;
+  uint32_t* o = &out.x;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __half2 qh = __hsub2(u32_as_h2(p[i]), k1024);  // exact
+    __half2 y = __hfma2(qh, s2, z2);               // RN16(q*s + z), one rounding
+    o[i] = h2_as_u32(__hmin2(y, kmax));            // saturate (+inf -> 65504)
+  }
+  return out;
+}
+
+// min (x) and -max (y) of 8 halves, as one half2 so one shuffle reduces both.
+__device__ __forceinline__ __half2 minnegmax8(const U4& v) {
+  __half2 a = u32_as_h2(v.x), b = u32_as_h2(v.y), c = u32_as_h2(v.z), d = u32_as_h2(v.w);
+  __half2 mn = __hmin2(__hmin2(a, b), __hmin2(c, d));
+  __half2 mx = __hmax2(__hmax2(a, b), __hmax2(c, d));
+  __half lo = __hmin(__low2half(mn), __high2half(mn));
+  __half hi = __hmax(__low2half(mx), __high2half(mx));
+  return __halves2half2(lo, __hneg(hi));
+}
+
+// Token-row geometry shared by both kernels.
+struct Geo {
+  const char* k_plane;     // K plane of layer 0 (paged/dense side)
+  const char* v_plane;     // V plane of layer 0
+  int64_t layer_stride_b;  // bytes between layers on the paged/dense side
+  const int64_t* slots;    // token -> position on the paged side (nullable)
+  int64_t n_tokens;
+  int64_t n_token_rows;    // n_layers * 2 * n_tokens
+  int64_t codes_ls;        // payload: bytes between layers of the codes array
+  int64_t meta_ls;         // payload: bytes between layers of scale / zero
+  int row_elems;           // n_heads * head_dim
+  int vecs;                // row_elems / 8
+};
+
+__device__ __forceinline__ int64_t pos_of(const Geo& g, int64_t t) {
+  return g.slots ? __ldg(g.slots + t) : t;
+}
+
+// Token row tr = (l*2 + kv)*T + t -> (layer, row index inside the layer's payload).
+__device__ __forceinline__ void split_tr(const Geo& g, int64_t tr, int64_t& lk, int64_t& t,
+                                         int64_t& layer, int64_t& lrow) {
+  lk = tr / g.n_tokens;
+  t = tr - lk * g.n_tokens;
+  layer = lk >> 1;
+  lrow = tr - layer * 2 * g.n_tokens;
+}
+
+// ---------------------------------------------------------------------------
+// K1: quantise + pack.  codes/scale/zero may be peer (NVLink push) pointers.
+// ---------------------------------------------------------------------------
+template <int BITS, int G, int UNROLL>
+__global__ void __launch_bounds__(256) quant_pack_kernel(Geo g, uint8_t* __restrict__ codes,
+                                                         __half* __restrict__ scale,
+                                                         __half* __restrict__ zero) {
+  constexpr int LPG = G / 8;  // lanes per group
+  constexpr float QMAXF = float((1 << BITS) - 1);
+  using CT = typename CodeVec<BITS>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int groups_per_row = g.row_elems / G;
+
+  for (int64_t tr = warp; tr < g.n_token_rows; tr += n_warps) {
+    int64_t lk, t, layer, lrow;
+    split_tr(g, tr, lk, t, layer, lrow);
+    const int64_t pos = pos_of(g, t);
+    const char* plane = ((lk & 1) ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
+    const U4* src = reinterpret_cast<const U4*>(plane + pos * int64_t(g.row_elems) * 2);
+    CT* dst_codes = reinterpret_cast<CT*>(codes + layer * g.codes_ls) + lrow * g.vecs;
+    __half* dst_scale =
+        reinterpret_cast<__half*>(reinterpret_cast<char*>(scale) + layer * g.meta_ls) +
+        lrow * groups_per_row;
+    __half* dst_zero =
+        reinterpret_cast<__half*>(reinterpret_cast<char*>(zero) + layer * g.meta_ls) +
+        lrow * groups_per_row;
+
+    for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
+      U4 v[UNROLL];
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int vi = base + k * 32 + lane;
+        if (vi < g.vecs) v[k] = ld_stream(src + vi);
+        else v[k] = U4{0u, 0u, 0u, 0u};
+      }
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int vi = base + k * 32 + lane;
+        __half2 r = minnegmax8(v[k]);
+#pragma unroll
+        for (int off = LPG / 2; off > 0; off >>= 1)
+          r = __hmin2(r, u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(r), off)));
+        const float mn = __low2float(r);
+        const float mx = -__high2float(r);
+        const __half z16 = __float2half_rn(__fadd_rn(mn, 0.0f));
+        const float sq = __fdiv_rn(__fsub_rn(mx, mn), QMAXF);
+        const __half s16 = __float2half_rn(__fadd_rn(sq, 0.0f));
+        const float s = __half2float(s16);
+        const float inv = (s != 0.0f) ? __frcp_rn(s) : 0.0f;
+        const CT c = quant8<BITS>(v[k], __half2float(z16), inv);
+        if (vi < g.vecs) {
+          dst_codes[vi] = c;
+          if ((lane & (LPG - 1)) == 0) {
+            const int gi = vi / LPG;
+            dst_scale[gi] = s16;
+            dst_zero[gi] = z16;
+          }
+        }
+      }
+    }
+  }
+}
+
+// 16-bit passthrough on the prefill side: copy rows into the dense payload.
+template <int UNROLL>
+__global__ void __launch_bounds__(256) pack16_kernel(Geo g, uint8_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t tr = warp; tr < g.n_token_rows; tr += n_warps) {
+    int64_t lk, t, layer, lrow;
+    split_tr(g, tr, lk, t, layer, lrow);
+    const int64_t pos = pos_of(g, t);
+    const char* plane = ((lk & 1) ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
+    const U4* src = reinterpret_cast<const U4*>(plane + pos * int64_t(g.row_elems) * 2);
+    U4* dst = reinterpret_cast<U4*>(out + layer * g.codes_ls) + lrow * g.vecs;
+    for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
+      U4 v[UNROLL];
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int vi = base + k * 32 + lane;
+        if (vi < g.vecs) v[k] = ld_stream(src + vi);
+      }
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int vi = base + k * 32 + lane;
+        if (vi < g.vecs) st_stream(dst + vi, v[k]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: unpack + dequantise + scatter into the paged cache.  codes/scale/zero
+// may be peer (NVLink pull) pointers.  Token rows with slot < 0 are skipped.
+// ---------------------------------------------------------------------------
+template <int BITS, int G, int UNROLL>
+__global__ void __launch_bounds__(256) dequant_scatter_kernel(Geo g,
+                                                              const uint8_t* __restrict__ codes,
+                                                              const __half* __restrict__ scale,
+                                                              const __half* __restrict__ zero) {
+  constexpr int LPG = G / 8;
+  using CT = typename CodeVec<BITS>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int groups_per_row = g.row_elems / G;
+
+  for (int64_t tr = warp; tr < g.n_token_rows; tr += n_warps) {
+    int64_t lk, t, layer, lrow;
+    split_tr(g, tr, lk, t, layer, lrow);
+    const int64_t pos = pos_of(g, t);
+    if (pos < 0) continue;  // padding token (vLLM slot -1)
+    char* plane = const_cast<char*>((lk & 1) ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
+    U4* dst = reinterpret_cast<U4*>(plane + pos * int64_t(g.row_elems) * 2);
+    const CT* src_codes = reinterpret_cast<const CT*>(codes + layer * g.codes_ls) + lrow * g.vecs;
+    const __half* src_scale =
+        reinterpret_cast<const __half*>(reinterpret_cast<const char*>(scale) + layer * g.meta_ls) +
+        lrow * groups_per_row;
+    const __half* src_zero =
+        reinterpret_cast<const __half*>(reinterpret_cast<const char*>(zero) + layer * g.meta_ls) +
+        lrow * groups_per_row;
+
+    for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
+      CT c[UNROLL];
+      __half s[UNROLL], z[UNROLL];
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int vi = base + k * 32 + lane;
+        if (vi < g.vecs) {
+          c[k] = src_codes[vi];
+          s[k] = src_scale[vi / LPG];
+          z[k] = src_zero[vi / LPG];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int vi = base + k * 32 + lane;
+        if (vi < g.vecs) st_stream(dst + vi, dequant8<BITS>(c[k], __half2half2(s[k]), __half2half2(z[k])));
+      }
+    }
+  }
+}
+
+// 16-bit passthrough on the decode side: scatter the raw fp16 rows.
+template <int UNROLL>
+__global__ void __launch_bounds__(256) scatter16_kernel(Geo g, const uint8_t* __restrict__ in) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t tr = warp; tr < g.n_token_rows; tr += n_warps) {
+    int64_t lk, t, layer, lrow;
+    split_tr(g, tr, lk, t, layer, lrow);
+    const int64_t pos = pos_of(g, t);
+    if (pos < 0) continue;
+    char* plane = const_cast<char*>((lk & 1) ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
+    U4* dst = reinterpret_cast<U4*>(plane + pos * int64_t(g.row_elems) * 2);
+    const U4* src = reinterpret_cast<const U4*>(in + layer * g.codes_ls) + lrow * g.vecs;
+    for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
+      U4 v[UNROLL];
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int vi = base + k * 32 + lane;
+        if (vi < g.vecs) v[k] = ld_stream(src + vi);
+      }
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const int vi = base + k * 32 + lane;
+        if (vi < g.vecs) st_stream(dst + vi, v[k]);
+      }
+    }
+  }
+}
+
+}  // namespace kvx

@@ -1,0 +1,107 @@
+"""The C-ABI boundary on CPU: the library loads without a GPU, exports every
+symbol include/kvx.h declares, and validates arguments before touching CUDA."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2502_09334_b200 import _lib, build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "kvx.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(kvx_\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _lib.load()
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for must in ("kvx_quant_pack", "kvx_dequant_scatter_paged", "kvx_enable_peer",
+                 "kvx_copy_peer", "kvx_ipc_get_handle", "kvx_ipc_open", "kvx_stream_signal",
+                 "kvx_stream_wait", "kvx_strerror"):
+        assert must in syms
+
+
+def test_every_declared_symbol_is_exported(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.SO_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (kvx_\w+)", out))
+    missing = set(declared_symbols()) - exported
+    assert not missing, missing
+    assert set(_lib.SIGNATURES) == set(declared_symbols())
+
+
+def test_sm100a_cubin_embedded():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.SO_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_strerror(lib):
+    assert lib.kvx_version() >= 100
+    assert _lib.strerror(0) == "ok"
+    assert "invalid" in _lib.strerror(_lib.KVX_ERR_INVALID_ARG)
+    assert "peer" in _lib.strerror(_lib.KVX_ERR_NO_PATH)
+
+
+def test_packed_sizes(lib):
+    c, s, z = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    rows = 32 * 2 * 512 * 32  # cfg1 rows
+    assert lib.kvx_packed_sizes(rows, 128, 128, 4, ctypes.byref(c), ctypes.byref(s), ctypes.byref(z)) == 0
+    assert c.value == 67_108_864 and s.value == z.value == rows * 2
+    assert c.value + s.value + z.value == 71_303_168  # SURVEY 8(d) cfg1 packed bytes
+    assert lib.kvx_packed_sizes(rows, 128, 128, 16, ctypes.byref(c), ctypes.byref(s), ctypes.byref(z)) == 0
+    assert c.value == 268_435_456 and s.value == 0
+
+
+@pytest.mark.parametrize("bits,group,head_dim", [(5, 128, 128), (4, 96, 128), (4, 128, 64),
+                                                 (4, 64, 100), (3, 32, 128)])
+def test_invalid_format_rejected_before_cuda(lib, bits, group, head_dim):
+    rc = lib.kvx_quant_pack(16, 16, 0, None, 1, 1, 1, head_dim, group, bits, 16, 16, 16, 0, None)
+    assert rc == _lib.KVX_ERR_INVALID_ARG
+    rc = lib.kvx_dequant_scatter_paged(16, 16, 16, 0, None, 1, 1, 1, head_dim, group, bits, 16, 16,
+                                       0, None)
+    assert rc == _lib.KVX_ERR_INVALID_ARG
+    with pytest.raises(ValueError):
+        _lib.check(rc)
+
+
+def test_misaligned_pointers_rejected(lib):
+    rc = lib.kvx_quant_pack(8, 16, 0, None, 1, 1, 1, 128, 128, 4, 16, 16, 16, 0, None)
+    assert rc == _lib.KVX_ERR_INVALID_ARG
+
+
+def test_empty_is_a_noop(lib):
+    assert lib.kvx_quant_pack(None, None, 0, None, 0, 0, 1, 128, 128, 4, None, None, None, 0,
+                              None) == 0
+    assert lib.kvx_dequant_scatter_paged(None, None, None, 0, None, 4, 0, 8, 128, 128, 4, None,
+                                         None, 0, None) == 0
+
+
+def test_no_gpu_reports_zero_devices(lib):
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU host")
+    n = ctypes.c_int(-1)
+    assert lib.kvx_device_count(ctypes.byref(n)) == 0 and n.value == 0
+
+
+def test_no_cpu_fallback(monkeypatch, tmp_path):
+    """A missing extension must fail loudly, never fall back to the oracle."""
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(ImportError):
+        _lib.load(str(tmp_path / "missing.so"))
+    import paper_2502_09334_b200.datapath as dp
+    src = open(dp.__file__).read()
+    assert "oracle" not in src.replace("no CPU path", "")
