@@ -48,7 +48,8 @@
  *    bits == 16 is passthrough: codes are the raw fp16 rows, no scale/zero.
  *  - Arithmetic (bit-exact vs oracle/):
  *      z = f16(min + 0), s = f16((max - min)/(2^bits-1) + 0)  [IEEE fp32]
- *      q = s == 0 ? 0 : min(rint_even((x - z) * rcp_rn(s)), 2^bits-1)
+ *      q = s == 0 ? 0 : min(rint_even(RN32(x - z) * rcp_rn(s)), 2^bits-1)
+ *          (the product is NOT rounded to fp32: one rounding to integer)
  *      x_hat = f16_rn(min(q*s + z, 65504))  (one rounding: fp16 FMA)
  */
 #ifndef KVX_H_

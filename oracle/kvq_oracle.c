@@ -8,7 +8,8 @@
  *
  *   group  = G contiguous elements of one (layer, K|V, token, head) row
  *   zero16 = f16(mn + 0.0f); scale16 = f16((mx - mn) / (2^bits-1) + 0.0f)
- *   q      = s == 0 ? 0 : clamp(rint_even((x - z) * (1.0f / s)), 0, 2^bits-1)
+ *   q      = s == 0 ? 0 : min(rint_even(RN32(x - z) * RN32(1/s)), 2^bits-1)
+ *            (product exact, one rounding: the GPU's fused FFMA(t, inv, 2^23))
  *   x_hat  = f16_rn(min(q * s + z, 65504))  (exact in double, one rounding)
  *
  * Build (oracle/Makefile): gcc -O2 -fopenmp -ffp-contract=off -fno-fast-math
@@ -80,10 +81,10 @@ int kvq_quant_pack(const uint16_t* src, int64_t rows, int head_dim, int group, i
         int e = g * group + i;
         int q = 0;
         if (s != 0.0f) {
-          volatile float t = h2f(x[e]) - z;
-          float u = t * inv;
-          float rq = nearbyintf(u); /* default mode: half-to-even */
-          rq = rq < 0.0f ? 0.0f : (rq > (float)qmax ? (float)qmax : rq);
+          volatile float t = h2f(x[e]) - z;          /* RN32(x - z) */
+          double u = (double)t * (double)inv;         /* exact product */
+          double rq = nearbyint(u);                   /* one rounding, half-to-even */
+          rq = rq < 0.0 ? 0.0 : (rq > (double)qmax ? (double)qmax : rq);
           q = (int)rq;
         }
         out[e / per] |= (uint8_t)(q << ((e % per) * bits));

@@ -97,12 +97,31 @@ int make_geo(kvx::Geo& g, const void* k, const void* v, int64_t layer_stride, co
 
 constexpr int kUnroll = 4;
 
+kvx::FastDiv make_fastdiv(uint32_t d) {
+  kvx::FastDiv f;
+  f.d = d ? d : 1;
+  uint32_t s = 0;
+  while ((uint64_t(1) << s) < f.d) ++s;
+  f.s = s;
+  f.m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << s) - f.d)) / f.d + 1);
+  return f;
+}
+
 template <int BITS, int G>
 cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero, cudaStream_t s) {
-  auto k = kvx::quant_pack_kernel<BITS, G, kUnroll>;
-  k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, static_cast<uint8_t*>(codes),
-                                                      static_cast<__half*>(scale),
-                                                      static_cast<__half*>(zero));
+  kvx::ItemGeo ig;
+  ig.cpr = g.row_elems / 32;
+  const uint32_t ipr = uint32_t((ig.cpr + 31) / 32);
+  const int64_t n_items = g.n_token_rows * ipr;
+  if (n_items >= (int64_t(1) << 31) || g.n_tokens >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  ig.ipr = make_fastdiv(ipr);
+  ig.tokens = make_fastdiv(uint32_t(g.n_tokens));
+  ig.n_items = uint32_t(n_items);
+  auto k = kvx::quant_pack_kernel<BITS, G>;
+  // one warp per item at most; the grid is capped at the resident CTA count
+  k<<<grid_for(k, n_items), kThreads, 0, s>>>(g, ig, static_cast<uint8_t*>(codes),
+                                              static_cast<__half*>(scale),
+                                              static_cast<__half*>(zero));
   return cudaGetLastError();
 }
 
@@ -215,8 +234,11 @@ int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_strid
     k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, static_cast<uint8_t*>(codes));
     return cudaGetLastError();
   }
-  if (!codes || !scale || !zero || !aligned(codes, bits) || !aligned(scale, 2) || !aligned(zero, 2))
+  if (!codes || !scale || !zero || !aligned(codes, 8 * bits) || !aligned(scale, 2) ||
+      !aligned(zero, 2))
     return KVX_ERR_INVALID_ARG;
+  if (k_src && (!aligned(k_src, 32) || !aligned(v_src, 32) || (src_layer_stride * 2) % 32))
+    return KVX_ERR_INVALID_ARG;  // 256-bit loads
   switch (bits) {
     case 2: return dispatch_quant<2>(group, g, codes, scale, zero, s);
     case 8: return dispatch_quant<8>(group, g, codes, scale, zero, s);

@@ -14,7 +14,7 @@
 //
 // Format (bit-exact with oracle/, see include/kvx.h):
 //   z = f16(min + 0); s = f16((max - min)/(2^b - 1) + 0)   [IEEE fp32]
-//   q = s == 0 ? 0 : min(rint_even((x - z) * rcp_rn(s)), 2^b - 1)
+//   q = s == 0 ? 0 : min(rint_even(RN32(x - z) * rcp_rn(s)), 2^b - 1)  [product exact]
 //   x_hat = f16_rn(min(q*s + z, 65504))     [single-rounding fp16 FMA]
 #pragma once
 
@@ -189,66 +189,238 @@ __device__ __forceinline__ void split_tr(const Geo& g, int64_t tr, int64_t& lk, 
 
 // ---------------------------------------------------------------------------
 // K1: quantise + pack.  codes/scale/zero may be peer (NVLink push) pointers.
+//
+// Lane owns a 32-element chunk (64 B = two 256-bit LDG.E.256 loads); a group
+// of G elements is G/32 consecutive lanes (4 at G=128), so per-group scalar
+// work (one IEEE divide, one IEEE reciprocal) is amortised over 32 elements
+// and the min/max reduction needs at most two shuffles.  Per element the
+// fast path is FHADD (f16 - f32 -> f32, the exact-input subtraction), half an
+// FFMA2 (t*inv + 2^23: fused multiply + round-half-even), and ~0.9 integer
+// ops of nibble packing (LEA/PRMT on the raw float bits).  Work items are
+// (token row, 32-chunk block); each warp software-pipelines its items
+// (loads of item i+1 in flight while item i is computed).
 // ---------------------------------------------------------------------------
-template <int BITS, int G, int UNROLL>
-__global__ void __launch_bounds__(256) quant_pack_kernel(Geo g, uint8_t* __restrict__ codes,
+struct FastDiv {  // n / d for n < 2^31 via mul-hi (host-precomputed magic)
+  uint32_t d, m, s;
+};
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return (__umulhi(n, f.m) + n) >> f.s;
+}
+
+struct ItemGeo {
+  FastDiv ipr;      // items (32-chunk blocks) per token row
+  FastDiv tokens;   // n_tokens
+  int cpr;          // 32-element chunks per token row
+  uint32_t n_items;
+};
+
+__device__ __forceinline__ void ld256(const void* p, uint32_t (&r)[8]) {
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "l"(p));
+}
+
+// x(f16, low or high half of h2) - z(f32) -> f32, one FHADD, exact inputs, RN.
+__device__ __forceinline__ float sub_lo(uint32_t h2, float z) {
+  float r;
+  asm("{.reg .f16 l, h; mov.b32 {l, h}, %1; sub.rn.f32.f16 %0, l, %2;}" : "=f"(r) : "r"(h2), "f"(z));
+  return r;
+}
+__device__ __forceinline__ float sub_hi(uint32_t h2, float z) {
+  float r;
+  asm("{.reg .f16 l, h; mov.b32 {l, h}, %1; sub.rn.f32.f16 %0, h, %2;}" : "=f"(r) : "r"(h2), "f"(z));
+  return r;
+}
+
+// (a, b) * inv + 2^23 in one FFMA2; returns the raw bits of both results.
+__device__ __forceinline__ void fma_magic2(float a, float b, float inv, uint32_t& ra,
+                                           uint32_t& rb) {
+  unsigned long long x, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a), "f"(b));
+  asm("{.reg .b64 iv, mg; mov.b64 iv, {%2, %2}; mov.b64 mg, {%3, %3};"
+      " fma.rn.f32x2 %0, %1, iv, mg;}"
+      : "=l"(r) : "l"(x), "f"(inv), "f"(8388608.0f));
+  ra = uint32_t(r);
+  rb = uint32_t(r >> 32);
+}
+
+__device__ __forceinline__ uint32_t lea4(uint32_t hi, uint32_t lo) { return (hi << 4) + lo; }
+__device__ __forceinline__ uint32_t lea2(uint32_t hi, uint32_t lo) { return (hi << 2) + lo; }
+
+// Gather the low bytes of 4 words into one word: [a0, b0, c0, d0].
+__device__ __forceinline__ uint32_t bytes4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return prmt(prmt(a, b, 0x0040u), prmt(c, d, 0x0040u), 0x5410u);
+}
+
+template <int BITS>
+struct Chunk32 {  // packed codes of 32 elements
+  static constexpr int WORDS = BITS;  // 32*BITS/32
+  uint32_t w[WORDS];
+};
+
+// q bits (raw float bits with q in the low byte) of 32 elements -> packed codes.
+template <int BITS>
+__device__ __forceinline__ Chunk32<BITS> pack32(const uint32_t (&b)[32]) {
+  Chunk32<BITS> out;
+  if constexpr (BITS == 4) {
+    uint32_t p[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) p[i] = lea4(b[2 * i + 1], b[2 * i]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out.w[k] = bytes4(p[4 * k], p[4 * k + 1], p[4 * k + 2], p[4 * k + 3]);
+  } else if constexpr (BITS == 8) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) out.w[k] = bytes4(b[4 * k], b[4 * k + 1], b[4 * k + 2], b[4 * k + 3]);
+  } else {
+    uint32_t p[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      p[i] = lea4(lea2(b[4 * i + 3], b[4 * i + 2]), lea2(b[4 * i + 1], b[4 * i]));
+#pragma unroll
+    for (int k = 0; k < 2; ++k) out.w[k] = bytes4(p[4 * k], p[4 * k + 1], p[4 * k + 2], p[4 * k + 3]);
+  }
+  return out;
+}
+
+template <int BITS>
+__device__ __forceinline__ void store_chunk(void* dst, const Chunk32<BITS>& c) {
+  if constexpr (BITS == 4) {
+    asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(c.w[0]), "r"(c.w[1]),
+                 "r"(c.w[2]), "r"(c.w[3]) : "memory");
+  } else if constexpr (BITS == 8) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(c.w[0]),
+                 "r"(c.w[1]), "r"(c.w[2]), "r"(c.w[3]), "r"(c.w[4]), "r"(c.w[5]), "r"(c.w[6]),
+                 "r"(c.w[7]) : "memory");
+  } else {
+    asm volatile("st.global.v2.b32 [%0], {%1,%2};" ::"l"(dst), "r"(c.w[0]), "r"(c.w[1]) : "memory");
+  }
+}
+
+struct K1Item {
+  const char* src;   // this lane's 64 source bytes (valid iff active)
+  char* codes;       // this lane's code bytes
+  __half* scale;     // group scale slot (this lane's group)
+  __half* zero;
+  bool active;
+};
+
+template <int BITS, int G>
+__device__ __forceinline__ K1Item k1_item(const Geo& g, const ItemGeo& ig, uint32_t item, int lane,
+                                          uint8_t* codes, __half* scale, __half* zero) {
+  constexpr int CB = 32 * BITS / 8;  // code bytes per chunk
+  K1Item it;
+  const uint32_t tr = fdiv(item, ig.ipr);
+  const int c = int(item - tr * ig.ipr.d) * 32 + lane;  // chunk inside the token row
+  const uint32_t lk = fdiv(tr, ig.tokens);
+  const uint32_t t = tr - lk * ig.tokens.d;
+  const uint32_t layer = lk >> 1;
+  const uint32_t lrow = tr - layer * 2 * ig.tokens.d;
+  const int64_t pos = pos_of(g, t);
+  const char* plane = ((lk & 1) ? g.v_plane : g.k_plane) + int64_t(layer) * g.layer_stride_b;
+  it.active = c < ig.cpr;
+  it.src = plane + pos * int64_t(g.row_elems) * 2 + int64_t(c) * 64;
+  it.codes = reinterpret_cast<char*>(codes) + int64_t(layer) * g.codes_ls +
+             (int64_t(lrow) * ig.cpr + c) * CB;
+  const int64_t gi = (int64_t(lrow) * ig.cpr + c) * 32 / G;
+  it.scale = reinterpret_cast<__half*>(reinterpret_cast<char*>(scale) + int64_t(layer) * g.meta_ls) + gi;
+  it.zero = reinterpret_cast<__half*>(reinterpret_cast<char*>(zero) + int64_t(layer) * g.meta_ls) + gi;
+  return it;
+}
+
+template <int BITS, int G>
+__device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)[16], int lane) {
+  constexpr int LPG = G / 32;
+  constexpr float QMAXF = float((1 << BITS) - 1);
+  constexpr uint32_t QMAX = (1u << BITS) - 1u;
+  // group min and -max as one half2 (tree for ILP)
+  __half2 mn[8], mx[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    mn[i] = __hmin2(u32_as_h2(w[2 * i]), u32_as_h2(w[2 * i + 1]));
+    mx[i] = __hmax2(u32_as_h2(w[2 * i]), u32_as_h2(w[2 * i + 1]));
+  }
+#pragma unroll
+  for (int st = 4; st > 0; st >>= 1)
+#pragma unroll
+    for (int i = 0; i < st; ++i) {
+      mn[i] = __hmin2(mn[i], mn[i + st]);
+      mx[i] = __hmax2(mx[i], mx[i + st]);
+    }
+  __half2 r = __halves2half2(__hmin(__low2half(mn[0]), __high2half(mn[0])),
+                             __hneg(__hmax(__low2half(mx[0]), __high2half(mx[0]))));
+#pragma unroll
+  for (int off = LPG / 2; off > 0; off >>= 1)
+    r = __hmin2(r, u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(r), off)));
+  const float fmn = __low2float(r);
+  const float fmx = -__high2float(r);
+  const __half z16 = __float2half_rn(__fadd_rn(fmn, 0.0f));
+  const float sq = __fdiv_rn(__fsub_rn(fmx, fmn), QMAXF);
+  const __half s16 = __float2half_rn(__fadd_rn(sq, 0.0f));
+  const float s = __half2float(s16);
+  const float inv = (s != 0.0f) ? __frcp_rn(s) : 0.0f;
+  const float z = __half2float(z16);
+  // Only a subnormal scale can push rint(t*inv) past 2^bits-1.
+  const bool clamp = __any_sync(0xffffffffu, it.active && s != 0.0f && s < 6.103515625e-05f);
+  uint32_t b[32];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) fma_magic2(sub_lo(w[i], z), sub_hi(w[i], z), inv, b[2 * i], b[2 * i + 1]);
+  if (clamp) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) b[i] = min(b[i] - 0x4B000000u, QMAX);
+  }
+  const Chunk32<BITS> out = pack32<BITS>(b);
+  if (it.active) {
+    store_chunk<BITS>(it.codes, out);
+    if ((lane & (LPG - 1)) == 0) {
+      *it.scale = s16;
+      *it.zero = z16;
+    }
+  }
+}
+
+template <int BITS, int G>
+__global__ void __launch_bounds__(256) quant_pack_kernel(Geo g, ItemGeo ig,
+                                                         uint8_t* __restrict__ codes,
                                                          __half* __restrict__ scale,
                                                          __half* __restrict__ zero) {
-  constexpr int LPG = G / 8;  // lanes per group
-  constexpr float QMAXF = float((1 << BITS) - 1);
-  using CT = typename CodeVec<BITS>::T;
   const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const int groups_per_row = g.row_elems / G;
-
-  for (int64_t tr = warp; tr < g.n_token_rows; tr += n_warps) {
-    int64_t lk, t, layer, lrow;
-    split_tr(g, tr, lk, t, layer, lrow);
-    const int64_t pos = pos_of(g, t);
-    const char* plane = ((lk & 1) ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
-    const U4* src = reinterpret_cast<const U4*>(plane + pos * int64_t(g.row_elems) * 2);
-    CT* dst_codes = reinterpret_cast<CT*>(codes + layer * g.codes_ls) + lrow * g.vecs;
-    __half* dst_scale =
-        reinterpret_cast<__half*>(reinterpret_cast<char*>(scale) + layer * g.meta_ls) +
-        lrow * groups_per_row;
-    __half* dst_zero =
-        reinterpret_cast<__half*>(reinterpret_cast<char*>(zero) + layer * g.meta_ls) +
-        lrow * groups_per_row;
-
-    for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
-      U4 v[UNROLL];
-#pragma unroll
-      for (int k = 0; k < UNROLL; ++k) {
-        const int vi = base + k * 32 + lane;
-        if (vi < g.vecs) v[k] = ld_stream(src + vi);
-        else v[k] = U4{0u, 0u, 0u, 0u};
-      }
-#pragma unroll
-      for (int k = 0; k < UNROLL; ++k) {
-        const int vi = base + k * 32 + lane;
-        __half2 r = minnegmax8(v[k]);
-#pragma unroll
-        for (int off = LPG / 2; off > 0; off >>= 1)
-          r = __hmin2(r, u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(r), off)));
-        const float mn = __low2float(r);
-        const float mx = -__high2float(r);
-        const __half z16 = __float2half_rn(__fadd_rn(mn, 0.0f));
-        const float sq = __fdiv_rn(__fsub_rn(mx, mn), QMAXF);
-        const __half s16 = __float2half_rn(__fadd_rn(sq, 0.0f));
-        const float s = __half2float(s16);
-        const float inv = (s != 0.0f) ? __frcp_rn(s) : 0.0f;
-        const CT c = quant8<BITS>(v[k], __half2float(z16), inv);
-        if (vi < g.vecs) {
-          dst_codes[vi] = c;
-          if ((lane & (LPG - 1)) == 0) {
-            const int gi = vi / LPG;
-            dst_scale[gi] = s16;
-            dst_zero[gi] = z16;
-          }
-        }
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t wa[16], wb[16];
+  uint32_t item = warp;
+  K1Item a, b;
+  if (item < ig.n_items) {
+    a = k1_item<BITS, G>(g, ig, item, lane, codes, scale, zero);
+    if (a.active) {
+      ld256(a.src, *reinterpret_cast<uint32_t(*)[8]>(&wa[0]));
+      ld256(a.src + 32, *reinterpret_cast<uint32_t(*)[8]>(&wa[8]));
+    }
+  }
+  while (item < ig.n_items) {
+    const uint32_t nxt = item + n_warps;
+    if (nxt < ig.n_items) {
+      b = k1_item<BITS, G>(g, ig, nxt, lane, codes, scale, zero);
+      if (b.active) {
+        ld256(b.src, *reinterpret_cast<uint32_t(*)[8]>(&wb[0]));
+        ld256(b.src + 32, *reinterpret_cast<uint32_t(*)[8]>(&wb[8]));
       }
     }
+    k1_process<BITS, G>(a, wa, lane);
+    item = nxt;
+    if (item >= ig.n_items) break;
+    const uint32_t nn = item + n_warps;
+    if (nn < ig.n_items) {
+      a = k1_item<BITS, G>(g, ig, nn, lane, codes, scale, zero);
+      if (a.active) {
+        ld256(a.src, *reinterpret_cast<uint32_t(*)[8]>(&wa[0]));
+        ld256(a.src + 32, *reinterpret_cast<uint32_t(*)[8]>(&wa[8]));
+      }
+    }
+    k1_process<BITS, G>(b, wb, lane);
+    item = nn;
   }
 }
 

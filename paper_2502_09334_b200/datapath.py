@@ -470,8 +470,10 @@ class HostHandoff:
         self.device = torch.device(device)
         self.kv_host, self.kc_host, self.vc_host = kv_host, k_cache_host, v_cache_host
         self.kv = torch.empty(kv_host.shape, dtype=torch.float16, device=self.device)
-        self.kc = torch.empty(k_cache_host.shape, dtype=torch.float16, device=self.device)
-        self.vc = torch.empty(v_cache_host.shape, dtype=torch.float16, device=self.device)
+        # device mirror of the host cache: blocks outside the slot mapping keep
+        # the host's contents (they are copied back unchanged)
+        self.kc = k_cache_host.to(self.device)
+        self.vc = v_cache_host.to(self.device)
         self.slots = slot_mapping.to(self.device)
         self.src = KVPlanes.dense(self.kv)
         self.dst = KVPlanes.paged(self.kc, self.vc, self.slots)
