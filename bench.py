@@ -318,7 +318,8 @@ def main():
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--bits", type=int, default=4)
     ap.add_argument("--group", type=int, default=128)
-    ap.add_argument("--chunks", type=int, default=1)
+    ap.add_argument("--chunks", type=int, default=None,
+                    help="layer chunks per hand-off (default: 1 at N=1, 8 per pair at N>1)")
     ap.add_argument("--mode", default="pull", choices=["pull", "push", "copy", "nccl"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
@@ -345,6 +346,7 @@ def main():
         transport.bench_pairs(args, torch, rank, world, emit=emit)
         return
     torch.cuda.set_device(0)
+    args.chunks = args.chunks or 1
     r = run_local(args, torch)
     emit(args, r, world)
 

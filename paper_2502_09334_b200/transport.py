@@ -1,0 +1,416 @@
+"""Multi-process (one process per GPU) prefill -> decode hand-off over NVLink.
+
+The reference models each hand-off as an independent point-to-point delay over
+the bottleneck link between the last prefill stage and the first decode stage
+(``/root/reference/pkg/src/hetplan/simulate.py:221-235``,
+``costs.py:51-65,83-103``); the paper's system pre-builds a pool of
+communication groups and has decode replicas pull KV from queues kept in the
+prefill replicas' GPU memory (``PAPER.md:859``).  Here:
+
+* pairing: ranks [0, N/2) prefill, [N/2, N) decode, pair
+  i -> i + N/2 (1P1D / 2P2D / 4P4D).  Pairs are independent: no collective on
+  the data path, NVSwitch gives every pair a full link.
+* the channel pool: at setup every rank exports its staging buffers and its
+  doorbell flags with CUDA IPC and maps its partner's (the analogue of the
+  paper's pre-built group pool); nothing is allocated per hand-off.
+* transports (``mode``):
+    "pull" - K1 on P into P's HBM; D's K3 reads the payload over NVLink (peer
+             loads) and dequantises straight into D's paged cache.  The
+             payload crosses NVLink once and D's HBM sees only the fp16 writes.
+    "push" - P's K1 stores the payload straight into D's landing buffer over
+             NVLink (fused quantise + transfer); K3 on D reads it locally.
+    "copy" - K1 local, copy-engine cudaMemcpyAsync into D's landing buffer,
+             K3 local (the non-fused baseline).
+    "nccl" - K1 local, torch.distributed (NCCL) send/recv per chunk, K3 local.
+* chunk pipeline: layers are cut into chunks; per chunk P signals a 32-bit
+  doorbell in D's memory (cuStreamWriteValue32, fenced) and D's stream waits on
+  it in the front-end (cuStreamWaitValue32 GEQ epoch), so K1 of chunk c+1, the
+  link and K3 of chunk c overlap.  D acks each chunk back into P's memory so
+  the next hand-off never overwrites a chunk still being read.  No spinning
+  kernels, no host round trips per chunk.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .costs import DEFAULT_GROUP, KvPrecision
+from .datapath import (KVPlanes, PackedKV, PackedLayout, _bits_of, _round_up, _stream_ptr,
+                       dequant_scatter_layers, layer_chunks, quant_pack_layers)
+
+MODES = ("pull", "push", "copy", "nccl")
+FLAG_SLOTS = 256  # doorbells per direction (>= chunks)
+
+
+# ---------------------------------------------------------------------------
+# Host-side plan (pure Python: unit-tested with gloo on CPU)
+# ---------------------------------------------------------------------------
+
+def pairing(world: int):
+    """[(prefill_rank, decode_rank)] for N = 2, 4, 8 ... (pair i -> i + N/2)."""
+    if world < 2 or world % 2:
+        raise ValueError("the hand-off pairs prefill and decode ranks: world must be even >= 2")
+    h = world // 2
+    return [(i, i + h) for i in range(h)]
+
+
+def role_of(rank: int, world: int):
+    """('prefill'|'decode', pair index, partner rank)."""
+    for i, (p, d) in enumerate(pairing(world)):
+        if rank == p:
+            return "prefill", i, d
+        if rank == d:
+            return "decode", i, p
+    raise ValueError(f"rank {rank} outside world {world}")
+
+
+@dataclass(frozen=True)
+class ChannelSpec:
+    """What both ends of a pair must agree on (capacity, format, chunking)."""
+
+    n_layers: int
+    max_tokens: int
+    n_heads: int
+    head_dim: int
+    bits: int = 4
+    group: int = DEFAULT_GROUP
+    n_chunks: int = 8
+    mode: str = "pull"
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}")
+        KvPrecision(self.bits)
+        if self.n_chunks < 1 or self.n_chunks > FLAG_SLOTS:
+            raise ValueError("n_chunks out of range")
+
+    def layout(self, n_tokens: int) -> PackedLayout:
+        if not 0 <= n_tokens <= self.max_tokens:
+            raise ValueError("n_tokens exceeds the channel capacity")
+        return PackedLayout(self.n_layers, n_tokens, self.n_heads, self.head_dim, self.bits,
+                            self.group)
+
+    @property
+    def capacity_bytes(self) -> int:
+        return self.layout(self.max_tokens).nbytes + 256
+
+    def chunks(self):
+        return layer_chunks(self.n_layers, self.n_chunks)
+
+
+def exchange(obj, group=None):
+    """all_gather_object over the control group (gloo)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Device buffers exported / imported with CUDA IPC
+# ---------------------------------------------------------------------------
+
+class IpcBuffer:
+    """A kvx_malloc'd device buffer that can be mapped by another process."""
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        _lib.call("kvx_malloc", ctypes.byref(p), int(nbytes))
+        self.ptr = int(p.value)
+        self.nbytes = int(nbytes)
+        _lib.call("kvx_memset_async", self.ptr, 0, self.nbytes, None)
+        torch.cuda.synchronize()
+
+    def handle(self) -> bytes:
+        n = _lib.load().kvx_ipc_handle_size()
+        buf = ctypes.create_string_buffer(n)
+        _lib.call("kvx_ipc_get_handle", self.ptr, buf)
+        return buf.raw
+
+    def free(self):
+        if self.ptr:
+            _lib.call("kvx_free", self.ptr)
+            self.ptr = 0
+
+
+def ipc_open(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(handle, len(handle))
+    _lib.call("kvx_ipc_open", buf, ctypes.byref(p))
+    return int(p.value)
+
+
+def memops_supported() -> bool:
+    v = ctypes.c_int(0)
+    _lib.call("kvx_stream_memops_supported", ctypes.byref(v))
+    return bool(v.value)
+
+
+def signal(flag_addr: int, value: int, stream) -> None:
+    _lib.call("kvx_stream_signal", flag_addr, value & 0xFFFFFFFF, _stream_ptr(stream))
+
+
+def wait(flag_addr: int, value: int, stream) -> None:
+    _lib.call("kvx_stream_wait", flag_addr, value & 0xFFFFFFFF, _stream_ptr(stream))
+
+
+# ---------------------------------------------------------------------------
+# The channel
+# ---------------------------------------------------------------------------
+
+class PairChannel:
+    """One end of a prefill -> decode pair (construct on every rank, collectively).
+
+    prefill end: ``send(src_planes, n_tokens)``; decode end:
+    ``recv(dst_planes, n_tokens)``.  Both enqueue asynchronously on the
+    channel's stream, ordered after the caller's current stream, and make the
+    caller's current stream wait for completion (like a collective's work).
+    """
+
+    def __init__(self, spec: ChannelSpec, rank: int, world: int, control_group=None,
+                 data_group=None):
+        self.spec = spec
+        self.rank, self.world = rank, world
+        self.role, self.pair, self.peer = role_of(rank, world)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.stream = torch.cuda.Stream(self.device)
+        self.data_group = data_group
+        self.epoch = 0
+        self._prev_ranges = None
+        self.chunks = spec.chunks()
+        mode = spec.mode
+        if mode != "nccl" and not memops_supported():
+            raise RuntimeError("stream memory operations unavailable: use mode='nccl'")
+        # local buffers: doorbells (written by the partner) + payload staging
+        self.flags = IpcBuffer(FLAG_SLOTS * 4)
+        stage_here = (self.role == "prefill" and mode in ("pull", "nccl")) or (
+            self.role == "decode" and mode in ("push", "copy", "nccl"))
+        self.local_payload = None
+        if stage_here:
+            if mode == "nccl":  # NCCL needs a torch tensor
+                t = torch.empty(spec.capacity_bytes, dtype=torch.uint8, device=self.device)
+                self.local_payload = (t, _round_up(t.data_ptr()))
+            else:
+                b = IpcBuffer(spec.capacity_bytes)
+                self.local_payload = (b, _round_up(b.ptr))
+        mine = {"flags": self.flags.handle()}
+        if self.local_payload is not None and mode != "nccl":
+            mine["payload"] = self.local_payload[0].handle()
+            mine["payload_off"] = self.local_payload[1] - self.local_payload[0].ptr
+        allv = exchange(mine, control_group)
+        theirs = allv[self.peer]
+        self.peer_flags = ipc_open(theirs["flags"])
+        self.peer_payload = None
+        self._peer_payload_map = 0
+        if "payload" in theirs:
+            self._peer_payload_map = ipc_open(theirs["payload"])
+            self.peer_payload = self._peer_payload_map + theirs["payload_off"]
+        # where K1 writes / K3 reads
+        if self.role == "prefill":
+            self.k1_target = self.peer_payload if mode == "push" else self.local_payload[1]
+        else:
+            self.k3_source = self.peer_payload if mode == "pull" else self.local_payload[1]
+
+    # flags: slot c = "chunk c of epoch e ready" (written by P into D's flags);
+    #        slot FLAG_SLOTS//2 + c = "chunk c of epoch e consumed" (D -> P)
+    def _ready(self, base: int, c: int) -> int:
+        return base + 4 * c
+
+    def _ack(self, base: int, c: int) -> int:
+        return base + 4 * (FLAG_SLOTS // 2 + c)
+
+    def send(self, src: KVPlanes, n_tokens: int, timing: list | None = None) -> None:
+        assert self.role == "prefill"
+        lay = self.spec.layout(n_tokens)
+        self.epoch += 1
+        e = self.epoch
+        mode = self.spec.mode
+        s = self.stream
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        payload = PackedKV(lay, self.k1_target, self.device)
+        ranges = [(l0 * lay.layer_stride, l1 * lay.layer_stride) for l0, l1 in self.chunks]
+        prev = self._prev_ranges
+        for c, (l0, l1) in enumerate(self.chunks):
+            if mode != "nccl" and prev:
+                # never overwrite bytes the decode side may still be reading:
+                # wait for the ack of the last previous-epoch chunk that overlaps
+                # (D acks in chunk order, so that ack covers all earlier ones)
+                last = max(i for i, (a, _) in enumerate(prev) if a < ranges[c][1])
+                wait(self._ack(self.flags.ptr, last), e - 1, s)
+            ev = _kernel_events(timing, s, "k1")
+            quant_pack_layers(src, payload, l0, l1, s)
+            _kernel_events_end(ev, s)
+            addr, nbytes = payload.byte_range(l0, l1)
+            if mode == "copy":
+                dst = self.peer_payload + (addr - self.k1_target)
+                with torch.cuda.stream(s):
+                    _lib.call("kvx_copy_peer", dst, self.device.index, addr, self.device.index,
+                              nbytes, _stream_ptr(s))
+            if mode == "nccl":
+                import torch.distributed as dist
+                t = self.local_payload[0]
+                off = addr - t.data_ptr()
+                with torch.cuda.stream(s):
+                    dist.send(t[off:off + nbytes], self.peer, group=self.data_group)
+            else:
+                signal(self._ready(self.peer_flags, c), e, s)
+        self._prev_ranges = ranges
+        torch.cuda.current_stream(self.device).wait_stream(s)
+
+    def recv(self, dst: KVPlanes, n_tokens: int, timing: list | None = None) -> None:
+        assert self.role == "decode"
+        lay = self.spec.layout(n_tokens)
+        self.epoch += 1
+        e = self.epoch
+        mode = self.spec.mode
+        s = self.stream
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        payload = PackedKV(lay, self.k3_source, self.device)
+        for c, (l0, l1) in enumerate(self.chunks):
+            if mode == "nccl":
+                import torch.distributed as dist
+                t = self.local_payload[0]
+                addr, nbytes = payload.byte_range(l0, l1)
+                off = addr - t.data_ptr()
+                with torch.cuda.stream(s):
+                    dist.recv(t[off:off + nbytes], self.peer, group=self.data_group)
+            else:
+                wait(self._ready(self.flags.ptr, c), e, s)
+            ev = _kernel_events(timing, s, "k3")
+            dequant_scatter_layers(payload, dst, l0, l1, s)
+            _kernel_events_end(ev, s)
+            if mode != "nccl":
+                signal(self._ack(self.peer_flags, c), e, s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+
+    def close(self):
+        """Unmap the partner's buffers and free ours (call after a barrier)."""
+        torch.cuda.synchronize(self.device)
+        if self.peer_flags:
+            _lib.call("kvx_ipc_close", self.peer_flags)
+            self.peer_flags = 0
+        if self._peer_payload_map:
+            _lib.call("kvx_ipc_close", self._peer_payload_map)
+            self._peer_payload_map = 0
+            self.peer_payload = None
+        if self.local_payload is not None and isinstance(self.local_payload[0], IpcBuffer):
+            self.local_payload[0].free()
+        self.local_payload = None
+        self.flags.free()
+
+
+def _kernel_events(timing, stream, name):
+    if timing is None:
+        return None
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    return (timing, name, a, b)
+
+
+def _kernel_events_end(ev, stream):
+    if ev is None:
+        return
+    timing, name, a, b = ev
+    b.record(stream)
+    timing.append((name, a, b))
+
+
+# ---------------------------------------------------------------------------
+# bench.py N > 1
+# ---------------------------------------------------------------------------
+
+def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
+    """Weak-scaling pair benchmark: every pair hands off the same workload."""
+    import json
+    import torch.distributed as dist
+
+    import bench as B
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    ctrl = dist.new_group(backend="gloo")
+    wl = args.workload or B.default_pair_workload(world)
+    L, H, D, b, s = B.WORKLOADS[wl]
+    T = b * s
+    mode = args.mode
+    n_chunks = args.chunks or 8
+    spec = ChannelSpec(L, T, H, D, args.bits, args.group, n_chunks, mode)
+    ch = PairChannel(spec, rank, world, control_group=ctrl)
+    lay = spec.layout(T)
+    if ch.role == "prefill":
+        kv = B.synthetic_kv_device(torch, L, T, H, D, dev, seed=ch.pair)
+        planes = KVPlanes.dense(kv)
+        step = lambda timing=None: ch.send(planes, T, timing)  # noqa: E731
+    else:
+        slots, nb = B.paged_slots(torch, T, dev, seed=ch.pair)
+        kc = torch.zeros((L, nb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
+        vc = torch.zeros_like(kc)
+        planes = KVPlanes.paged(kc, vc, slots)
+        step = lambda timing=None: ch.recv(planes, T, timing)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    timing = []
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with B.ClockSampler(local) as clk:
+        t0.record()
+        for _ in range(args.steps):
+            step(timing)
+        t1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    kern = {}
+    for name, a, b_ in timing:
+        kern[name] = kern.get(name, 0.0) + a.elapsed_time(b_) / args.steps
+    stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0)], dtype=torch.float64,
+                         device=dev)
+    gathered = [torch.zeros_like(stats) for _ in range(world)]
+    dist.all_gather(gathered, stats)
+    clocks = exchange(clk.summary(), ctrl)
+    if rank == 0:
+        g = torch.stack(gathered).cpu()
+        ms_max = float(g[:, 0].max())
+        k1 = float(g[:, 1].max())
+        k3 = float(g[:, 2].max())
+        pairs = world // 2
+        fp16 = lay.fp16_bytes
+        value = pairs * fp16 / (ms_max * 1e-3) / 1e9
+        wire = lay.wire_bytes
+        link_gbs = wire / (ms_max * 1e-3) / 1e9  # per pair
+        hbm, peak_kind = B.peaks()
+        k3_link = wire / (k3 * 1e-3) / 1e9 if k3 > 0 else None
+        sm = [c["sm_mhz"] for c in clocks if c.get("sm_mhz")]
+        reasons = sorted({r for c in clocks for r in c.get("reasons", [])})
+        r = dict(
+            value=value, ms=ms_max, workload=wl, fp16_bytes=fp16 * pairs, wire_bytes=wire * pairs,
+            launches=2 * len(spec.chunks()) * pairs * args.steps,
+            clocks={"sm_mhz": min(sm) if sm else None,
+                    "sm_max_mhz": max((c.get("sm_max_mhz") or 0) for c in clocks) or None,
+                    "reasons": reasons, "per_rank_median_sm_mhz": sm},
+            e2e=None, cpu=None,
+            roofline={"bound": "nvlink", "kernel": "dequant_scatter_paged (pull over NVLink)"
+                      if mode == "pull" else f"hand-off ({mode})",
+                      "achieved": round(link_gbs, 1), "peak": B.NVLINK_GBS,
+                      "peak_kind": "measured peer copy, B200_PROFILING.md (900 nominal)",
+                      "unit": "GB/s", "frac": round(link_gbs / B.NVLINK_GBS, 4), "traffic": None,
+                      "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
+                      "k3_link_gbs": round(k3_link, 1) if k3_link else None,
+                      "frac_of_nominal_900": round(link_gbs / 900.0, 4),
+                      "hbm_peak": hbm},
+            extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
+                   "pairing": pairing(world), "parallelism": f"{pairs}P{pairs}D"},
+        )
+        emit(args, r, world)
+    dist.barrier()
+    ch.close()
+    dist.destroy_process_group()

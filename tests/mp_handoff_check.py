@@ -1,0 +1,70 @@
+"""torchrun worker for tests/test_gpu_multiproc.py: every transport mode over
+real IPC/NVLink between one process per GPU, checked bit-exactly against the
+oracle on the decode side.  Exits non-zero on any mismatch."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import kvq_oracle as O  # noqa: E402
+from paper_2502_09334_b200.datapath import KVPlanes  # noqa: E402
+from paper_2502_09334_b200.transport import ChannelSpec, PairChannel  # noqa: E402
+
+
+def main():
+    modes = sys.argv[1].split(",") if len(sys.argv) > 1 else ["pull", "push", "copy", "nccl"]
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    ctrl = dist.new_group(backend="gloo")
+    L, Tmax, H, D, bs = 6, 200, 8, 128, 16
+    failures = 0
+    for mode in modes:
+        for bits in (4, 8, 16):
+            spec = ChannelSpec(L, Tmax, H, D, bits, 64 if bits != 16 else 128, 3, mode)
+            ch = PairChannel(spec, rank, world, control_group=ctrl)
+            nb = Tmax // bs + 4
+            if ch.role == "decode":
+                kc = torch.zeros((L, nb, bs, H, D), dtype=torch.float16, device=dev)
+                vc = torch.zeros_like(kc)
+            for epoch, T in enumerate((Tmax, 77, 130)):  # several hand-offs, varying length
+                seed = 1000 * ch.pair + 10 * epoch + bits
+                if ch.role == "prefill":
+                    kv = torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=seed)).to(dev)
+                    ch.send(KVPlanes.dense(kv), T)
+                    torch.cuda.synchronize()
+                else:
+                    slots_np = O.synthetic_slots(T, bs, nb, seed=seed)
+                    kc.zero_(); vc.zero_()
+                    ch.recv(KVPlanes.paged(kc, vc, torch.from_numpy(slots_np).to(dev)), T)
+                    torch.cuda.synchronize()
+                    okc = np.zeros((L, nb, bs, H, D), np.float16); ovc = okc.copy()
+                    kv_np = O.synthetic_kv(L, T, H, D, seed=seed)
+                    g = spec.group
+                    c, s, z = O.quant_pack(kv_np.reshape(-1, D), bits, g)
+                    O.scatter_paged(O.unpack_dequant(c, s, z, bits, g, D).reshape(L, 2, T, H, D),
+                                    slots_np, okc, ovc)
+                    ok = (np.array_equal(kc.cpu().numpy().view(np.uint16), okc.view(np.uint16))
+                          and np.array_equal(vc.cpu().numpy().view(np.uint16), ovc.view(np.uint16)))
+                    if not ok:
+                        failures += 1
+                        print(f"MISMATCH rank={rank} mode={mode} bits={bits} T={T}", flush=True)
+            dist.barrier()
+            ch.close()
+    f = torch.tensor([failures], device=dev)
+    dist.all_reduce(f)
+    if rank == 0:
+        print(f"mp_handoff_check modes={modes} world={world} failures={int(f.item())}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if f.item() else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,23 @@
+"""One process per GPU over NVLink (torchrun): every transport mode bit-exact
+vs the oracle on the decode side.  Needs >= 2 GPUs (gpurun --gpus 2/4)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_modes_over_ipc(cuda, nproc):
+    if cuda.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29533",
+           os.path.join(HERE, "mp_handoff_check.py"), "pull,push,copy,nccl"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "failures=0" in r.stdout

@@ -1,0 +1,87 @@
+"""Host-side logic of the multi-process hand-off on CPU (gloo, world size 2/4):
+pairing, channel specs both ends must agree on, and the IPC handle exchange
+protocol (the kvx IPC calls themselves need GPUs and run in the -m gpu tests)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2502_09334_b200.transport import ChannelSpec, exchange, pairing, role_of
+
+
+def test_pairing_matches_survey_8e():
+    assert pairing(2) == [(0, 1)]
+    assert pairing(4) == [(0, 2), (1, 3)]
+    assert pairing(8) == [(0, 4), (1, 5), (2, 6), (3, 7)]
+    for bad in (0, 1, 3):
+        with pytest.raises(ValueError):
+            pairing(bad)
+
+
+def test_roles_cover_every_rank_once():
+    for world in (2, 4, 8):
+        seen = {}
+        for r in range(world):
+            role, pair, peer = role_of(r, world)
+            assert role_of(peer, world)[2] == r and role_of(peer, world)[1] == pair
+            seen.setdefault(pair, set()).add(role)
+        assert all(v == {"prefill", "decode"} for v in seen.values())
+
+
+def test_channel_spec_layout_and_capacity():
+    spec = ChannelSpec(80, 8192, 8, 128, 4, 128, 8, "pull")
+    lay = spec.layout(8192)
+    assert lay.fp16_bytes == 2_684_354_560  # one 4P4D pair of BASELINE config 4
+    assert lay.wire_bytes == 713_031_680
+    assert spec.capacity_bytes >= lay.nbytes
+    assert len(spec.chunks()) == 8 and spec.chunks()[0] == (0, 10)
+    assert spec.layout(100).nbytes < lay.nbytes
+    with pytest.raises(ValueError):
+        spec.layout(8193)
+    with pytest.raises(ValueError):
+        ChannelSpec(80, 8192, 8, 128, mode="rdma")
+    with pytest.raises(ValueError):
+        ChannelSpec(80, 8192, 8, 128, bits=3)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    role, pair, peer = role_of(rank, world)
+    # each rank publishes fake handles; every rank must receive its partner's
+    mine = {"flags": bytes([rank]) * 64, "rank": rank, "role": role}
+    if role == "prefill":
+        mine["payload"] = bytes([100 + rank]) * 64
+        mine["payload_off"] = 0
+    allv = exchange(mine)
+    theirs = allv[peer]
+    ok = theirs["rank"] == peer and theirs["flags"] == bytes([peer]) * 64
+    ok &= ("payload" in theirs) == (role == "decode")
+    dist.barrier()
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_handle_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res.values()) and len(res) == world
