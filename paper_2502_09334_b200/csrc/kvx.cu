@@ -107,9 +107,9 @@ kvx::FastDiv make_fastdiv(uint32_t d) {
   return f;
 }
 
-template <int BITS, int G>
-cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero, cudaStream_t s) {
-  kvx::ItemGeo ig;
+// Item geometry shared by K1 and K3: one item = one token row's block of up
+// to 32 chunks of 32 elements; one warp per item at a time.
+cudaError_t make_items(const kvx::Geo& g, kvx::ItemGeo& ig) {
   ig.cpr = g.row_elems / 32;
   const uint32_t ipr = uint32_t((ig.cpr + 31) / 32);
   const int64_t n_items = g.n_token_rows * ipr;
@@ -117,21 +117,31 @@ cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero
   ig.ipr = make_fastdiv(ipr);
   ig.tokens = make_fastdiv(uint32_t(g.n_tokens));
   ig.n_items = uint32_t(n_items);
+  return cudaSuccess;
+}
+
+template <int BITS, int G>
+cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero, cudaStream_t s) {
+  kvx::ItemGeo ig;
+  cudaError_t e = make_items(g, ig);
+  if (e != cudaSuccess) return e;
   auto k = kvx::quant_pack_kernel<BITS, G>;
-  // one warp per item at most; the grid is capped at the resident CTA count
-  k<<<grid_for(k, n_items), kThreads, 0, s>>>(g, ig, static_cast<uint8_t*>(codes),
-                                              static_cast<__half*>(scale),
-                                              static_cast<__half*>(zero));
+  k<<<grid_for(k, ig.n_items), kThreads, 0, s>>>(g, ig, static_cast<uint8_t*>(codes),
+                                                 static_cast<__half*>(scale),
+                                                 static_cast<__half*>(zero));
   return cudaGetLastError();
 }
 
 template <int BITS, int G>
 cudaError_t launch_dequant(const kvx::Geo& g, const void* codes, const void* scale,
                            const void* zero, cudaStream_t s) {
-  auto k = kvx::dequant_scatter_kernel<BITS, G, kUnroll>;
-  k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, static_cast<const uint8_t*>(codes),
-                                                      static_cast<const __half*>(scale),
-                                                      static_cast<const __half*>(zero));
+  kvx::ItemGeo ig;
+  cudaError_t e = make_items(g, ig);
+  if (e != cudaSuccess) return e;
+  auto k = kvx::dequant_scatter_kernel<BITS, G>;
+  k<<<grid_for(k, ig.n_items), kThreads, 0, s>>>(g, ig, static_cast<const uint8_t*>(codes),
+                                                 static_cast<const __half*>(scale),
+                                                 static_cast<const __half*>(zero));
   return cudaGetLastError();
 }
 
@@ -265,8 +275,11 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
     k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, static_cast<const uint8_t*>(codes));
     return cudaGetLastError();
   }
-  if (!codes || !scale || !zero || !aligned(codes, bits) || !aligned(scale, 2) || !aligned(zero, 2))
+  if (!codes || !scale || !zero || !aligned(codes, 8 * bits) || !aligned(scale, 2) ||
+      !aligned(zero, 2))
     return KVX_ERR_INVALID_ARG;
+  if (k_cache && (!aligned(k_cache, 32) || !aligned(v_cache, 32) || (dst_layer_stride * 2) % 32))
+    return KVX_ERR_INVALID_ARG;  // 256-bit stores
   switch (bits) {
     case 2: return dispatch_dequant<2>(group, g, codes, scale, zero, s);
     case 8: return dispatch_dequant<8>(group, g, codes, scale, zero, s);

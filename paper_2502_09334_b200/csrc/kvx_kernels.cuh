@@ -77,41 +77,6 @@ struct CodeVec<2> {
   using T = uint16_t;
 };
 
-// Quantise 8 fp32-exact values (given as 4 half2) with (z, inv) and pack.
-template <int BITS>
-__device__ __forceinline__ typename CodeVec<BITS>::T quant8(const U4& v, float z, float inv) {
-  constexpr uint32_t QMAX = (1u << BITS) - 1u;
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  uint32_t q[8];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float2 f = __half22float2(u32_as_h2(w[i]));
-    // t = RN(RN(x - z) * inv); rint_even(t) via the 2^23 magic add (t >= 0).
-    float t0 = __fmul_rn(__fsub_rn(f.x, z), inv);
-    float t1 = __fmul_rn(__fsub_rn(f.y, z), inv);
-    uint32_t m0 = __float_as_uint(__fadd_rn(t0, 8388608.0f)) - 0x4B000000u;
-    uint32_t m1 = __float_as_uint(__fadd_rn(t1, 8388608.0f)) - 0x4B000000u;
-    q[2 * i] = min(m0, QMAX);
-    q[2 * i + 1] = min(m1, QMAX);
-  }
-  if constexpr (BITS == 4) {
-    uint32_t r = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r |= q[i] << (4 * i);
-    return r;
-  } else if constexpr (BITS == 8) {
-    uint2 r;
-    r.x = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
-    r.y = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
-    return r;
-  } else {
-    uint32_t r = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r |= q[i] << (2 * i);
-    return (uint16_t)r;
-  }
-}
-
 // Dequantise 8 codes to 8 fp16 with a single-rounding fp16 FMA.
 template <int BITS>
 __device__ __forceinline__ U4 dequant8(typename CodeVec<BITS>::T c, __half2 s2, __half2 z2) {
@@ -148,16 +113,6 @@ __device__ __forceinline__ U4 dequant8(typename CodeVec<BITS>::T c, __half2 s2, 
     o[i] = h2_as_u32(__hmin2(y, kmax));            // saturate (+inf -> 65504)
   }
   return out;
-}
-
-// min (x) and -max (y) of 8 halves, as one half2 so one shuffle reduces both.
-__device__ __forceinline__ __half2 minnegmax8(const U4& v) {
-  __half2 a = u32_as_h2(v.x), b = u32_as_h2(v.y), c = u32_as_h2(v.z), d = u32_as_h2(v.w);
-  __half2 mn = __hmin2(__hmin2(a, b), __hmin2(c, d));
-  __half2 mx = __hmax2(__hmax2(a, b), __hmax2(c, d));
-  __half lo = __hmin(__low2half(mn), __high2half(mn));
-  __half hi = __hmax(__low2half(mx), __high2half(mx));
-  return __halves2half2(lo, __hneg(hi));
 }
 
 // Token-row geometry shared by both kernels.
@@ -457,51 +412,128 @@ __global__ void __launch_bounds__(256) pack16_kernel(Geo g, uint8_t* __restrict_
 // K3: unpack + dequantise + scatter into the paged cache.  codes/scale/zero
 // may be peer (NVLink pull) pointers.  Token rows with slot < 0 are skipped.
 // ---------------------------------------------------------------------------
-template <int BITS, int G, int UNROLL>
-__global__ void __launch_bounds__(256) dequant_scatter_kernel(Geo g,
+// Lane owns a 32-element chunk: one 16-byte code load (4-bit; 32 B at 8-bit,
+// 8 B at 2-bit) -- wide requests matter when the payload is read over NVLink
+// -- and two 256-bit stores into the paged cache.  Items and software
+// pipelining as in K1.
+struct K3Item {
+  const char* codes;
+  const __half* scale;
+  const __half* zero;
+  char* dst;
+  bool active;
+};
+
+template <int BITS, int G>
+__device__ __forceinline__ K3Item k3_item(const Geo& g, const ItemGeo& ig, uint32_t item, int lane,
+                                          const uint8_t* codes, const __half* scale,
+                                          const __half* zero) {
+  constexpr int CB = 32 * BITS / 8;
+  K3Item it;
+  const uint32_t tr = fdiv(item, ig.ipr);
+  const int c = int(item - tr * ig.ipr.d) * 32 + lane;
+  const uint32_t lk = fdiv(tr, ig.tokens);
+  const uint32_t t = tr - lk * ig.tokens.d;
+  const uint32_t layer = lk >> 1;
+  const uint32_t lrow = tr - layer * 2 * ig.tokens.d;
+  const int64_t pos = pos_of(g, t);
+  char* plane = const_cast<char*>((lk & 1) ? g.v_plane : g.k_plane) + int64_t(layer) * g.layer_stride_b;
+  it.active = (c < ig.cpr) && (pos >= 0);  // pos < 0: padding token, skipped
+  it.dst = plane + pos * int64_t(g.row_elems) * 2 + int64_t(c) * 64;
+  it.codes = reinterpret_cast<const char*>(codes) + int64_t(layer) * g.codes_ls +
+             (int64_t(lrow) * ig.cpr + c) * CB;
+  const int64_t gi = (int64_t(lrow) * ig.cpr + c) * 32 / G;
+  it.scale = reinterpret_cast<const __half*>(reinterpret_cast<const char*>(scale) +
+                                             int64_t(layer) * g.meta_ls) + gi;
+  it.zero = reinterpret_cast<const __half*>(reinterpret_cast<const char*>(zero) +
+                                            int64_t(layer) * g.meta_ls) + gi;
+  return it;
+}
+
+template <int BITS>
+struct K3Data {
+  Chunk32<BITS> c;
+  __half s, z;
+};
+
+template <int BITS>
+__device__ __forceinline__ void k3_load(const K3Item& it, K3Data<BITS>& d) {
+  if (!it.active) return;
+  if constexpr (BITS == 4) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(d.c.w[0]), "=r"(d.c.w[1]), "=r"(d.c.w[2]), "=r"(d.c.w[3])
+                 : "l"(it.codes));
+  } else if constexpr (BITS == 8) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(d.c.w[0]), "=r"(d.c.w[1]), "=r"(d.c.w[2]), "=r"(d.c.w[3]),
+                   "=r"(d.c.w[4]), "=r"(d.c.w[5]), "=r"(d.c.w[6]), "=r"(d.c.w[7])
+                 : "l"(it.codes));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];"
+                 : "=r"(d.c.w[0]), "=r"(d.c.w[1])
+                 : "l"(it.codes));
+  }
+  d.s = __ldg(it.scale);
+  d.z = __ldg(it.zero);
+}
+
+__device__ __forceinline__ void st256(void* p, const U4& a, const U4& b) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+               "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
+template <int BITS>
+__device__ __forceinline__ void k3_process(const K3Item& it, const K3Data<BITS>& d) {
+  if (!it.active) return;
+  const __half2 s2 = __half2half2(d.s), z2 = __half2half2(d.z);
+  U4 o[4];
+  if constexpr (BITS == 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = dequant8<4>(d.c.w[i], s2, z2);
+  } else if constexpr (BITS == 8) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = dequant8<8>(make_uint2(d.c.w[2 * i], d.c.w[2 * i + 1]), s2, z2);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      o[i] = dequant8<2>(uint16_t(d.c.w[i >> 1] >> (16 * (i & 1))), s2, z2);
+  }
+  st256(it.dst, o[0], o[1]);
+  st256(it.dst + 32, o[2], o[3]);
+}
+
+template <int BITS, int G>
+__global__ void __launch_bounds__(256) dequant_scatter_kernel(Geo g, ItemGeo ig,
                                                               const uint8_t* __restrict__ codes,
                                                               const __half* __restrict__ scale,
                                                               const __half* __restrict__ zero) {
-  constexpr int LPG = G / 8;
-  using CT = typename CodeVec<BITS>::T;
   const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const int groups_per_row = g.row_elems / G;
-
-  for (int64_t tr = warp; tr < g.n_token_rows; tr += n_warps) {
-    int64_t lk, t, layer, lrow;
-    split_tr(g, tr, lk, t, layer, lrow);
-    const int64_t pos = pos_of(g, t);
-    if (pos < 0) continue;  // padding token (vLLM slot -1)
-    char* plane = const_cast<char*>((lk & 1) ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
-    U4* dst = reinterpret_cast<U4*>(plane + pos * int64_t(g.row_elems) * 2);
-    const CT* src_codes = reinterpret_cast<const CT*>(codes + layer * g.codes_ls) + lrow * g.vecs;
-    const __half* src_scale =
-        reinterpret_cast<const __half*>(reinterpret_cast<const char*>(scale) + layer * g.meta_ls) +
-        lrow * groups_per_row;
-    const __half* src_zero =
-        reinterpret_cast<const __half*>(reinterpret_cast<const char*>(zero) + layer * g.meta_ls) +
-        lrow * groups_per_row;
-
-    for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
-      CT c[UNROLL];
-      __half s[UNROLL], z[UNROLL];
-#pragma unroll
-      for (int k = 0; k < UNROLL; ++k) {
-        const int vi = base + k * 32 + lane;
-        if (vi < g.vecs) {
-          c[k] = src_codes[vi];
-          s[k] = src_scale[vi / LPG];
-          z[k] = src_zero[vi / LPG];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < UNROLL; ++k) {
-        const int vi = base + k * 32 + lane;
-        if (vi < g.vecs) st_stream(dst + vi, dequant8<BITS>(c[k], __half2half2(s[k]), __half2half2(z[k])));
-      }
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t item = warp;
+  K3Item a, b;
+  K3Data<BITS> da, db;
+  if (item < ig.n_items) {
+    a = k3_item<BITS, G>(g, ig, item, lane, codes, scale, zero);
+    k3_load<BITS>(a, da);
+  }
+  while (item < ig.n_items) {
+    const uint32_t nxt = item + n_warps;
+    if (nxt < ig.n_items) {
+      b = k3_item<BITS, G>(g, ig, nxt, lane, codes, scale, zero);
+      k3_load<BITS>(b, db);
     }
+    k3_process<BITS>(a, da);
+    item = nxt;
+    if (item >= ig.n_items) break;
+    const uint32_t nn = item + n_warps;
+    if (nn < ig.n_items) {
+      a = k3_item<BITS, G>(g, ig, nn, lane, codes, scale, zero);
+      k3_load<BITS>(a, da);
+    }
+    k3_process<BITS>(b, db);
+    item = nn;
   }
 }
 

@@ -187,7 +187,7 @@ class PairChannel:
             raise RuntimeError("stream memory operations unavailable: use mode='nccl'")
         # local buffers: doorbells (written by the partner) + payload staging
         self.flags = IpcBuffer(FLAG_SLOTS * 4)
-        stage_here = (self.role == "prefill" and mode in ("pull", "nccl")) or (
+        stage_here = (self.role == "prefill" and mode in ("pull", "copy", "nccl")) or (
             self.role == "decode" and mode in ("push", "copy", "nccl"))
         self.local_payload = None
         if stage_here:
