@@ -235,7 +235,8 @@ def run_local(args, torch):
     kc = torch.zeros((L, nb, BLOCK, H, D), dtype=torch.float16, device=dev)
     vc = torch.zeros_like(kc)
     plan = HandoffPlan(KVPlanes.dense(kv), KVPlanes.paged(kc, vc, slots), T,
-                       KvPrecision(args.bits), args.group, mode="local", n_chunks=args.chunks)
+                       KvPrecision(args.bits), args.group, mode="local", n_chunks=args.chunks,
+                       bulk=(args.k3 == "bulk"))
     lay = plan.layout
     fp16_bytes = lay.fp16_bytes
     for _ in range(args.warmup):
@@ -300,7 +301,7 @@ def run_local(args, torch):
                   "algorithmic_bytes_per_launch": kernel_bytes // len(plan_chunks(args, L)),
                   "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
                   "step_roofline_ms": round(roof_ms, 4), "step_frac": round(roof_ms / ms, 4)},
-        extra={"n_chunks": args.chunks, "mode": "local"},
+        extra={"n_chunks": args.chunks, "mode": "local", "k3": args.k3},
     )
 
 
@@ -320,7 +321,9 @@ def main():
     ap.add_argument("--group", type=int, default=128)
     ap.add_argument("--chunks", type=int, default=None,
                     help="layer chunks per hand-off (default: 1 at N=1, 8 per pair at N>1)")
-    ap.add_argument("--mode", default="pull", choices=["pull", "push", "copy", "nccl"])
+    ap.add_argument("--mode", default="pull", choices=["pull", "pull_ldg", "push", "copy", "nccl"])
+    ap.add_argument("--k3", default="ldg", choices=["ldg", "bulk"],
+                    help="N=1: K3 variant (per-lane loads or TMA bulk staging)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-layers", type=int, default=2)

@@ -104,6 +104,19 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
                               int group, int bits, void* k_cache, void* v_cache,
                               int64_t dst_layer_stride, void* stream);
 
+/*
+ * K3 with TMA bulk staging: same contract as kvx_dequant_scatter_paged, but
+ * the payload is streamed into shared memory with cp.async.bulk (one request
+ * per span of token rows) -- the fused NVLink-pull variant for a payload that
+ * lives in the prefill GPU's HBM.  Falls back to the per-lane kernel for
+ * shapes whose rows are not 16-byte multiples.
+ */
+int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
+                                   int64_t payload_layer_stride, const int64_t* dst_slots,
+                                   int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                                   int group, int bits, void* k_cache, void* v_cache,
+                                   int64_t dst_layer_stride, void* stream);
+
 /* Packed payload sizes in bytes for n_rows rows (codes, scale, zero). */
 int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t* codes_bytes,
                      int64_t* scale_bytes, int64_t* zero_bytes);

@@ -145,6 +145,62 @@ cudaError_t launch_dequant(const kvx::Geo& g, const void* codes, const void* sca
   return cudaGetLastError();
 }
 
+constexpr int kBulkStages = 4;
+constexpr int kBulkThreads = 288;
+constexpr int kBulkStageTarget = 16384;  // code bytes per stage
+
+template <int BITS, int G>
+cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale, const void* zero,
+                        cudaStream_t s, bool* ok) {
+  *ok = false;
+  kvx::BulkGeo bg;
+  bg.code_row_bytes = int(int64_t(g.row_elems) * BITS / 8);
+  bg.meta_row_bytes = int(int64_t(g.row_elems) / G * 2);
+  bg.cpr = g.row_elems / 32;
+  if (bg.code_row_bytes % 16 || bg.meta_row_bytes % 16 || !aligned(codes, 16) ||
+      !aligned(scale, 16) || !aligned(zero, 16) || g.codes_ls % 16 || g.meta_ls % 16)
+    return cudaSuccess;  // not bulk-copyable: caller falls back to the LDG kernel
+  const int64_t two_t = 2 * g.n_tokens;
+  int64_t r = kBulkStageTarget / bg.code_row_bytes;
+  if (r < 1) r = 1;
+  if (r > two_t) r = two_t;
+  bg.rows_per_span = int(r);
+  bg.stage_bytes = bg.rows_per_span * (bg.code_row_bytes + 2 * bg.meta_row_bytes);
+  const int smem = kBulkStages * bg.stage_bytes;
+  if (smem > 200 * 1024) return cudaSuccess;
+  bg.spans_per_layer = int((two_t + r - 1) / r);
+  const int64_t n_layers = g.n_token_rows / two_t;
+  const int64_t n_spans = n_layers * bg.spans_per_layer;
+  if (n_spans >= (int64_t(1) << 31)) return cudaSuccess;
+  bg.n_spans = uint32_t(n_spans);
+  auto k = kvx::pull_dequant_scatter_kernel<BITS, G, kBulkStages>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBulkThreads, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int64_t grid = int64_t(sm_count(dev)) * per_sm;
+  if (grid > n_spans) grid = n_spans;
+  *ok = true;
+  k<<<unsigned(grid), kBulkThreads, smem, s>>>(g, bg, static_cast<const uint8_t*>(codes),
+                                                static_cast<const __half*>(scale),
+                                                static_cast<const __half*>(zero));
+  return cudaGetLastError();
+}
+
+template <int BITS>
+cudaError_t dispatch_pull(int group, const kvx::Geo& g, const void* c, const void* sc,
+                          const void* z, cudaStream_t s, bool* ok) {
+  switch (group) {
+    case 32: return launch_pull<BITS, 32>(g, c, sc, z, s, ok);
+    case 64: return launch_pull<BITS, 64>(g, c, sc, z, s, ok);
+    default: return launch_pull<BITS, 128>(g, c, sc, z, s, ok);
+  }
+}
+
 template <int BITS>
 cudaError_t dispatch_quant(int group, const kvx::Geo& g, void* c, void* sc, void* z, cudaStream_t s) {
   switch (group) {
@@ -285,6 +341,37 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
     case 8: return dispatch_dequant<8>(group, g, codes, scale, zero, s);
     default: return dispatch_dequant<4>(group, g, codes, scale, zero, s);
   }
+}
+
+int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
+                                   int64_t payload_layer_stride, const int64_t* dst_slots,
+                                   int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                                   int group, int bits, void* k_cache, void* v_cache,
+                                   int64_t dst_layer_stride, void* stream) {
+  int rc = valid_format(head_dim, group, bits);
+  if (rc) return rc;
+  kvx::Geo g;
+  rc = make_geo(g, k_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
+                head_dim, group, bits, payload_layer_stride);
+  if (rc) return rc;
+  if (g.n_token_rows == 0) return KVX_OK;
+  if (bits != 16 && codes && scale && zero && k_cache && aligned(k_cache, 32) &&
+      aligned(v_cache, 32) && (dst_layer_stride * 2) % 32 == 0) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    bool ok = false;
+    cudaError_t e;
+    switch (bits) {
+      case 2: e = dispatch_pull<2>(group, g, codes, scale, zero, s, &ok); break;
+      case 8: e = dispatch_pull<8>(group, g, codes, scale, zero, s, &ok); break;
+      default: e = dispatch_pull<4>(group, g, codes, scale, zero, s, &ok); break;
+    }
+    if (e != cudaSuccess) return e;
+    if (ok) return KVX_OK;
+  }
+  // shapes the bulk path cannot stage (16-bit, unaligned rows): per-lane loads
+  return kvx_dequant_scatter_paged(codes, scale, zero, payload_layer_stride, dst_slots, n_layers,
+                                   n_tokens, n_heads, head_dim, group, bits, k_cache, v_cache,
+                                   dst_layer_stride, stream);
 }
 
 // ---- transport -------------------------------------------------------------

@@ -567,4 +567,154 @@ __global__ void __launch_bounds__(256) scatter16_kernel(Geo g, const uint8_t* __
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3-bulk: TMA-staged pull + dequantise + paged scatter.
+//
+// For a payload that sits in another GPU's HBM (fused NVLink pull) the load
+// side is what limits: per-lane LDGs become many small NVLink reads.  Here one
+// producer thread per CTA streams "spans" (R consecutive token rows of one
+// layer: codes, scales and zeros are each ONE contiguous range) into a
+// STAGES-deep shared-memory ring with cp.async.bulk (the bulk-copy/TMA
+// engine; large requests over NVLink), completion tracked by mbarrier
+// transaction counts.  Eight consumer warps dequantise out of shared memory
+// (16-byte conflict-free LDS per lane) and write 64 B per lane into the paged
+// cache; each warp releases the stage through an "empty" mbarrier.
+// ---------------------------------------------------------------------------
+struct BulkGeo {
+  int rows_per_span;     // R
+  int spans_per_layer;   // ceil(2T / R)
+  uint32_t n_spans;      // n_layers * spans_per_layer
+  int code_row_bytes;    // row_elems * bits / 8  (multiple of 16)
+  int meta_row_bytes;    // row_elems / G * 2     (multiple of 16)
+  int stage_bytes;       // R * (code_row_bytes + 2 * meta_row_bytes)
+  int cpr;               // 32-element chunks per token row
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes,
+                                        uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int BITS, int G, int STAGES>
+__global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
+    Geo g, BulkGeo bg, const uint8_t* __restrict__ codes, const __half* __restrict__ scale,
+    const __half* __restrict__ zero) {
+  constexpr int CONSUMERS = 8;
+  constexpr int CB = 32 * BITS / 8;
+  constexpr int LPG = G / 32;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t two_t = 2 * g.n_tokens;
+
+  if (warp == CONSUMERS) {  // ---- producer: one elected thread
+    if (lane == 0) {
+      uint32_t k = 0;
+      for (uint32_t sp = blockIdx.x; sp < bg.n_spans; sp += gridDim.x, ++k) {
+        const int st = k % STAGES;
+        if (k >= STAGES) mbar_wait(&empty[st], ((k / STAGES) & 1) ^ 1);
+        const uint32_t layer = sp / bg.spans_per_layer;
+        const int64_t r0 = int64_t(sp - layer * bg.spans_per_layer) * bg.rows_per_span;
+        const int rows = int(min(int64_t(bg.rows_per_span), two_t - r0));
+        uint8_t* buf = smem + st * bg.stage_bytes;
+        const uint32_t cb = rows * bg.code_row_bytes, mb = rows * bg.meta_row_bytes;
+        mbar_expect_tx(&full[st], cb + 2 * mb);
+        bulk_g2s(buf, codes + layer * g.codes_ls + r0 * bg.code_row_bytes, cb, &full[st]);
+        const char* sbase = reinterpret_cast<const char*>(scale) + layer * g.meta_ls;
+        const char* zbase = reinterpret_cast<const char*>(zero) + layer * g.meta_ls;
+        uint8_t* mbuf = buf + bg.rows_per_span * bg.code_row_bytes;
+        bulk_g2s(mbuf, sbase + r0 * bg.meta_row_bytes, mb, &full[st]);
+        bulk_g2s(mbuf + bg.rows_per_span * bg.meta_row_bytes, zbase + r0 * bg.meta_row_bytes, mb,
+                 &full[st]);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers
+  uint32_t k = 0;
+  for (uint32_t sp = blockIdx.x; sp < bg.n_spans; sp += gridDim.x, ++k) {
+    const int st = k % STAGES;
+    const uint32_t layer = sp / bg.spans_per_layer;
+    const int64_t r0 = int64_t(sp - layer * bg.spans_per_layer) * bg.rows_per_span;
+    const int rows = int(min(int64_t(bg.rows_per_span), two_t - r0));
+    const uint8_t* buf = smem + st * bg.stage_bytes;
+    const __half* sbuf = reinterpret_cast<const __half*>(buf + bg.rows_per_span * bg.code_row_bytes);
+    const __half* zbuf = sbuf + bg.rows_per_span * bg.meta_row_bytes / 2;
+    mbar_wait(&full[st], (k / STAGES) & 1);
+    for (int r = warp; r < rows; r += CONSUMERS) {
+      const int64_t lrow = r0 + r;
+      const int kv = lrow >= g.n_tokens;
+      const int64_t t = lrow - kv * g.n_tokens;
+      const int64_t pos = pos_of(g, t);
+      if (pos < 0) continue;  // padding token
+      char* dst = const_cast<char*>(kv ? g.v_plane : g.k_plane) + int64_t(layer) * g.layer_stride_b +
+                  pos * int64_t(g.row_elems) * 2;
+      const uint8_t* crow = buf + r * bg.code_row_bytes;
+      const int gpr = bg.meta_row_bytes / 2;
+      for (int c = lane; c < bg.cpr; c += 32) {
+        K3Data<BITS> d;
+        if constexpr (BITS == 2) {
+          const uint2 v = *reinterpret_cast<const uint2*>(crow + c * CB);
+          d.c.w[0] = v.x;
+          d.c.w[1] = v.y;
+        } else {
+#pragma unroll
+          for (int i = 0; i < Chunk32<BITS>::WORDS / 4; ++i) {
+            const uint4 v = reinterpret_cast<const uint4*>(crow + c * CB)[i];
+            d.c.w[4 * i] = v.x;
+            d.c.w[4 * i + 1] = v.y;
+            d.c.w[4 * i + 2] = v.z;
+            d.c.w[4 * i + 3] = v.w;
+          }
+        }
+        d.s = sbuf[r * gpr + c / LPG];
+        d.z = zbuf[r * gpr + c / LPG];
+        K3Item it;
+        it.active = true;
+        it.dst = dst + int64_t(c) * 64;
+        k3_process<BITS>(it, d);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+}
+
 }  // namespace kvx

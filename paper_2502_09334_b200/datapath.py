@@ -252,11 +252,14 @@ def quant_pack_layers(src: KVPlanes, packed: PackedKV, l0: int, l1: int, stream=
 
 
 def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
-                           stream=None) -> None:
+                           stream=None, bulk: bool = False) -> None:
+    """K3 on layers [l0, l1).  ``bulk``: TMA bulk-staged variant (for payloads
+    read over NVLink)."""
     lay = packed.layout
     k, v = dst.ptrs(l0)
     c, s, z = packed.ptrs(l0)
-    _lib.call("kvx_dequant_scatter_paged", c, s, z, lay.layer_stride, dst.slots_ptr, l1 - l0,
+    fn = "kvx_pull_dequant_scatter_paged" if bulk else "kvx_dequant_scatter_paged"
+    _lib.call(fn, c, s, z, lay.layer_stride, dst.slots_ptr, l1 - l0,
               lay.n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
               dst.layer_stride, _stream_ptr(stream))
 
@@ -304,16 +307,17 @@ def compress_paged(k_cache: torch.Tensor, v_cache: torch.Tensor, slot_mapping: t
 
 
 def decompress_into_paged(packed: PackedKV, k_cache: torch.Tensor, v_cache: torch.Tensor,
-                          slot_mapping: torch.Tensor, *, stream=None) -> None:
+                          slot_mapping: torch.Tensor, *, stream=None, bulk: bool = False) -> None:
     """Unpack + dequantise + scatter into the decode side's paged cache.
-    ``packed`` may live on a peer GPU (fused NVLink pull) if peer access is on."""
+    ``packed`` may live on a peer GPU (fused NVLink pull) if peer access is on;
+    ``bulk`` selects the TMA bulk-staged kernel (best for peer payloads)."""
     dst = KVPlanes.paged(k_cache, v_cache, slot_mapping)
     lay = packed.layout
     if (dst.n_layers, dst.n_heads, dst.head_dim) != (lay.n_layers, lay.n_heads, lay.head_dim):
         raise ValueError("cache geometry does not match the packed payload")
     if slot_mapping.numel() != lay.n_tokens:
         raise ValueError("slot_mapping length must equal the payload's token count")
-    dequant_scatter_layers(packed, dst, 0, lay.n_layers, stream)
+    dequant_scatter_layers(packed, dst, 0, lay.n_layers, stream, bulk=bulk)
 
 
 def enable_peer(dev_a: int, dev_b: int) -> None:
@@ -357,8 +361,11 @@ class HandoffPlan:
     """
 
     def __init__(self, src: KVPlanes, dst: KVPlanes, n_tokens: int, prec=KvPrecision(4),
-                 group_size: int = DEFAULT_GROUP, mode: str = "pull", n_chunks: int = 8):
+                 group_size: int = DEFAULT_GROUP, mode: str = "pull", n_chunks: int = 8,
+                 bulk: bool | None = None):
         self.src, self.dst = src, dst
+        # TMA bulk-staged K3 by default when the payload is read over NVLink
+        self.bulk = (mode == "pull") if bulk is None else bool(bulk)
         self.bits = _bits_of(prec)
         self.layout = _layout_for(src, n_tokens, self.bits, group_size)
         if (dst.n_layers, dst.n_heads, dst.head_dim) != (src.n_layers, src.n_heads, src.head_dim):
@@ -424,7 +431,8 @@ class HandoffPlan:
                     ev["k3"] = (torch.cuda.Event(enable_timing=True),
                                 torch.cuda.Event(enable_timing=True))
                     ev["k3"][0].record(self.d_stream)
-                dequant_scatter_layers(self.d_buf, self.dst, l0, l1, self.d_stream)
+                dequant_scatter_layers(self.d_buf, self.dst, l0, l1, self.d_stream,
+                                       bulk=self.bulk)
                 if ev is not None:
                     ev["k3"][1].record(self.d_stream)
                     timing.append(ev)

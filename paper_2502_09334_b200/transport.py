@@ -14,9 +14,11 @@ prefill replicas' GPU memory (``PAPER.md:859``).  Here:
   doorbell flags with CUDA IPC and maps its partner's (the analogue of the
   paper's pre-built group pool); nothing is allocated per hand-off.
 * transports (``mode``):
-    "pull" - K1 on P into P's HBM; D's K3 reads the payload over NVLink (peer
-             loads) and dequantises straight into D's paged cache.  The
+    "pull" - K1 on P into P's HBM; D's K3-bulk streams the payload over NVLink
+             with TMA bulk copies (cp.async.bulk, peer source) into shared
+             memory and dequantises straight into D's paged cache.  The
              payload crosses NVLink once and D's HBM sees only the fp16 writes.
+    "pull_ldg" - same, but K3 reads the peer payload with per-lane 16-B loads.
     "push" - P's K1 stores the payload straight into D's landing buffer over
              NVLink (fused quantise + transfer); K3 on D reads it locally.
     "copy" - K1 local, copy-engine cudaMemcpyAsync into D's landing buffer,
@@ -42,7 +44,7 @@ from .costs import DEFAULT_GROUP, KvPrecision
 from .datapath import (KVPlanes, PackedKV, PackedLayout, _bits_of, _round_up, _stream_ptr,
                        dequant_scatter_layers, layer_chunks, quant_pack_layers)
 
-MODES = ("pull", "push", "copy", "nccl")
+MODES = ("pull", "pull_ldg", "push", "copy", "nccl")
 FLAG_SLOTS = 256  # doorbells per direction (>= chunks)
 
 
@@ -177,17 +179,20 @@ class PairChannel:
         self.rank, self.world = rank, world
         self.role, self.pair, self.peer = role_of(rank, world)
         self.device = torch.device("cuda", torch.cuda.current_device())
-        self.stream = torch.cuda.Stream(self.device)
+        self.stream = torch.cuda.Stream(self.device)    # kernels
+        self.cstream = torch.cuda.Stream(self.device)   # copy engine / NCCL
         self.data_group = data_group
         self.epoch = 0
         self._prev_ranges = None
         self.chunks = spec.chunks()
+        self.k_done = [torch.cuda.Event() for _ in self.chunks]
+        self.comm_done = [torch.cuda.Event() for _ in self.chunks]
         mode = spec.mode
         if mode != "nccl" and not memops_supported():
             raise RuntimeError("stream memory operations unavailable: use mode='nccl'")
         # local buffers: doorbells (written by the partner) + payload staging
         self.flags = IpcBuffer(FLAG_SLOTS * 4)
-        stage_here = (self.role == "prefill" and mode in ("pull", "copy", "nccl")) or (
+        stage_here = (self.role == "prefill" and mode in ("pull", "pull_ldg", "copy", "nccl")) or (
             self.role == "decode" and mode in ("push", "copy", "nccl"))
         self.local_payload = None
         if stage_here:
@@ -213,7 +218,8 @@ class PairChannel:
         if self.role == "prefill":
             self.k1_target = self.peer_payload if mode == "push" else self.local_payload[1]
         else:
-            self.k3_source = self.peer_payload if mode == "pull" else self.local_payload[1]
+            self.k3_source = (self.peer_payload if mode in ("pull", "pull_ldg")
+                              else self.local_payload[1])
 
     # flags: slot c = "chunk c of epoch e ready" (written by P into D's flags);
     #        slot FLAG_SLOTS//2 + c = "chunk c of epoch e consumed" (D -> P)
@@ -223,43 +229,62 @@ class PairChannel:
     def _ack(self, base: int, c: int) -> int:
         return base + 4 * (FLAG_SLOTS // 2 + c)
 
+    @staticmethod
+    def _guard(prev, new_range):
+        """Index of the last previous-epoch chunk overlapping ``new_range``
+        (chunks complete in order, so waiting for it covers all earlier ones)."""
+        if not prev:
+            return None
+        hits = [i for i, (a, _) in enumerate(prev) if a < new_range[1]]
+        return max(hits) if hits else None
+
     def send(self, src: KVPlanes, n_tokens: int, timing: list | None = None) -> None:
         assert self.role == "prefill"
         lay = self.spec.layout(n_tokens)
         self.epoch += 1
         e = self.epoch
         mode = self.spec.mode
-        s = self.stream
-        s.wait_stream(torch.cuda.current_stream(self.device))
+        s, cs = self.stream, self.cstream
+        cur = torch.cuda.current_stream(self.device)
+        s.wait_stream(cur)
         payload = PackedKV(lay, self.k1_target, self.device)
         ranges = [(l0 * lay.layer_stride, l1 * lay.layer_stride) for l0, l1 in self.chunks]
         prev = self._prev_ranges
         for c, (l0, l1) in enumerate(self.chunks):
-            if mode != "nccl" and prev:
-                # never overwrite bytes the decode side may still be reading:
-                # wait for the ack of the last previous-epoch chunk that overlaps
-                # (D acks in chunk order, so that ack covers all earlier ones)
-                last = max(i for i, (a, _) in enumerate(prev) if a < ranges[c][1])
-                wait(self._ack(self.flags.ptr, last), e - 1, s)
+            g = self._guard(prev, ranges[c])
+            if g is not None:
+                if mode in ("pull", "pull_ldg", "push"):
+                    # the decode side may still be reading these bytes
+                    wait(self._ack(self.flags.ptr, g), e - 1, s)
+                else:
+                    # local staging still being copied / sent
+                    s.wait_event(self.comm_done[g])
             ev = _kernel_events(timing, s, "k1")
             quant_pack_layers(src, payload, l0, l1, s)
             _kernel_events_end(ev, s)
             addr, nbytes = payload.byte_range(l0, l1)
+            if mode in ("pull", "pull_ldg", "push"):
+                signal(self._ready(self.peer_flags, c), e, s)
+                continue
+            self.k_done[c].record(s)
+            cs.wait_event(self.k_done[c])
             if mode == "copy":
+                if g is not None:
+                    wait(self._ack(self.flags.ptr, g), e - 1, cs)  # D's landing bytes free
                 dst = self.peer_payload + (addr - self.k1_target)
-                with torch.cuda.stream(s):
-                    _lib.call("kvx_copy_peer", dst, self.device.index, addr, self.device.index,
-                              nbytes, _stream_ptr(s))
-            if mode == "nccl":
+                _lib.call("kvx_copy_peer", dst, self.device.index, addr, self.device.index,
+                          nbytes, _stream_ptr(cs))
+                signal(self._ready(self.peer_flags, c), e, cs)
+            else:  # nccl
                 import torch.distributed as dist
                 t = self.local_payload[0]
                 off = addr - t.data_ptr()
-                with torch.cuda.stream(s):
+                with torch.cuda.stream(cs):
                     dist.send(t[off:off + nbytes], self.peer, group=self.data_group)
-            else:
-                signal(self._ready(self.peer_flags, c), e, s)
+            self.comm_done[c].record(cs)
         self._prev_ranges = ranges
-        torch.cuda.current_stream(self.device).wait_stream(s)
+        cur.wait_stream(s)
+        cur.wait_stream(cs)
 
     def recv(self, dst: KVPlanes, n_tokens: int, timing: list | None = None) -> None:
         assert self.role == "decode"
@@ -267,25 +292,38 @@ class PairChannel:
         self.epoch += 1
         e = self.epoch
         mode = self.spec.mode
-        s = self.stream
-        s.wait_stream(torch.cuda.current_stream(self.device))
+        s, cs = self.stream, self.cstream
+        cur = torch.cuda.current_stream(self.device)
+        s.wait_stream(cur)
+        cs.wait_stream(cur)
         payload = PackedKV(lay, self.k3_source, self.device)
+        ranges = [(l0 * lay.layer_stride, l1 * lay.layer_stride) for l0, l1 in self.chunks]
+        prev = self._prev_ranges
         for c, (l0, l1) in enumerate(self.chunks):
             if mode == "nccl":
                 import torch.distributed as dist
+                g = self._guard(prev, ranges[c])
+                if g is not None:
+                    cs.wait_event(self.k_done[g])  # landing bytes consumed by K3
                 t = self.local_payload[0]
                 addr, nbytes = payload.byte_range(l0, l1)
                 off = addr - t.data_ptr()
-                with torch.cuda.stream(s):
+                with torch.cuda.stream(cs):
                     dist.recv(t[off:off + nbytes], self.peer, group=self.data_group)
+                self.comm_done[c].record(cs)
+                s.wait_event(self.comm_done[c])
             else:
                 wait(self._ready(self.flags.ptr, c), e, s)
             ev = _kernel_events(timing, s, "k3")
-            dequant_scatter_layers(payload, dst, l0, l1, s)
+            dequant_scatter_layers(payload, dst, l0, l1, s, bulk=(mode == "pull"))
             _kernel_events_end(ev, s)
-            if mode != "nccl":
+            if mode == "nccl":
+                self.k_done[c].record(s)
+            else:
                 signal(self._ack(self.peer_flags, c), e, s)
-        torch.cuda.current_stream(self.device).wait_stream(s)
+        self._prev_ranges = ranges
+        cur.wait_stream(s)
+        cur.wait_stream(cs)
 
     def close(self):
         """Unmap the partner's buffers and free ours (call after a barrier)."""
@@ -398,8 +436,8 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
                     "sm_max_mhz": max((c.get("sm_max_mhz") or 0) for c in clocks) or None,
                     "reasons": reasons, "per_rank_median_sm_mhz": sm},
             e2e=None, cpu=None,
-            roofline={"bound": "nvlink", "kernel": "dequant_scatter_paged (pull over NVLink)"
-                      if mode == "pull" else f"hand-off ({mode})",
+            roofline={"bound": "nvlink", "kernel": "pull_dequant_scatter_paged (TMA bulk pull "
+                      "over NVLink)" if mode == "pull" else f"hand-off ({mode})",
                       "achieved": round(link_gbs, 1), "peak": B.NVLINK_GBS,
                       "peak_kind": "measured peer copy, B200_PROFILING.md (900 nominal)",
                       "unit": "GB/s", "frac": round(link_gbs / B.NVLINK_GBS, 4), "traffic": None,

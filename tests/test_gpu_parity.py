@@ -37,6 +37,7 @@ def oracle_payload(kv_np, bits, group):
 
 SHAPES = [  # (L, T, H, D)
     (1, 1, 1, 128),
+    (3, 300, 8, 128),    # several bulk spans per layer, partial last span
     (2, 3, 8, 128),
     (3, 17, 32, 128),
     (2, 64, 40, 128),    # 13B head count (non power of two)
@@ -114,9 +115,11 @@ def paged_case(torch, L, T, H, D, bs, nb, seed, pad=()):
     return slots, kc, vc
 
 
+@pytest.mark.parametrize("bulk", [False, True])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("bits", [2, 4, 8, 16])
-def test_dequant_scatter_paged_bit_exact(cuda, shape, bits):
+def test_dequant_scatter_paged_bit_exact(cuda, shape, bits, bulk):
+    """K3 (per-lane loads) and K3-bulk (TMA cp.async.bulk staging)."""
     from paper_2502_09334_b200 import decompress_into_paged
     L, T, H, D = shape
     group = 64 if D == 64 else 128
@@ -124,7 +127,7 @@ def test_dequant_scatter_paged_bit_exact(cuda, shape, bits):
     bs, nb = 16, (T + 15) // 16 + 3
     slots, kc, vc = paged_case(cuda, L, T, H, D, bs, nb, seed=T, pad=(0,) if T > 2 else ())
     p = run_k1(cuda, kv, bits, group)
-    decompress_into_paged(p, kc, vc, cuda.from_numpy(slots).cuda())
+    decompress_into_paged(p, kc, vc, cuda.from_numpy(slots).cuda(), bulk=bulk)
     cuda.cuda.synchronize()
     # oracle: same dequant + scatter into sentinel-filled caches
     okc = np.full((L, nb, bs, H, D), -7.0, np.float16); ovc = okc.copy()
