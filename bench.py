@@ -46,6 +46,27 @@ WORKLOADS = {
 }
 BLOCK = 16
 
+# Config 5: mixed prompt-length trace: batches of 1-16
+# requests, lengths log-uniform in [128, 8192], np.random.default_rng(0),
+# a batch closes at 16,384 tokens (a prefill batch's worth of KV).
+TRACE_MODELS = {"trace_7b": (32, 32, 128), "trace_70b_gqa": (80, 8, 128)}
+TRACE_CAP = 16384
+
+
+def make_trace(n_batches: int, seed: int = 0, cap: int = TRACE_CAP):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n_batches):
+        lens = []
+        for _ in range(int(rng.integers(1, 17))):
+            n = int(round(float(np.exp(rng.uniform(np.log(128), np.log(8192))))))
+            if sum(lens) + n > cap:
+                break
+            lens.append(n)
+        out.append(lens or [128])
+    return out
+
 
 def peaks():
     try:
@@ -316,7 +337,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS) + sorted(TRACE_MODELS))
     ap.add_argument("--bits", type=int, default=4)
     ap.add_argument("--group", type=int, default=128)
     ap.add_argument("--chunks", type=int, default=None,

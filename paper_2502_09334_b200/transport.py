@@ -187,6 +187,9 @@ class PairChannel:
         self.chunks = spec.chunks()
         self.k_done = [torch.cuda.Event() for _ in self.chunks]
         self.comm_done = [torch.cuda.Event() for _ in self.chunks]
+        self.xfer = torch.cuda.Stream(self.device)      # host <-> device staging
+        self.x_ready = [torch.cuda.Event() for _ in self.chunks]
+        self.x_done = [torch.cuda.Event() for _ in self.chunks]
         mode = spec.mode
         if mode != "nccl" and not memops_supported():
             raise RuntimeError("stream memory operations unavailable: use mode='nccl'")
@@ -238,7 +241,11 @@ class PairChannel:
         hits = [i for i, (a, _) in enumerate(prev) if a < new_range[1]]
         return max(hits) if hits else None
 
-    def send(self, src: KVPlanes, n_tokens: int, timing: list | None = None) -> None:
+    def send(self, src: KVPlanes, n_tokens: int, timing: list | None = None,
+             stage_in: tuple | None = None) -> None:
+        """Hand ``src`` to the partner.  ``stage_in=(host_kv, dev_kv)``: upload
+        each layer chunk from pinned host memory first (the host-buffer e2e
+        path; H2D of chunk c+1 overlaps K1 of chunk c)."""
         assert self.role == "prefill"
         lay = self.spec.layout(n_tokens)
         self.epoch += 1
@@ -251,6 +258,13 @@ class PairChannel:
         ranges = [(l0 * lay.layer_stride, l1 * lay.layer_stride) for l0, l1 in self.chunks]
         prev = self._prev_ranges
         for c, (l0, l1) in enumerate(self.chunks):
+            if stage_in is not None:
+                host, devt = stage_in
+                self.xfer.wait_event(self.x_done[c])  # K1 of the previous epoch read it
+                with torch.cuda.stream(self.xfer):
+                    devt[l0:l1].copy_(host[l0:l1], non_blocking=True)
+                self.x_ready[c].record(self.xfer)
+                s.wait_event(self.x_ready[c])
             g = self._guard(prev, ranges[c])
             if g is not None:
                 if mode in ("pull", "pull_ldg", "push"):
@@ -262,6 +276,8 @@ class PairChannel:
             ev = _kernel_events(timing, s, "k1")
             quant_pack_layers(src, payload, l0, l1, s)
             _kernel_events_end(ev, s)
+            if stage_in is not None:
+                self.x_done[c].record(s)
             addr, nbytes = payload.byte_range(l0, l1)
             if mode in ("pull", "pull_ldg", "push"):
                 signal(self._ready(self.peer_flags, c), e, s)
@@ -285,8 +301,14 @@ class PairChannel:
         self._prev_ranges = ranges
         cur.wait_stream(s)
         cur.wait_stream(cs)
+        if stage_in is not None:
+            cur.wait_stream(self.xfer)
 
-    def recv(self, dst: KVPlanes, n_tokens: int, timing: list | None = None) -> None:
+    def recv(self, dst: KVPlanes, n_tokens: int, timing: list | None = None,
+             stage_out: tuple | None = None) -> None:
+        """Receive into ``dst``.  ``stage_out=((dev_k, dev_v), (host_k, host_v))``:
+        download each finished layer chunk of the cache to pinned host memory
+        (D2H of chunk c overlaps K3 of chunk c+1)."""
         assert self.role == "decode"
         lay = self.spec.layout(n_tokens)
         self.epoch += 1
@@ -314,9 +336,19 @@ class PairChannel:
                 s.wait_event(self.comm_done[c])
             else:
                 wait(self._ready(self.flags.ptr, c), e, s)
+            if stage_out is not None:
+                s.wait_event(self.x_done[c])  # previous epoch's download of these layers
             ev = _kernel_events(timing, s, "k3")
             dequant_scatter_layers(payload, dst, l0, l1, s, bulk=(mode == "pull"))
             _kernel_events_end(ev, s)
+            if stage_out is not None:
+                (dk, dv), (hk, hv) = stage_out
+                self.x_ready[c].record(s)
+                self.xfer.wait_event(self.x_ready[c])
+                with torch.cuda.stream(self.xfer):
+                    hk[l0:l1].copy_(dk[l0:l1], non_blocking=True)
+                    hv[l0:l1].copy_(dv[l0:l1], non_blocking=True)
+                self.x_done[c].record(self.xfer)
             if mode == "nccl":
                 self.k_done[c].record(s)
             else:
@@ -324,6 +356,8 @@ class PairChannel:
         self._prev_ranges = ranges
         cur.wait_stream(s)
         cur.wait_stream(cs)
+        if stage_out is not None:
+            cur.wait_stream(self.xfer)
 
     def close(self):
         """Unmap the partner's buffers and free ours (call after a barrier)."""
@@ -374,23 +408,59 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     dist.init_process_group("nccl", device_id=dev)
     ctrl = dist.new_group(backend="gloo")
     wl = args.workload or B.default_pair_workload(world)
-    L, H, D, b, s = B.WORKLOADS[wl]
-    T = b * s
+    trace = None
+    if wl in B.TRACE_MODELS:
+        L, H, D = B.TRACE_MODELS[wl]
+        trace = B.make_trace(args.warmup + args.steps + 2, seed=0)
+        T = B.TRACE_CAP
+    else:
+        L, H, D, b, s = B.WORKLOADS[wl]
+        T = b * s
     mode = args.mode
     n_chunks = args.chunks or 8
     spec = ChannelSpec(L, T, H, D, args.bits, args.group, n_chunks, mode)
     ch = PairChannel(spec, rank, world, control_group=ctrl)
     lay = spec.layout(T)
+    # per step token counts (fixed workload, or the trace's batches)
+    tok = [T] * (args.warmup + args.steps + 2) if trace is None else [sum(x) for x in trace]
+    it = {"i": 0}
+
+    def next_t():
+        t = tok[it["i"] % len(tok)]
+        it["i"] += 1
+        return t
+
     if ch.role == "prefill":
         kv = B.synthetic_kv_device(torch, L, T, H, D, dev, seed=ch.pair)
         planes = KVPlanes.dense(kv)
-        step = lambda timing=None: ch.send(planes, T, timing)  # noqa: E731
+        step = lambda timing=None: ch.send(planes, next_t(), timing)  # noqa: E731
     else:
         slots, nb = B.paged_slots(torch, T, dev, seed=ch.pair)
         kc = torch.zeros((L, nb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
         vc = torch.zeros_like(kc)
-        planes = KVPlanes.paged(kc, vc, slots)
-        step = lambda timing=None: ch.recv(planes, T, timing)  # noqa: E731
+        if trace is None:
+            planes = KVPlanes.paged(kc, vc, slots)
+            step = lambda timing=None: ch.recv(planes, T, timing)  # noqa: E731
+        else:
+            # each batch gets its own random block placement (requests start on
+            # a block boundary, as a paged allocator hands them out)
+            import numpy as np
+            rng = np.random.default_rng(ch.pair + 7)
+            per_batch = []
+            for lens in trace:
+                nblk = sum((n + B.BLOCK - 1) // B.BLOCK for n in lens)
+                blocks = rng.permutation(nb)[:nblk]
+                sl, bi = [], 0
+                for n in lens:
+                    t = np.arange(n)
+                    sl.append(blocks[bi + t // B.BLOCK] * B.BLOCK + t % B.BLOCK)
+                    bi += (n + B.BLOCK - 1) // B.BLOCK
+                per_batch.append(torch.from_numpy(np.concatenate(sl).astype(np.int64)).to(dev))
+            planes_b = [KVPlanes.paged(kc, vc, sl) for sl in per_batch]
+
+            def step(timing=None):
+                i = it["i"] % len(tok)
+                ch.recv(planes_b[i], next_t(), timing)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -410,8 +480,40 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     kern = {}
     for name, a, b_ in timing:
         kern[name] = kern.get(name, 0.0) + a.elapsed_time(b_) / args.steps
-    stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0)], dtype=torch.float64,
-                         device=dev)
+    # e2e through the same public API with host buffers: pinned host KV on the
+    # prefill side (H2D inside the step), pinned host paged cache on the decode
+    # side (D2H inside the step)
+    e2e_ms, h2d, d2h = 0.0, 0, 0
+    if not args.no_e2e:
+        if ch.role == "prefill":
+            host = torch.empty(kv.shape, dtype=torch.float16, pin_memory=True)
+            host.copy_(kv)
+            stage = dict(stage_in=(host, kv))
+            h2d = host.numel() * 2
+            e2e_step = lambda: ch.send(planes, next_t(), None, **stage)  # noqa: E731
+        else:
+            hk = torch.empty(kc.shape, dtype=torch.float16, pin_memory=True)
+            hv = torch.empty(vc.shape, dtype=torch.float16, pin_memory=True)
+            stage = dict(stage_out=((kc, vc), (hk, hv)))
+            d2h = (hk.numel() + hv.numel()) * 2
+            e2e_step = (lambda: ch.recv(planes, next_t(), None, **stage)) if trace is None else (
+                lambda: ch.recv(planes_b[it["i"] % len(tok)], next_t(), None, **stage))
+        n_e2e = max(1, min(args.steps, args.e2e_steps))
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / n_e2e
+        dist.barrier()
+    stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0), e2e_ms, h2d, d2h],
+                         dtype=torch.float64, device=dev)
     gathered = [torch.zeros_like(stats) for _ in range(world)]
     dist.all_gather(gathered, stats)
     clocks = exchange(clk.summary(), ctrl)
@@ -421,9 +523,14 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
         k1 = float(g[:, 1].max())
         k3 = float(g[:, 2].max())
         pairs = world // 2
-        fp16 = lay.fp16_bytes
+        if trace is None:
+            fp16 = lay.fp16_bytes
+        else:  # mean fp16 bytes of the timed batches
+            timed = tok[args.warmup:args.warmup + args.steps]
+            fp16 = sum(spec.layout(t).fp16_bytes for t in timed) / len(timed)
+            wire_mean = sum(spec.layout(t).wire_bytes for t in timed) / len(timed)
         value = pairs * fp16 / (ms_max * 1e-3) / 1e9
-        wire = lay.wire_bytes
+        wire = lay.wire_bytes if trace is None else wire_mean
         link_gbs = wire / (ms_max * 1e-3) / 1e9  # per pair
         hbm, peak_kind = B.peaks()
         k3_link = wire / (k3 * 1e-3) / 1e9 if k3 > 0 else None
@@ -435,7 +542,14 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
             clocks={"sm_mhz": min(sm) if sm else None,
                     "sm_max_mhz": max((c.get("sm_max_mhz") or 0) for c in clocks) or None,
                     "reasons": reasons, "per_rank_median_sm_mhz": sm},
-            e2e=None, cpu=None,
+            e2e=None if args.no_e2e else {
+                "value": round(pairs * fp16 / (float(g[:, 3].max()) * 1e-3) / 1e9, 3),
+                "unit": "GB/s", "h2d_bytes_per_step": int(g[:, 4].sum()),
+                "d2h_bytes_per_step": int(g[:, 5].sum()),
+                "ms_per_step": round(float(g[:, 3].max()), 3),
+                "path": "pinned host KV -(H2D)-> K1 on P -(NVLink)-> K3 on D -(D2H)-> pinned "
+                        "host paged cache, per layer chunk"},
+            cpu=None,
             roofline={"bound": "nvlink", "kernel": "pull_dequant_scatter_paged (TMA bulk pull "
                       "over NVLink)" if mode == "pull" else f"hand-off ({mode})",
                       "achieved": round(link_gbs, 1), "peak": B.NVLINK_GBS,
@@ -446,6 +560,9 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
                       "frac_of_nominal_900": round(link_gbs / 900.0, 4),
                       "hbm_peak": hbm},
             extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
+                   **({"trace_batches_timed": tok[args.warmup:args.warmup + args.steps],
+                       "trace": "lengths log-uniform [128, 8192], 1-16 req/batch, <=16384 "
+                                "tokens/batch, rng(0)"} if trace is not None else {}),
                    "pairing": pairing(world), "parallelism": f"{pairs}P{pairs}D"},
         )
         emit(args, r, world)

@@ -58,6 +58,37 @@ def main():
                         print(f"MISMATCH rank={rank} mode={mode} bits={bits} T={T}", flush=True)
             dist.barrier()
             ch.close()
+    # host-buffer path (e2e): pinned host KV -> P, D -> pinned host cache
+    spec = ChannelSpec(L, Tmax, H, D, 4, 128, 4, "pull")
+    ch = PairChannel(spec, rank, world, control_group=ctrl)
+    nb = Tmax // bs + 4
+    for epoch, T in enumerate((150, Tmax)):
+        seed = 77 + 1000 * ch.pair + epoch
+        if ch.role == "prefill":
+            kv_np = O.synthetic_kv(L, Tmax, H, D, seed=seed)
+            host = torch.from_numpy(kv_np).pin_memory()
+            devt = torch.empty_like(host, device=dev)
+            ch.send(KVPlanes.dense(devt), T, stage_in=(host, devt))
+            torch.cuda.synchronize()
+        else:
+            slots_np = O.synthetic_slots(T, bs, nb, seed=seed)
+            kc = torch.zeros((L, nb, bs, H, D), dtype=torch.float16, device=dev)
+            vc = torch.zeros_like(kc)
+            hk, hv = torch.zeros_like(kc, device="cpu").pin_memory(), torch.zeros_like(vc, device="cpu").pin_memory()
+            ch.recv(KVPlanes.paged(kc, vc, torch.from_numpy(slots_np).to(dev)), T,
+                    stage_out=((kc, vc), (hk, hv)))
+            torch.cuda.synchronize()
+            kv_np = O.synthetic_kv(L, Tmax, H, D, seed=seed)[:, :, :T]
+            okc = np.zeros((L, nb, bs, H, D), np.float16); ovc = okc.copy()
+            c, s_, z = O.quant_pack(np.ascontiguousarray(kv_np).reshape(-1, D), 4, 128)
+            O.scatter_paged(O.unpack_dequant(c, s_, z, 4, 128, D).reshape(L, 2, T, H, D),
+                            slots_np, okc, ovc)
+            if not (np.array_equal(hk.numpy().view(np.uint16), okc.view(np.uint16)) and
+                    np.array_equal(hv.numpy().view(np.uint16), ovc.view(np.uint16))):
+                failures += 1
+                print(f"MISMATCH staged rank={rank} T={T}", flush=True)
+    dist.barrier()
+    ch.close()
     f = torch.tensor([failures], device=dev)
     dist.all_reduce(f)
     if rank == 0:
