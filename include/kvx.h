@@ -108,14 +108,24 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
  * K3 with TMA bulk staging: same contract as kvx_dequant_scatter_paged, but
  * the payload is streamed into shared memory with cp.async.bulk (one request
  * per span of token rows) -- the fused NVLink-pull variant for a payload that
- * lives in the prefill GPU's HBM.  Falls back to the per-lane kernel for
- * shapes whose rows are not 16-byte multiples.
+ * lives in the prefill GPU's HBM.
+ * ready_flags (nullable, this GPU's memory): the kernel itself waits, per
+ * chunk of layers_per_chunk layers, until ready_flags[chunk] >= epoch
+ * (wrap-safe), so ONE launch consumes a whole hand-off while the prefill GPU
+ * is still producing it (the producer publishes chunks with
+ * kvx_stream_signal).  Without flags, shapes whose rows are not 16-byte
+ * multiples fall back to the per-lane kernel; with flags they return
+ * KVX_ERR_UNSUPPORTED (see kvx_pull_supported).
  */
 int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
                                    int64_t payload_layer_stride, const int64_t* dst_slots,
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
-                                   int64_t dst_layer_stride, void* stream);
+                                   int64_t dst_layer_stride, const void* ready_flags,
+                                   uint32_t epoch, int layers_per_chunk, void* stream);
+
+/* 1 if kvx_pull_dequant_scatter_paged can bulk-stage this shape. */
+int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, int bits);
 
 /* Packed payload sizes in bytes for n_rows rows (codes, scale, zero). */
 int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t* codes_bytes,

@@ -39,6 +39,15 @@ static int check(int head_dim, int group, int bits) {
   return 0;
 }
 
+void kvq_set_threads(int n) {
+#ifdef _OPENMP
+  extern void omp_set_num_threads(int);
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int kvq_threads(void) {
 #ifdef _OPENMP
   extern int omp_get_max_threads(void);

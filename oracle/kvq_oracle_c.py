@@ -34,6 +34,9 @@ def lib():
         L.kvq_dequant.argtypes = [P, P, P, I64, I, I, I, P]
         L.kvq_dequant_scatter_paged.argtypes = [P, P, P, P, I64, I64, I, I, I, I, P, P, I64]
         L.kvq_threads.argtypes = []
+        L.kvq_set_threads.argtypes = [ctypes.c_int]
+        # all host threads this process may use (torchrun exports OMP_NUM_THREADS=1)
+        L.kvq_set_threads(len(os.sched_getaffinity(0)))
         _lib = L
     return _lib
 

@@ -151,9 +151,13 @@ constexpr int kBulkStageTarget = 16384;  // code bytes per stage
 
 template <int BITS, int G>
 cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale, const void* zero,
-                        cudaStream_t s, bool* ok) {
+                        cudaStream_t s, bool* ok, const uint32_t* ready, uint32_t epoch,
+                        int layers_per_chunk) {
   *ok = false;
   kvx::BulkGeo bg;
+  bg.ready = ready;
+  bg.epoch = epoch;
+  bg.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
   bg.code_row_bytes = int(int64_t(g.row_elems) * BITS / 8);
   bg.meta_row_bytes = int(int64_t(g.row_elems) / G * 2);
   bg.cpr = g.row_elems / 32;
@@ -193,11 +197,12 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
 
 template <int BITS>
 cudaError_t dispatch_pull(int group, const kvx::Geo& g, const void* c, const void* sc,
-                          const void* z, cudaStream_t s, bool* ok) {
+                          const void* z, cudaStream_t s, bool* ok, const uint32_t* ready,
+                          uint32_t epoch, int lpc) {
   switch (group) {
-    case 32: return launch_pull<BITS, 32>(g, c, sc, z, s, ok);
-    case 64: return launch_pull<BITS, 64>(g, c, sc, z, s, ok);
-    default: return launch_pull<BITS, 128>(g, c, sc, z, s, ok);
+    case 32: return launch_pull<BITS, 32>(g, c, sc, z, s, ok, ready, epoch, lpc);
+    case 64: return launch_pull<BITS, 64>(g, c, sc, z, s, ok, ready, epoch, lpc);
+    default: return launch_pull<BITS, 128>(g, c, sc, z, s, ok, ready, epoch, lpc);
   }
 }
 
@@ -347,7 +352,8 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
                                    int64_t payload_layer_stride, const int64_t* dst_slots,
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
-                                   int64_t dst_layer_stride, void* stream) {
+                                   int64_t dst_layer_stride, const void* ready_flags,
+                                   uint32_t epoch, int layers_per_chunk, void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
   kvx::Geo g;
@@ -355,23 +361,33 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
                 head_dim, group, bits, payload_layer_stride);
   if (rc) return rc;
   if (g.n_token_rows == 0) return KVX_OK;
+  if (ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) return KVX_ERR_INVALID_ARG;
   if (bits != 16 && codes && scale && zero && k_cache && aligned(k_cache, 32) &&
       aligned(v_cache, 32) && (dst_layer_stride * 2) % 32 == 0) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t* rf = static_cast<const uint32_t*>(ready_flags);
     bool ok = false;
     cudaError_t e;
     switch (bits) {
-      case 2: e = dispatch_pull<2>(group, g, codes, scale, zero, s, &ok); break;
-      case 8: e = dispatch_pull<8>(group, g, codes, scale, zero, s, &ok); break;
-      default: e = dispatch_pull<4>(group, g, codes, scale, zero, s, &ok); break;
+      case 2: e = dispatch_pull<2>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk); break;
+      case 8: e = dispatch_pull<8>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk); break;
+      default: e = dispatch_pull<4>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk); break;
     }
     if (e != cudaSuccess) return e;
     if (ok) return KVX_OK;
   }
-  // shapes the bulk path cannot stage (16-bit, unaligned rows): per-lane loads
+  // shapes the bulk path cannot stage (16-bit, unaligned rows): per-lane loads,
+  // which cannot wait in-kernel -- callers pass ready_flags only for bulk shapes
+  if (ready_flags) return KVX_ERR_UNSUPPORTED;
   return kvx_dequant_scatter_paged(codes, scale, zero, payload_layer_stride, dst_slots, n_layers,
                                    n_tokens, n_heads, head_dim, group, bits, k_cache, v_cache,
                                    dst_layer_stride, stream);
+}
+
+int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, int bits) {
+  if (valid_format(head_dim, group, bits) || bits == 16 || n_tokens < 1) return 0;
+  const int64_t row = int64_t(n_heads) * head_dim;
+  return (row * bits / 8) % 16 == 0 && (row / group * 2) % 16 == 0;
 }
 
 // ---- transport -------------------------------------------------------------

@@ -581,6 +581,9 @@ __global__ void __launch_bounds__(256) scatter16_kernel(Geo g, const uint8_t* __
 // cache; each warp releases the stage through an "empty" mbarrier.
 // ---------------------------------------------------------------------------
 struct BulkGeo {
+  const uint32_t* ready; // per-chunk doorbells (nullable): wait ready[c] >= epoch
+  uint32_t epoch;
+  int layers_per_chunk;
   int rows_per_span;     // R
   int spans_per_layer;   // ceil(2T / R)
   uint32_t n_spans;      // n_layers * spans_per_layer
@@ -614,6 +617,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Block (producer thread only) until the prefill side has published chunk c of
+// this epoch.  The doorbell lives in this GPU's memory and is written over
+// NVLink by the prefill GPU's stream (cuStreamWriteValue32, fenced); the
+// acquire + proxy fence order the following bulk reads of the peer payload.
+// Bounded: traps after ~60 s instead of hanging the GPU.
+__device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t epoch) {
+  uint32_t v;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (int32_t(v - epoch) >= 0) break;
+    if (spin > (1u << 26)) __trap();
+    __nanosleep(spin < 64 ? 32 : 512);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes,
                                         uint64_t* bar) {
   asm volatile(
@@ -646,10 +665,18 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
   if (warp == CONSUMERS) {  // ---- producer: one elected thread
     if (lane == 0) {
       uint32_t k = 0;
+      int ready_chunk = -1;  // highest chunk known to be published
       for (uint32_t sp = blockIdx.x; sp < bg.n_spans; sp += gridDim.x, ++k) {
         const int st = k % STAGES;
         if (k >= STAGES) mbar_wait(&empty[st], ((k / STAGES) & 1) ^ 1);
         const uint32_t layer = sp / bg.spans_per_layer;
+        if (bg.ready) {
+          const int c = int(layer) / bg.layers_per_chunk;
+          if (c > ready_chunk) {
+            wait_ready(bg.ready + c, bg.epoch);
+            ready_chunk = c;
+          }
+        }
         const int64_t r0 = int64_t(sp - layer * bg.spans_per_layer) * bg.rows_per_span;
         const int rows = int(min(int64_t(bg.rows_per_span), two_t - r0));
         uint8_t* buf = smem + st * bg.stage_bytes;

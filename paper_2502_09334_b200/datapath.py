@@ -252,16 +252,27 @@ def quant_pack_layers(src: KVPlanes, packed: PackedKV, l0: int, l1: int, stream=
 
 
 def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
-                           stream=None, bulk: bool = False) -> None:
+                           stream=None, bulk: bool = False, ready: tuple | None = None) -> None:
     """K3 on layers [l0, l1).  ``bulk``: TMA bulk-staged variant (for payloads
-    read over NVLink)."""
+    read over NVLink).  ``ready=(flags_addr, epoch, layers_per_chunk)``: the
+    bulk kernel waits in-kernel for each chunk's doorbell (one launch per
+    hand-off)."""
     lay = packed.layout
     k, v = dst.ptrs(l0)
     c, s, z = packed.ptrs(l0)
-    fn = "kvx_pull_dequant_scatter_paged" if bulk else "kvx_dequant_scatter_paged"
-    _lib.call(fn, c, s, z, lay.layer_stride, dst.slots_ptr, l1 - l0,
-              lay.n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
-              dst.layer_stride, _stream_ptr(stream))
+    args = (c, s, z, lay.layer_stride, dst.slots_ptr, l1 - l0, lay.n_tokens, lay.n_heads,
+            lay.head_dim, lay.group, lay.bits, k, v, dst.layer_stride)
+    if bulk or ready is not None:
+        rf, epoch, lpc = ready if ready is not None else (None, 0, 1)
+        _lib.call("kvx_pull_dequant_scatter_paged", *args, rf, epoch & 0xFFFFFFFF, lpc,
+                  _stream_ptr(stream))
+    else:
+        _lib.call("kvx_dequant_scatter_paged", *args, _stream_ptr(stream))
+
+
+def pull_supported(lay: PackedLayout) -> bool:
+    return bool(_lib.load().kvx_pull_supported(lay.n_tokens, lay.n_heads, lay.head_dim,
+                                                  lay.group, lay.bits))
 
 
 def _layout_for(src: KVPlanes, n_tokens: int, bits: int, group: int) -> PackedLayout:
@@ -342,10 +353,16 @@ def transfer(packed: PackedKV, dst_device, *, out: PackedKV | None = None, strea
     return out
 
 
+def layers_per_chunk(n_layers: int, n_chunks: int) -> int:
+    n_chunks = max(1, min(n_chunks, max(n_layers, 1)))
+    return max(1, -(-n_layers // n_chunks))
+
+
 def layer_chunks(n_layers: int, n_chunks: int):
-    n_chunks = max(1, min(n_chunks, n_layers))
-    bounds = [round(i * n_layers / n_chunks) for i in range(n_chunks + 1)]
-    return [(bounds[i], bounds[i + 1]) for i in range(n_chunks) if bounds[i + 1] > bounds[i]]
+    """Uniform chunks of ceil(L / n_chunks) layers (chunk of layer l = l // lpc,
+    the rule the in-kernel doorbell wait uses)."""
+    lpc = layers_per_chunk(n_layers, n_chunks)
+    return [(l0, min(n_layers, l0 + lpc)) for l0 in range(0, n_layers, lpc)]
 
 
 class HandoffPlan:

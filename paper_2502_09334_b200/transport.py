@@ -41,10 +41,12 @@ import torch
 
 from . import _lib
 from .costs import DEFAULT_GROUP, KvPrecision
-from .datapath import (KVPlanes, PackedKV, PackedLayout, _bits_of, _round_up, _stream_ptr,
-                       dequant_scatter_layers, layer_chunks, quant_pack_layers)
+from .datapath import (KVPlanes, PackedKV, PackedLayout, _round_up, _stream_ptr,
+                       dequant_scatter_layers, layer_chunks, layers_per_chunk, pull_supported,
+                       quant_pack_layers)
 
 MODES = ("pull", "pull_ldg", "push", "copy", "nccl")
+PULL_MODES = ("pull", "pull_ldg")
 FLAG_SLOTS = 256  # doorbells per direction (>= chunks)
 
 
@@ -185,6 +187,7 @@ class PairChannel:
         self.epoch = 0
         self._prev_ranges = None
         self.chunks = spec.chunks()
+        self.lpc = layers_per_chunk(spec.n_layers, spec.n_chunks)
         self.k_done = [torch.cuda.Event() for _ in self.chunks]
         self.comm_done = [torch.cuda.Event() for _ in self.chunks]
         self.xfer = torch.cuda.Stream(self.device)      # host <-> device staging
@@ -203,7 +206,10 @@ class PairChannel:
                 t = torch.empty(spec.capacity_bytes, dtype=torch.uint8, device=self.device)
                 self.local_payload = (t, _round_up(t.data_ptr()))
             else:
-                b = IpcBuffer(spec.capacity_bytes)
+                # pull modes double-buffer the prefill-side queue: hand-off e
+                # fills half e % 2 while the decode side may still read e - 1
+                halves = 2 if mode in PULL_MODES else 1
+                b = IpcBuffer(_round_up(spec.capacity_bytes) * halves)
                 self.local_payload = (b, _round_up(b.ptr))
         mine = {"flags": self.flags.handle()}
         if self.local_payload is not None and mode != "nccl":
@@ -223,6 +229,10 @@ class PairChannel:
         else:
             self.k3_source = (self.peer_payload if mode in ("pull", "pull_ldg")
                               else self.local_payload[1])
+
+    def _half(self, e: int) -> int:
+        """Byte offset of the payload half used by hand-off ``e`` (pull modes)."""
+        return (e & 1) * _round_up(self.spec.capacity_bytes)
 
     # flags: slot c = "chunk c of epoch e ready" (written by P into D's flags);
     #        slot FLAG_SLOTS//2 + c = "chunk c of epoch e consumed" (D -> P)
@@ -254,9 +264,14 @@ class PairChannel:
         s, cs = self.stream, self.cstream
         cur = torch.cuda.current_stream(self.device)
         s.wait_stream(cur)
-        payload = PackedKV(lay, self.k1_target, self.device)
+        if mode in PULL_MODES:
+            payload = PackedKV(lay, self.k1_target + self._half(e), self.device)
+            # the half we fill was last read by hand-off e - 2
+            wait(self._ack(self.flags.ptr, 0), e - 2, s)
+        else:
+            payload = PackedKV(lay, self.k1_target, self.device)
         ranges = [(l0 * lay.layer_stride, l1 * lay.layer_stride) for l0, l1 in self.chunks]
-        prev = self._prev_ranges
+        prev = self._prev_ranges if mode not in PULL_MODES else None
         for c, (l0, l1) in enumerate(self.chunks):
             if stage_in is not None:
                 host, devt = stage_in
@@ -267,7 +282,7 @@ class PairChannel:
                 s.wait_event(self.x_ready[c])
             g = self._guard(prev, ranges[c])
             if g is not None:
-                if mode in ("pull", "pull_ldg", "push"):
+                if mode == "push":
                     # the decode side may still be reading these bytes
                     wait(self._ack(self.flags.ptr, g), e - 1, s)
                 else:
@@ -318,7 +333,34 @@ class PairChannel:
         cur = torch.cuda.current_stream(self.device)
         s.wait_stream(cur)
         cs.wait_stream(cur)
-        payload = PackedKV(lay, self.k3_source, self.device)
+        if mode in PULL_MODES:
+            payload = PackedKV(lay, self.k3_source + self._half(e), self.device)
+            if mode == "pull" and pull_supported(lay):
+                # ONE persistent bulk-pull kernel for the whole hand-off: its
+                # producer threads wait in-kernel for each chunk's doorbell
+                if stage_out is not None:
+                    for c in range(len(self.chunks)):
+                        s.wait_event(self.x_done[c])
+                ev = _kernel_events(timing, s, "k3")
+                dequant_scatter_layers(payload, dst, 0, lay.n_layers, s,
+                                       ready=(self.flags.ptr, e, self.lpc))
+                _kernel_events_end(ev, s)
+                if stage_out is not None:
+                    (dk, dv), (hk, hv) = stage_out
+                    self.x_ready[0].record(s)
+                    self.xfer.wait_event(self.x_ready[0])
+                    with torch.cuda.stream(self.xfer):
+                        hk.copy_(dk, non_blocking=True)
+                        hv.copy_(dv, non_blocking=True)
+                    for c in range(len(self.chunks)):
+                        self.x_done[c].record(self.xfer)
+                signal(self._ack(self.peer_flags, 0), e, s)
+                cur.wait_stream(s)
+                if stage_out is not None:
+                    cur.wait_stream(self.xfer)
+                return
+        else:
+            payload = PackedKV(lay, self.k3_source, self.device)
         ranges = [(l0 * lay.layer_stride, l1 * lay.layer_stride) for l0, l1 in self.chunks]
         prev = self._prev_ranges
         for c, (l0, l1) in enumerate(self.chunks):
@@ -351,8 +393,10 @@ class PairChannel:
                 self.x_done[c].record(self.xfer)
             if mode == "nccl":
                 self.k_done[c].record(s)
-            else:
+            elif mode not in PULL_MODES:
                 signal(self._ack(self.peer_flags, c), e, s)
+        if mode in PULL_MODES:
+            signal(self._ack(self.peer_flags, 0), e, s)  # whole half consumed
         self._prev_ranges = ranges
         cur.wait_stream(s)
         cur.wait_stream(cs)
