@@ -194,6 +194,9 @@ def run_reference(args, rank: int, world: int):
     bits, group = args.bits, args.group
     wl = args.workload or ("cfg2_7b_2048x8" if world == 1 else default_pair_workload(world))
     L, H, D, b, s = WORKLOADS[wl]
+    if not args.ref_layers:
+        per_layer = 2 * b * s * H * D * 2
+        args.ref_layers = max(1, min(L, round(1.0e9 / per_layer)))
     for _ in range(args.warmup):
         cpu_reference(wl, bits, group, budget_s=None, max_layers=1)
     vals, secs = [], []
@@ -347,7 +350,8 @@ def main():
                     help="N=1: K3 variant (per-lane loads or TMA bulk staging)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--ref-layers", type=int, default=2)
+    ap.add_argument("--ref-layers", type=int, default=None,
+                    help="reference arm: layers per step (default: ~1 GB of fp16 KV)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -556,8 +556,8 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / n_e2e
         dist.barrier()
-    stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0), e2e_ms, h2d, d2h],
-                         dtype=torch.float64, device=dev)
+    stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0), e2e_ms, h2d, d2h,
+                          len(timing)], dtype=torch.float64, device=dev)
     gathered = [torch.zeros_like(stats) for _ in range(world)]
     dist.all_gather(gathered, stats)
     clocks = exchange(clk.summary(), ctrl)
@@ -582,7 +582,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
         reasons = sorted({r for c in clocks for r in c.get("reasons", [])})
         r = dict(
             value=value, ms=ms_max, workload=wl, fp16_bytes=fp16 * pairs, wire_bytes=wire * pairs,
-            launches=2 * len(spec.chunks()) * pairs * args.steps,
+            launches=int(g[:, 6].sum()),  # kvx kernels launched in the timed region
             clocks={"sm_mhz": min(sm) if sm else None,
                     "sm_max_mhz": max((c.get("sm_max_mhz") or 0) for c in clocks) or None,
                     "reasons": reasons, "per_rank_median_sm_mhz": sm},
