@@ -286,6 +286,7 @@ def run_local(args, torch):
     step_bytes = 2 * kernel_bytes  # algorithmic HBM bytes of the round trip
     roof_ms = step_bytes / (hbm * 1e9) * 1e3
     value = fp16_bytes / (ms * 1e-3) / 1e9
+    verified = None if args.no_verify else verify_local(torch, kv, kc, vc, slots, args)
 
     # e2e: the same hand-off from pinned host KV to a host paged cache
     e2e = None
@@ -325,8 +326,27 @@ def run_local(args, torch):
                   "algorithmic_bytes_per_launch": kernel_bytes // len(plan_chunks(args, L)),
                   "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
                   "step_roofline_ms": round(roof_ms, 4), "step_frac": round(roof_ms / ms, 4)},
-        extra={"n_chunks": args.chunks, "mode": "local", "k3": args.k3},
+        extra={"n_chunks": args.chunks, "mode": "local", "k3": args.k3,
+               "verified_sampled_rows_bit_exact": verified},
     )
+
+
+def verify_local(torch, kv, kc, vc, slots, args):
+    """Full-size parity outside the timed region: 3 layers x 32 sampled tokens
+    of the decode cache vs the C oracle applied to the same source rows."""
+    import numpy as np
+    from oracle import kvq_oracle_c as C  # the checker, not the measured path
+    L, _, T, H, D = kv.shape
+    rng = np.random.default_rng(99)
+    toks = torch.from_numpy(np.sort(rng.choice(T, size=min(32, T), replace=False))).to(kv.device)
+    layers = sorted({0, L // 2, L - 1})
+    src = kv[layers][:, :, toks].cpu().numpy()
+    sl = slots[toks]
+    got = torch.stack([kc[layers].reshape(len(layers), -1, H, D)[:, sl],
+                       vc[layers].reshape(len(layers), -1, H, D)[:, sl]], 1).cpu().numpy()
+    c, s_, z = C.quant_pack(src.reshape(-1, D), args.bits, args.group)
+    want = C.unpack_dequant(c, s_, z, args.bits, args.group, D).reshape(src.shape)
+    return bool(np.array_equal(want.view(np.uint16), got.view(np.uint16)))
 
 
 def plan_chunks(args, L):
@@ -354,6 +374,8 @@ def main():
                     help="reference arm: layers per step (default: ~1 GB of fp16 KV)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true",
+                    help="skip the full-size sampled bit-exact check (outside the timed region)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps

@@ -439,6 +439,40 @@ def _kernel_events_end(ev, stream):
 # bench.py N > 1
 # ---------------------------------------------------------------------------
 
+def _verify_last(ch, trace, tok, it, L, H, D, spec, ctrl, kv=None, dec=None):
+    """Bit-exact check of 3 layers x 32 sampled tokens of the last hand-off at
+    full size: the prefill rank ships its source rows, the decode rank runs the
+    C oracle on them and compares with its paged cache.  Returns the AND over
+    all pairs (every rank gets it)."""
+    import numpy as np
+
+    last = (it["i"] - 1) % len(tok)
+    T_last = tok[last]
+    rng = np.random.default_rng(1234 + last)
+    toks = np.sort(rng.choice(T_last, size=min(32, T_last), replace=False))
+    layers = sorted({0, L // 2, L - 1})
+    mine = None
+    if ch.role == "prefill":
+        rows = kv[layers][:, :, torch.from_numpy(toks).to(kv.device)]  # [nl, 2, n, H, D]
+        mine = rows.cpu().numpy()
+    else:
+        kc, vc, pl = dec
+        planes = pl if trace is None else pl[last]
+        sl = planes.slots[torch.from_numpy(toks).to(kc.device)]
+        ks = kc[layers].reshape(len(layers), -1, H, D)[:, sl]
+        vs = vc[layers].reshape(len(layers), -1, H, D)[:, sl]
+        mine = torch.stack([ks, vs], 1).cpu().numpy()
+    allv = exchange(mine, ctrl)
+    ok = True
+    if ch.role == "decode":
+        from oracle import kvq_oracle_c as C  # the checker, never the measured path
+        src = allv[ch.peer]
+        c, s_, z = C.quant_pack(np.ascontiguousarray(src).reshape(-1, D), spec.bits, spec.group)
+        want = C.unpack_dequant(c, s_, z, spec.bits, spec.group, D).reshape(src.shape)
+        ok = bool(np.array_equal(want.view(np.uint16), mine.view(np.uint16)))
+    return all(exchange(ok, ctrl))
+
+
 def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     """Weak-scaling pair benchmark: every pair hands off the same workload."""
     import json
@@ -524,6 +558,14 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     kern = {}
     for name, a, b_ in timing:
         kern[name] = kern.get(name, 0.0) + a.elapsed_time(b_) / args.steps
+    # full-size parity (outside the timed region): sampled token rows of the
+    # last hand-off, decode cache vs the CPU oracle applied to the source rows
+    verified = None
+    if not getattr(args, "no_verify", False):
+        verified = _verify_last(ch, trace, tok, it, L, H, D, spec, ctrl,
+                                kv if ch.role == "prefill" else None,
+                                (kc, vc, planes if trace is None else planes_b)
+                                if ch.role == "decode" else None)
     # e2e through the same public API with host buffers: pinned host KV on the
     # prefill side (H2D inside the step), pinned host paged cache on the decode
     # side (D2H inside the step)
@@ -604,6 +646,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
                       "frac_of_nominal_900": round(link_gbs / 900.0, 4),
                       "hbm_peak": hbm},
             extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
+                   "verified_sampled_rows_bit_exact": verified,
                    **({"trace_batches_timed": tok[args.warmup:args.warmup + args.steps],
                        "trace": "lengths log-uniform [128, 8192], 1-16 req/batch, <=16384 "
                                 "tokens/batch, rng(0)"} if trace is not None else {}),
