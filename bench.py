@@ -297,7 +297,7 @@ def run_local(args, torch):
         vc_h = torch.empty(vc.shape, dtype=torch.float16, pin_memory=True)
         del plan
         host = HostHandoff(kv_h, kc_h, vc_h, slots, dev, KvPrecision(args.bits), args.group,
-                           n_chunks=max(args.chunks, 8))
+                           n_chunks=args.e2e_chunks)
         for _ in range(max(1, min(args.warmup, 3))):
             host.run()
         torch.cuda.synchronize()
@@ -369,6 +369,8 @@ def main():
     ap.add_argument("--k3", default="ldg", choices=["ldg", "bulk"],
                     help="N=1: K3 variant (per-lane loads or TMA bulk staging)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunks", type=int, default=32,
+                    help="N=1 e2e: layer chunks for H2D/compute/D2H overlap")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-layers", type=int, default=None,
                     help="reference arm: layers per step (default: ~1 GB of fp16 KV)")

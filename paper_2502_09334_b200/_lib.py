@@ -65,7 +65,7 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = path or SO_PATH
+        p = path or os.environ.get("KVX_LIB") or SO_PATH
         if not os.path.exists(p):
             raise ImportError(
                 f"{p} not built: run `python -m paper_2502_09334_b200.build` "

@@ -37,18 +37,27 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: tuple = ()) -> str:
+    """Build _kvx.so (or _kvx_<variant>.so with extra -D defines, for A/B runs
+    selected at run time with KVX_LIB=<path>)."""
+    out = SO_PATH if variant is None else os.path.join(HERE, f"_kvx_{variant}.so")
+    if variant is None and not force and not stale():
         return SO_PATH
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", SO_PATH, *SOURCES]
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError(f"nvcc failed ({r.returncode}): {' '.join(cmd)}")
     if verbose:
         sys.stderr.write(r.stderr)
-    return SO_PATH
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], tuple(sys.argv[i + 2:])
+        print(build(variant=name, defines=defs))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

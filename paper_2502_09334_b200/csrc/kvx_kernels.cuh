@@ -337,7 +337,10 @@ __device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)
 }
 
 template <int BITS, int G>
-__global__ void __launch_bounds__(256) quant_pack_kernel(Geo g, ItemGeo ig,
+#ifndef KVX_K1_MIN_BLOCKS
+#define KVX_K1_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo g, ItemGeo ig,
                                                          uint8_t* __restrict__ codes,
                                                          __half* __restrict__ scale,
                                                          __half* __restrict__ zero) {
