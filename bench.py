@@ -317,18 +317,33 @@ def run_local(args, torch):
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_reference(wl, args.bits, args.group, budget_s=args.cpu_budget)
+    traffic = ncu_traffic(wl, args, dom)
     return dict(
         value=value, ms=ms, workload=wl, fp16_bytes=fp16_bytes, wire_bytes=lay.wire_bytes,
         launches=launches_per_step * args.steps, clocks=clk.summary(), e2e=e2e, cpu=cpu,
         roofline={"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                   "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                  "frac": round(achieved / hbm, 4), "traffic": None,
+                  "frac": round(achieved / hbm, 4), "traffic": traffic,
+                  "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram read+write "
+                                    "per launch)" if traffic else None,
                   "algorithmic_bytes_per_launch": kernel_bytes // len(plan_chunks(args, L)),
                   "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
                   "step_roofline_ms": round(roof_ms, 4), "step_frac": round(roof_ms / ms, 4)},
         extra={"n_chunks": args.chunks, "mode": "local", "k3": args.k3,
                "verified_sampled_rows_bit_exact": verified},
     )
+
+
+def ncu_traffic(workload, args, kernel):
+    """DRAM traffic per launch of ``kernel`` from the committed ncu capture of
+    this exact configuration (bench.py cannot run ncu itself), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            doc = json.load(f)
+        key = f"{workload}/bits{args.bits}/g{args.group}/chunks{args.chunks}"
+        return int(doc["configs"][key][kernel]["traffic_bytes"])
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def verify_local(torch, kv, kc, vc, slots, args):

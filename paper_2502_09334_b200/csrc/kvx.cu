@@ -145,9 +145,15 @@ cudaError_t launch_dequant(const kvx::Geo& g, const void* codes, const void* sca
   return cudaGetLastError();
 }
 
-constexpr int kBulkStages = 4;
+#ifndef KVX_BULK_STAGES
+#define KVX_BULK_STAGES 4
+#endif
+#ifndef KVX_BULK_STAGE_BYTES
+#define KVX_BULK_STAGE_BYTES 16384
+#endif
+constexpr int kBulkStages = KVX_BULK_STAGES;
 constexpr int kBulkThreads = 288;
-constexpr int kBulkStageTarget = 16384;  // code bytes per stage
+constexpr int kBulkStageTarget = KVX_BULK_STAGE_BYTES;  // code bytes per stage
 
 template <int BITS, int G>
 cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale, const void* zero,
