@@ -63,7 +63,7 @@ int valid_format(int head_dim, int group, int bits) {
 
 int make_geo(kvx::Geo& g, const void* k, const void* v, int64_t layer_stride, const int64_t* slots,
              int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim, int group, int bits,
-             int64_t payload_layer_stride) {
+             int64_t payload_layer_stride, int planes = 2, int plane0 = 0) {
   if (n_layers < 0 || n_tokens < 0 || n_heads <= 0) return KVX_ERR_INVALID_ARG;
   const int64_t row_elems = int64_t(n_heads) * head_dim;
   if (row_elems > (int64_t(1) << 30)) return KVX_ERR_INVALID_ARG;
@@ -76,12 +76,14 @@ int make_geo(kvx::Geo& g, const void* k, const void* v, int64_t layer_stride, co
   g.layer_stride_b = layer_stride * 2;
   g.slots = slots;
   g.n_tokens = n_tokens;
-  g.n_token_rows = n_layers * 2 * n_tokens;
+  g.planes = planes;
+  g.plane0 = plane0;
+  g.n_token_rows = n_layers * planes * n_tokens;
   g.row_elems = int(row_elems);
   g.vecs = int(row_elems / 8);
   // Payload layer strides: dense per-array layout when payload_layer_stride == 0,
   // else one segment per layer holding [codes | scale | zero].
-  const int64_t rows_per_layer = 2 * n_tokens * n_heads;
+  const int64_t rows_per_layer = planes * n_tokens * n_heads;
   const int64_t ng = bits == 16 ? 0 : head_dim / group;
   if (payload_layer_stride < 0) return KVX_ERR_INVALID_ARG;
   if (payload_layer_stride == 0) {
@@ -170,7 +172,7 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   if (bg.code_row_bytes % 16 || bg.meta_row_bytes % 16 || !aligned(codes, 16) ||
       !aligned(scale, 16) || !aligned(zero, 16) || g.codes_ls % 16 || g.meta_ls % 16)
     return cudaSuccess;  // not bulk-copyable: caller falls back to the LDG kernel
-  const int64_t two_t = 2 * g.n_tokens;
+  const int64_t two_t = int64_t(g.planes) * g.n_tokens;
   int64_t r = kBulkStageTarget / bg.code_row_bytes;
   if (r < 1) r = 1;
   if (r > two_t) r = two_t;

@@ -127,19 +127,27 @@ struct Geo {
   int64_t meta_ls;         // payload: bytes between layers of scale / zero
   int row_elems;           // n_heads * head_dim
   int vecs;                // row_elems / 8
+  int planes;              // planes per layer in this launch: 2 (K and V) or 1
+  int plane0;              // first plane: 0 = K, 1 = V (planes == 1: which one)
 };
+
+__device__ __forceinline__ const char* plane_ptr(const Geo& g, int kv, int64_t layer) {
+  return (kv ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
+}
 
 __device__ __forceinline__ int64_t pos_of(const Geo& g, int64_t t) {
   return g.slots ? __ldg(g.slots + t) : t;
 }
 
-// Token row tr = (l*2 + kv)*T + t -> (layer, row index inside the layer's payload).
-__device__ __forceinline__ void split_tr(const Geo& g, int64_t tr, int64_t& lk, int64_t& t,
+// Token row tr = (l*planes + p)*T + t -> (plane kv, layer, row inside the
+// layer's payload).
+__device__ __forceinline__ void split_tr(const Geo& g, int64_t tr, int& kv, int64_t& t,
                                          int64_t& layer, int64_t& lrow) {
-  lk = tr / g.n_tokens;
+  const int64_t lk = tr / g.n_tokens;
   t = tr - lk * g.n_tokens;
-  layer = lk >> 1;
-  lrow = tr - layer * 2 * g.n_tokens;
+  layer = lk >> (g.planes - 1);
+  kv = g.plane0 + int(lk - (layer << (g.planes - 1)));
+  lrow = tr - layer * g.planes * g.n_tokens;
 }
 
 // ---------------------------------------------------------------------------
@@ -271,10 +279,11 @@ __device__ __forceinline__ K1Item k1_item(const Geo& g, const ItemGeo& ig, uint3
   const int c = int(item - tr * ig.ipr.d) * 32 + lane;  // chunk inside the token row
   const uint32_t lk = fdiv(tr, ig.tokens);
   const uint32_t t = tr - lk * ig.tokens.d;
-  const uint32_t layer = lk >> 1;
-  const uint32_t lrow = tr - layer * 2 * ig.tokens.d;
+  const uint32_t layer = lk >> (g.planes - 1);
+  const int kv = g.plane0 + int(lk - (layer << (g.planes - 1)));
+  const uint32_t lrow = tr - layer * g.planes * ig.tokens.d;
   const int64_t pos = pos_of(g, t);
-  const char* plane = ((lk & 1) ? g.v_plane : g.k_plane) + int64_t(layer) * g.layer_stride_b;
+  const char* plane = plane_ptr(g, kv, layer);
   it.active = c < ig.cpr;
   it.src = plane + pos * int64_t(g.row_elems) * 2 + int64_t(c) * 64;
   it.codes = reinterpret_cast<char*>(codes) + int64_t(layer) * g.codes_ls +
@@ -389,10 +398,11 @@ __global__ void __launch_bounds__(256) pack16_kernel(Geo g, uint8_t* __restrict_
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t tr = warp; tr < g.n_token_rows; tr += n_warps) {
-    int64_t lk, t, layer, lrow;
-    split_tr(g, tr, lk, t, layer, lrow);
+    int kv;
+    int64_t t, layer, lrow;
+    split_tr(g, tr, kv, t, layer, lrow);
     const int64_t pos = pos_of(g, t);
-    const char* plane = ((lk & 1) ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
+    const char* plane = plane_ptr(g, kv, layer);
     const U4* src = reinterpret_cast<const U4*>(plane + pos * int64_t(g.row_elems) * 2);
     U4* dst = reinterpret_cast<U4*>(out + layer * g.codes_ls) + lrow * g.vecs;
     for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
@@ -437,10 +447,11 @@ __device__ __forceinline__ K3Item k3_item(const Geo& g, const ItemGeo& ig, uint3
   const int c = int(item - tr * ig.ipr.d) * 32 + lane;
   const uint32_t lk = fdiv(tr, ig.tokens);
   const uint32_t t = tr - lk * ig.tokens.d;
-  const uint32_t layer = lk >> 1;
-  const uint32_t lrow = tr - layer * 2 * ig.tokens.d;
+  const uint32_t layer = lk >> (g.planes - 1);
+  const int kv = g.plane0 + int(lk - (layer << (g.planes - 1)));
+  const uint32_t lrow = tr - layer * g.planes * ig.tokens.d;
   const int64_t pos = pos_of(g, t);
-  char* plane = const_cast<char*>((lk & 1) ? g.v_plane : g.k_plane) + int64_t(layer) * g.layer_stride_b;
+  char* plane = const_cast<char*>(plane_ptr(g, kv, layer));
   it.active = (c < ig.cpr) && (pos >= 0);  // pos < 0: padding token, skipped
   it.dst = plane + pos * int64_t(g.row_elems) * 2 + int64_t(c) * 64;
   it.codes = reinterpret_cast<const char*>(codes) + int64_t(layer) * g.codes_ls +
@@ -547,11 +558,12 @@ __global__ void __launch_bounds__(256) scatter16_kernel(Geo g, const uint8_t* __
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t tr = warp; tr < g.n_token_rows; tr += n_warps) {
-    int64_t lk, t, layer, lrow;
-    split_tr(g, tr, lk, t, layer, lrow);
+    int kv;
+    int64_t t, layer, lrow;
+    split_tr(g, tr, kv, t, layer, lrow);
     const int64_t pos = pos_of(g, t);
     if (pos < 0) continue;
-    char* plane = const_cast<char*>((lk & 1) ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
+    char* plane = const_cast<char*>(plane_ptr(g, kv, layer));
     U4* dst = reinterpret_cast<U4*>(plane + pos * int64_t(g.row_elems) * 2);
     const U4* src = reinterpret_cast<const U4*>(in + layer * g.codes_ls) + lrow * g.vecs;
     for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
@@ -663,7 +675,7 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int64_t two_t = 2 * g.n_tokens;
+  const int64_t two_t = int64_t(g.planes) * g.n_tokens;  // payload rows per layer
 
   if (warp == CONSUMERS) {  // ---- producer: one elected thread
     if (lane == 0) {
@@ -710,12 +722,12 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     mbar_wait(&full[st], (k / STAGES) & 1);
     for (int r = warp; r < rows; r += CONSUMERS) {
       const int64_t lrow = r0 + r;
-      const int kv = lrow >= g.n_tokens;
-      const int64_t t = lrow - kv * g.n_tokens;
+      const int p = lrow >= g.n_tokens;
+      const int kv = g.plane0 + p;
+      const int64_t t = lrow - p * g.n_tokens;
       const int64_t pos = pos_of(g, t);
       if (pos < 0) continue;  // padding token
-      char* dst = const_cast<char*>(kv ? g.v_plane : g.k_plane) + int64_t(layer) * g.layer_stride_b +
-                  pos * int64_t(g.row_elems) * 2;
+      char* dst = const_cast<char*>(plane_ptr(g, kv, layer)) + pos * int64_t(g.row_elems) * 2;
       const uint8_t* crow = buf + r * bg.code_row_bytes;
       const int gpr = bg.meta_row_bytes / 2;
       for (int c = lane; c < bg.cpr; c += 32) {

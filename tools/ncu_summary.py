@@ -58,5 +58,36 @@ def report(path: str):
         print(f"| {short(r[ki])} | " + " | ".join(r[i] for _, i in cols) + " |")
 
 
+def traffic(path: str, key: str, out: str = "profiles/ncu_traffic.json"):
+    """Merge DRAM traffic per launch of K1/K3 from a report into ncu_traffic.json."""
+    import json
+    import os
+    rep = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(rep)))
+    hdr, units = rows[0], rows[1]
+    ki = hdr.index("Kernel Name")
+    r, w, d = (hdr.index(k) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum",
+                                       "gpu__time_duration.sum"))
+    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+    res = {}
+    for row in rows[2:]:
+        n = row[ki]
+        name = ("quant_pack" if "quant_pack" in n else
+                "pull_dequant_scatter_paged" if "pull_dequant" in n else "dequant_scatter_paged")
+        rb, wb = float(row[r]) * scale[units[r]], float(row[w]) * scale[units[w]]
+        res[name] = {"dram_read_bytes": int(rb), "dram_write_bytes": int(wb),
+                     "traffic_bytes": int(rb + wb), "ncu_duration_ms": float(row[d])}
+    doc = json.load(open(out)) if os.path.exists(out) else {"configs": {}}
+    doc["configs"].setdefault(key, {}).update(res)
+    doc["source_" + key] = os.path.basename(path)
+    json.dump(doc, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
+    cmd = sys.argv[1]
+    if cmd == "traffic":
+        traffic(sys.argv[2], sys.argv[3])
+    else:
+        {"launches": launches, "report": report}[cmd](sys.argv[2])
