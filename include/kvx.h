@@ -127,6 +127,33 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
 /* 1 if kvx_pull_dequant_scatter_paged can bulk-stage this shape. */
 int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, int bits);
 
+/*
+ * "kivi" format (KIVI-style): K quantised PER CHANNEL over
+ * groups of `group` (32|64) consecutive tokens of one request -- the group
+ * starts are group_starts[n_groups] in batch token order -- and each request's
+ * last n % group tokens (residual_tokens[n_residual]) sent as fp16; V per
+ * token (group along head_dim) as in the default format.  bits in {4, 8};
+ * dense sources only.  Payload: one segment per layer (payload_layer_stride
+ * bytes) holding seven 16-B aligned sub-arrays at seg_offsets[7] (host array):
+ *   Kc u8 [n_groups*group][H][D*bits/8] (group-major rows)
+ *   Ks, Kz f16 [n_groups][H][D]   Kr f16 [n_residual][H][D]
+ *   Vc u8 [T][H][D*bits/8]        Vs, Vz f16 [T][H][D/group]
+ * Decode side: dst_slots[T] for every token, residual_dst_slots[n_residual]
+ * = dst_slots[residual_tokens].
+ */
+int kvx_quant_pack_kivi(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                        int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim, int group,
+                        int bits, const int64_t* group_starts, int64_t n_groups,
+                        const int64_t* residual_tokens, int64_t n_residual, void* payload,
+                        int64_t payload_layer_stride, const int64_t* seg_offsets, void* stream);
+int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_stride,
+                                   const int64_t* seg_offsets, const int64_t* dst_slots,
+                                   const int64_t* group_starts, int64_t n_groups,
+                                   const int64_t* residual_dst_slots, int64_t n_residual,
+                                   int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                                   int group, int bits, void* k_cache, void* v_cache,
+                                   int64_t dst_layer_stride, void* stream);
+
 /* Packed payload sizes in bytes for n_rows rows (codes, scale, zero). */
 int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t* codes_bytes,
                      int64_t* scale_bytes, int64_t* zero_bytes);

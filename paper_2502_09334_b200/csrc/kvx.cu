@@ -10,6 +10,7 @@
 
 #include "../../include/kvx.h"
 #include "kvx_kernels.cuh"
+#include "kvx_kivi.cuh"
 
 namespace {
 
@@ -256,6 +257,34 @@ void resolve_driver() {
   });
 }
 
+int kivi_check(int head_dim, int group, int bits) {
+  if (bits != 4 && bits != 8) return KVX_ERR_INVALID_ARG;
+  if (group != 32 && group != 64) return KVX_ERR_INVALID_ARG;
+  if (head_dim <= 0 || head_dim % 32 || head_dim % group) return KVX_ERR_INVALID_ARG;
+  return KVX_OK;
+}
+
+template <int BITS, int G>
+cudaError_t launch_kchan_quant(const kvx::KchanGeo& kg, cudaStream_t s) {
+  const int cblocks = (kg.row_elems + 255) / 256;
+  const int64_t items = kg.n_layers * kg.n_groups * cblocks;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int64_t grid = int64_t(sm_count(dev)) * 8;
+  if (grid > items) grid = items;
+  kvx::quant_pack_kchan_kernel<BITS, G><<<unsigned(grid), 128, 0, s>>>(kg);
+  return cudaGetLastError();
+}
+
+template <int BITS, int G>
+cudaError_t launch_kchan_dequant(const kvx::KchanGeo& kg, const int64_t* slots, void* kc,
+                                        int64_t dst_ls_b, cudaStream_t s) {
+  auto k = kvx::dequant_kchan_kernel<BITS, G>;
+  const int64_t rows = kg.n_layers * kg.n_groups * G;
+  k<<<grid_for(k, rows), kThreads, 0, s>>>(kg, slots, static_cast<char*>(kc), dst_ls_b);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 extern "C" {
@@ -396,6 +425,131 @@ int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, i
   if (valid_format(head_dim, group, bits) || bits == 16 || n_tokens < 1) return 0;
   const int64_t row = int64_t(n_heads) * head_dim;
   return (row * bits / 8) % 16 == 0 && (row / group * 2) % 16 == 0;
+}
+
+// ---- "kivi" format: per-channel K groups + fp16 residual window, V per token --
+
+int kvx_quant_pack_kivi(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                        int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim, int group,
+                        int bits, const int64_t* group_starts, int64_t n_groups,
+                        const int64_t* residual_tokens, int64_t n_residual, void* payload,
+                        int64_t payload_layer_stride, const int64_t* seg_offsets, void* stream) {
+  int rc = kivi_check(head_dim, group, bits);
+  if (rc) return rc;
+  if (n_layers < 0 || n_tokens < 0 || n_heads <= 0 || n_groups < 0 || n_residual < 0 ||
+      n_groups * group + n_residual != n_tokens || !seg_offsets || payload_layer_stride % 16)
+    return KVX_ERR_INVALID_ARG;
+  if (n_layers == 0 || n_tokens == 0) return KVX_OK;
+  if (!k_src || !v_src || !payload || (n_groups && !group_starts) || (n_residual && !residual_tokens))
+    return KVX_ERR_INVALID_ARG;
+  for (int i = 0; i < 7; ++i)
+    if (seg_offsets[i] < 0 || seg_offsets[i] % 16) return KVX_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(payload);
+  const int row_elems = n_heads * head_dim;
+  cudaError_t e = cudaSuccess;
+  if (n_groups) {
+    kvx::KchanGeo kg;
+    kg.k_plane = static_cast<const char*>(k_src);
+    kg.layer_stride_b = src_layer_stride * 2;
+    kg.group_starts = group_starts;
+    kg.n_groups = n_groups;
+    kg.row_elems = row_elems;
+    kg.n_layers = n_layers;
+    kg.codes = base + seg_offsets[0];
+    kg.scale = base + seg_offsets[1];
+    kg.zero = base + seg_offsets[2];
+    kg.payload_ls = payload_layer_stride;
+    if (bits == 4) e = group == 32 ? launch_kchan_quant<4, 32>(kg, s) : launch_kchan_quant<4, 64>(kg, s);
+    else e = group == 32 ? launch_kchan_quant<8, 32>(kg, s) : launch_kchan_quant<8, 64>(kg, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (n_residual) {  // residual window: fp16 rows gathered into the payload
+    kvx::Geo g;
+    rc = make_geo(g, k_src, k_src, src_layer_stride, residual_tokens, n_layers, n_residual, n_heads,
+                  head_dim, group, 16, payload_layer_stride, 1, 0);
+    if (rc) return rc;
+    auto k = kvx::pack16_kernel<kUnroll>;
+    k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, reinterpret_cast<uint8_t*>(base + seg_offsets[3]));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  {  // V per token
+    kvx::Geo g;
+    rc = make_geo(g, v_src, v_src, src_layer_stride, nullptr, n_layers, n_tokens, n_heads, head_dim,
+                  group, bits, payload_layer_stride, 1, 1);
+    if (rc) return rc;
+    e = bits == 4 ? dispatch_quant<4>(group, g, base + seg_offsets[4], base + seg_offsets[5],
+                                      base + seg_offsets[6], s)
+                  : dispatch_quant<8>(group, g, base + seg_offsets[4], base + seg_offsets[5],
+                                      base + seg_offsets[6], s);
+  }
+  return e;
+}
+
+int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_stride,
+                                   const int64_t* seg_offsets, const int64_t* dst_slots,
+                                   const int64_t* group_starts, int64_t n_groups,
+                                   const int64_t* residual_dst_slots, int64_t n_residual,
+                                   int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                                   int group, int bits, void* k_cache, void* v_cache,
+                                   int64_t dst_layer_stride, void* stream) {
+  int rc = kivi_check(head_dim, group, bits);
+  if (rc) return rc;
+  if (n_layers < 0 || n_tokens < 0 || n_heads <= 0 || n_groups < 0 || n_residual < 0 ||
+      n_groups * group + n_residual != n_tokens || !seg_offsets || payload_layer_stride % 16)
+    return KVX_ERR_INVALID_ARG;
+  if (n_layers == 0 || n_tokens == 0) return KVX_OK;
+  if (!payload || !dst_slots || !k_cache || !v_cache || !aligned(k_cache, 32) ||
+      !aligned(v_cache, 32) || (dst_layer_stride * 2) % 32 || (n_groups && !group_starts) ||
+      (n_residual && !residual_dst_slots))
+    return KVX_ERR_INVALID_ARG;
+  for (int i = 0; i < 7; ++i)
+    if (seg_offsets[i] < 0 || seg_offsets[i] % 16) return KVX_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const char* base = static_cast<const char*>(payload);
+  cudaError_t e = cudaSuccess;
+  if (n_groups) {
+    kvx::KchanGeo kg;
+    kg.k_plane = nullptr;
+    kg.layer_stride_b = 0;
+    kg.group_starts = group_starts;
+    kg.n_groups = n_groups;
+    kg.row_elems = n_heads * head_dim;
+    kg.n_layers = n_layers;
+    kg.codes = const_cast<char*>(base + seg_offsets[0]);
+    kg.scale = const_cast<char*>(base + seg_offsets[1]);
+    kg.zero = const_cast<char*>(base + seg_offsets[2]);
+    kg.payload_ls = payload_layer_stride;
+    const int64_t dls = dst_layer_stride * 2;
+    if (bits == 4)
+      e = group == 32 ? launch_kchan_dequant<4, 32>(kg, dst_slots, k_cache, dls, s)
+                      : launch_kchan_dequant<4, 64>(kg, dst_slots, k_cache, dls, s);
+    else
+      e = group == 32 ? launch_kchan_dequant<8, 32>(kg, dst_slots, k_cache, dls, s)
+                      : launch_kchan_dequant<8, 64>(kg, dst_slots, k_cache, dls, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (n_residual) {
+    kvx::Geo g;
+    rc = make_geo(g, k_cache, k_cache, dst_layer_stride, residual_dst_slots, n_layers, n_residual,
+                  n_heads, head_dim, group, 16, payload_layer_stride, 1, 0);
+    if (rc) return rc;
+    auto k = kvx::scatter16_kernel<kUnroll>;
+    k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(
+        g, reinterpret_cast<const uint8_t*>(base + seg_offsets[3]));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  {
+    kvx::Geo g;
+    rc = make_geo(g, v_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
+                  head_dim, group, bits, payload_layer_stride, 1, 1);
+    if (rc) return rc;
+    e = bits == 4 ? dispatch_dequant<4>(group, g, base + seg_offsets[4], base + seg_offsets[5],
+                                        base + seg_offsets[6], s)
+                  : dispatch_dequant<8>(group, g, base + seg_offsets[4], base + seg_offsets[5],
+                                        base + seg_offsets[6], s);
+  }
+  return e;
 }
 
 // ---- transport -------------------------------------------------------------

@@ -1,0 +1,175 @@
+// "kivi" format kernels (PAPER.md:490-492 borrows KIVI):
+// keys quantised PER CHANNEL over groups of G consecutive tokens of one
+// request (the request's last n % G tokens travel as fp16, the residual
+// window), values per token as in the default format.  Same scalar
+// arithmetic as K1/K3 (bit-exact with oracle/kvq_oracle.py quant_pack_kivi).
+#pragma once
+
+#include "kvx_kernels.cuh"
+
+namespace kvx {
+
+struct KchanGeo {
+  const char* k_plane;      // K plane of layer 0 (dense source [T, H*D] per layer)
+  int64_t layer_stride_b;   // bytes between source layers
+  const int64_t* group_starts;  // [n_groups] first token of each group (batch order)
+  int64_t n_groups;
+  int row_elems;            // H*D
+  int64_t n_layers;
+  char* codes;              // payload: Kc of layer 0
+  char* scale;              // Ks of layer 0
+  char* zero;               // Kz of layer 0
+  int64_t payload_ls;       // bytes between payload layers
+};
+
+// One thread = 2 adjacent channels x G tokens (G half2 registers): one pass,
+// min/max along tokens, then quantise from registers.  A block of 128
+// threads covers 256 channels of one (layer, group).
+template <int BITS, int G>
+__global__ void __launch_bounds__(128) quant_pack_kchan_kernel(KchanGeo g) {
+  constexpr uint32_t QMAX = (1u << BITS) - 1u;
+  constexpr float QMAXF = float(QMAX);
+  const int cblocks = (g.row_elems + 255) / 256;
+  const int64_t n_items = g.n_layers * g.n_groups * cblocks;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int64_t lg = item / cblocks;
+    const int cb = int(item - lg * cblocks);
+    const int64_t layer = lg / g.n_groups;
+    const int64_t k = lg - layer * g.n_groups;
+    const int ch = cb * 256 + threadIdx.x * 2;
+    const bool active = ch < g.row_elems;
+    const int64_t t0 = __ldg(g.group_starts + k);
+    const char* src = g.k_plane + layer * g.layer_stride_b + (t0 * g.row_elems + ch) * 2;
+    uint32_t w[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+      w[j] = active ? __ldg(reinterpret_cast<const uint32_t*>(src + int64_t(j) * g.row_elems * 2))
+                    : 0u;
+    __half2 mn = u32_as_h2(w[0]), mx = u32_as_h2(w[0]);
+#pragma unroll
+    for (int j = 1; j < G; ++j) {
+      mn = __hmin2(mn, u32_as_h2(w[j]));
+      mx = __hmax2(mx, u32_as_h2(w[j]));
+    }
+    float zf[2], inv[2];
+    __half z16[2], s16[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float fmn = h ? __high2float(mn) : __low2float(mn);
+      const float fmx = h ? __high2float(mx) : __low2float(mx);
+      z16[h] = __float2half_rn(__fadd_rn(fmn, 0.0f));
+      s16[h] = __float2half_rn(__fadd_rn(__fdiv_rn(__fsub_rn(fmx, fmn), QMAXF), 0.0f));
+      const float s = __half2float(s16[h]);
+      inv[h] = (s != 0.0f) ? __frcp_rn(s) : 0.0f;
+      zf[h] = __half2float(z16[h]);
+    }
+    const bool sub = active && ((__half2float(s16[0]) != 0.0f && __half2float(s16[0]) < 6.103515625e-05f) ||
+                                (__half2float(s16[1]) != 0.0f && __half2float(s16[1]) < 6.103515625e-05f));
+    const bool clamp = __any_sync(0xffffffffu, sub);
+    if (active) {
+      char* lc = g.codes + layer * g.payload_ls;
+      const int64_t meta = (k * g.row_elems + ch) * 2;
+      *reinterpret_cast<__half2*>(g.scale + layer * g.payload_ls + meta) = __halves2half2(s16[0], s16[1]);
+      *reinterpret_cast<__half2*>(g.zero + layer * g.payload_ls + meta) = __halves2half2(z16[0], z16[1]);
+      unsigned long long invv;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(invv) : "f"(inv[0]), "f"(inv[1]));
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        unsigned long long x, r;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(sub_lo(w[j], zf[0])), "f"(sub_hi(w[j], zf[1])));
+        asm("{.reg .b64 mg; mov.b64 mg, {%3, %3}; fma.rn.f32x2 %0, %1, %2, mg;}"
+            : "=l"(r) : "l"(x), "l"(invv), "f"(8388608.0f));
+        uint32_t b0 = uint32_t(r), b1 = uint32_t(r >> 32);
+        if (clamp) {
+          b0 = min(b0 - 0x4B000000u, QMAX);
+          b1 = min(b1 - 0x4B000000u, QMAX);
+        }
+        const int64_t row = k * G + j;  // group-major payload row
+        if constexpr (BITS == 4) {
+          lc[(row * g.row_elems + ch) / 2] = char(lea4(b1, b0));
+        } else {
+          *reinterpret_cast<uint16_t*>(lc + row * g.row_elems + ch) =
+              uint16_t(prmt(b0, b1, 0x0040u));
+        }
+      }
+    }
+  }
+}
+
+// Dequantise per-channel-grouped K rows into the paged cache.  Warp per
+// payload row (group k, token j), lane owns 32 channels: 16 B of codes plus
+// 64 B of scales and 64 B of zeros (shared by the group's G rows, L1 hits).
+template <int BITS, int G>
+__global__ void __launch_bounds__(256) dequant_kchan_kernel(KchanGeo g, const int64_t* dst_slots,
+                                                           char* k_cache, int64_t dst_layer_stride_b) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int cpr = g.row_elems / 32;
+  const int64_t rows = g.n_layers * g.n_groups * G;
+  const __half2 k1024 = u32_as_h2(0x64006400u), kmax = u32_as_h2(0x7BFF7BFFu);
+  for (int64_t r = warp; r < rows; r += n_warps) {
+    const int64_t layer = r / (g.n_groups * G);
+    const int64_t q = r - layer * g.n_groups * G;  // row inside the layer
+    const int64_t k = q / G;
+    const int64_t t = __ldg(g.group_starts + k) + (q - k * G);
+    const int64_t pos = __ldg(dst_slots + t);
+    if (pos < 0) continue;
+    const char* lc = g.codes + layer * g.payload_ls + q * g.row_elems * BITS / 8;
+    const char* ls = g.scale + layer * g.payload_ls + k * g.row_elems * 2;
+    const char* lz = g.zero + layer * g.payload_ls + k * g.row_elems * 2;
+    char* dst = k_cache + layer * dst_layer_stride_b + pos * g.row_elems * 2;
+    for (int c = lane; c < cpr; c += 32) {
+      uint32_t cw[BITS];  // 32 codes
+      if constexpr (BITS == 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(lc + c * 16);
+        cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
+      } else {
+        const uint4 v0 = reinterpret_cast<const uint4*>(lc + c * 32)[0];
+        const uint4 v1 = reinterpret_cast<const uint4*>(lc + c * 32)[1];
+        cw[0] = v0.x; cw[1] = v0.y; cw[2] = v0.z; cw[3] = v0.w;
+        cw[4] = v1.x; cw[5] = v1.y; cw[6] = v1.z; cw[7] = v1.w;
+      }
+      uint32_t sw[16], zw[16];  // half2 (scale, zero) pairs for the 32 channels
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 a = reinterpret_cast<const uint4*>(ls + c * 64)[i];
+        const uint4 b = reinterpret_cast<const uint4*>(lz + c * 64)[i];
+        sw[4 * i] = a.x; sw[4 * i + 1] = a.y; sw[4 * i + 2] = a.z; sw[4 * i + 3] = a.w;
+        zw[4 * i] = b.x; zw[4 * i + 1] = b.y; zw[4 * i + 2] = b.z; zw[4 * i + 3] = b.w;
+      }
+      U4 o[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {  // 8 elements per output vector
+        uint32_t p[4];
+        if constexpr (BITS == 4) {
+          const uint32_t cc = cw[v];
+          const uint32_t a0 = lop3_and_or(cc, 0x000F000Fu, 0x64006400u);
+          const uint32_t a1 = lop3_and_or(cc >> 4, 0x000F000Fu, 0x64006400u);
+          const uint32_t a2 = lop3_and_or(cc >> 8, 0x000F000Fu, 0x64006400u);
+          const uint32_t a3 = lop3_and_or(cc >> 12, 0x000F000Fu, 0x64006400u);
+          p[0] = prmt(a0, a1, 0x5410);
+          p[1] = prmt(a2, a3, 0x5410);
+          p[2] = prmt(a0, a1, 0x7632);
+          p[3] = prmt(a2, a3, 0x7632);
+        } else {
+          p[0] = prmt(cw[2 * v], 0x64646464u, 0x4140);
+          p[1] = prmt(cw[2 * v], 0x64646464u, 0x4342);
+          p[2] = prmt(cw[2 * v + 1], 0x64646464u, 0x4140);
+          p[3] = prmt(cw[2 * v + 1], 0x64646464u, 0x4342);
+        }
+        uint32_t* ov = &o[v].x;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const __half2 qh = __hsub2(u32_as_h2(p[i]), k1024);
+          const __half2 y = __hfma2(qh, u32_as_h2(sw[4 * v + i]), u32_as_h2(zw[4 * v + i]));
+          ov[i] = h2_as_u32(__hmin2(y, kmax));
+        }
+      }
+      st256(dst + c * 64, o[0], o[1]);
+      st256(dst + c * 64 + 32, o[2], o[3]);
+    }
+  }
+}
+
+}  // namespace kvx

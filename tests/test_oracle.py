@@ -179,3 +179,23 @@ def test_scatter_paged_oracles_agree():
     assert np.array_equal(h16(kc), h16(kc2)) and np.array_equal(h16(vc), h16(vc2))
     flat = kc.reshape(L, nb * bs, H, D)
     assert np.array_equal(flat[:, slots[0]], rows[:, 0, 0])
+
+
+def test_kivi_oracle_layout_and_accuracy():
+    from paper_2502_09334_b200.kivi import KiviLayout, kivi_groups
+    seq = (70, 64, 0, 66)
+    gs, rt = O.kivi_groups(seq, 32)
+    gs2, rt2 = kivi_groups(seq, 32)
+    assert np.array_equal(gs, gs2) and np.array_equal(rt, rt2)
+    assert list(gs) == [0, 32, 70, 102, 134, 166] and list(rt) == [64, 65, 66, 67, 68, 69, 198, 199]
+    kv = O.synthetic_kv(2, 200, 4, 128, seed=1)
+    p = O.quant_pack_kivi(kv, 4, 32, seq)
+    lay = KiviLayout(2, 4, 128, 4, 32, seq)
+    for name, size in zip(("Kc", "Ks", "Kz", "Kr", "Vc", "Vs", "Vz"), lay.sizes):
+        assert p[name].nbytes == 2 * size, name
+    K, V = O.unpack_dequant_kivi(p, 4, 32, seq, 4, 128)
+    assert np.array_equal(K[:, rt], kv[:, 0][:, rt])  # residual window is exact
+    e_kivi = np.abs(K.astype(np.float64) - kv[:, 0]).mean()
+    c, s, z = O.quant_pack(kv[:, 0].reshape(-1, 128), 4, 32)
+    e_tok = np.abs(O.unpack_dequant(c, s, z, 4, 32, 128).astype(np.float64) - kv[:, 0].reshape(-1, 128)).mean()
+    assert e_kivi < 0.75 * e_tok  # per-channel K isolates the outlier channels
