@@ -258,9 +258,13 @@ def run_local(args, torch):
     slots, nb = paged_slots(torch, T, dev)
     kc = torch.zeros((L, nb, BLOCK, H, D), dtype=torch.float16, device=dev)
     vc = torch.zeros_like(kc)
-    plan = HandoffPlan(KVPlanes.dense(kv), KVPlanes.paged(kc, vc, slots), T,
-                       KvPrecision(args.bits), args.group, mode="local", n_chunks=args.chunks,
-                       bulk=(args.k3 == "bulk"))
+    if args.format == "kivi":
+        from paper_2502_09334_b200.kivi import KiviHandoff
+        plan = KiviHandoff(kv, kc, vc, slots, KvPrecision(args.bits), args.group, (s,) * b)
+    else:
+        plan = HandoffPlan(KVPlanes.dense(kv), KVPlanes.paged(kc, vc, slots), T,
+                           KvPrecision(args.bits), args.group, mode="local", n_chunks=args.chunks,
+                           bulk=(args.k3 == "bulk"))
     lay = plan.layout
     fp16_bytes = lay.fp16_bytes
     for _ in range(args.warmup):
@@ -276,7 +280,7 @@ def run_local(args, torch):
         end.record()
         torch.cuda.synchronize()
     ms = start.elapsed_time(end) / args.steps
-    launches_per_step = 2 * len(plan.chunks)
+    launches_per_step = 6 if args.format == "kivi" else 2 * len(plan.chunks)
     k1 = sum(e["k1"][0].elapsed_time(e["k1"][1]) for e in timing) / args.steps
     k3 = sum(e["k3"][0].elapsed_time(e["k3"][1]) for e in timing) / args.steps
     kernel_bytes = fp16_bytes + lay.wire_bytes  # K1 reads fp16, writes payload; K3 the reverse
@@ -286,11 +290,12 @@ def run_local(args, torch):
     step_bytes = 2 * kernel_bytes  # algorithmic HBM bytes of the round trip
     roof_ms = step_bytes / (hbm * 1e9) * 1e3
     value = fp16_bytes / (ms * 1e-3) / 1e9
-    verified = None if args.no_verify else verify_local(torch, kv, kc, vc, slots, args)
+    verified = None if (args.no_verify or args.format == "kivi") else verify_local(
+        torch, kv, kc, vc, slots, args)
 
     # e2e: the same hand-off from pinned host KV to a host paged cache
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.format == "default":
         kv_h = torch.empty(kv.shape, dtype=torch.float16, pin_memory=True)
         kv_h.copy_(kv)
         kc_h = torch.empty(kc.shape, dtype=torch.float16, pin_memory=True)
@@ -329,7 +334,7 @@ def run_local(args, torch):
                   "algorithmic_bytes_per_launch": kernel_bytes // len(plan_chunks(args, L)),
                   "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
                   "step_roofline_ms": round(roof_ms, 4), "step_frac": round(roof_ms / ms, 4)},
-        extra={"n_chunks": args.chunks, "mode": "local", "k3": args.k3,
+        extra={"n_chunks": args.chunks, "mode": "local", "k3": args.k3, "format": args.format,
                "verified_sampled_rows_bit_exact": verified},
     )
 
@@ -377,6 +382,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS) + sorted(TRACE_MODELS))
     ap.add_argument("--bits", type=int, default=4)
+    ap.add_argument("--format", default="default", choices=["default", "kivi"],
+                    help="payload format: per-token groups, or KIVI per-channel K + residual")
     ap.add_argument("--group", type=int, default=128)
     ap.add_argument("--chunks", type=int, default=None,
                     help="layer chunks per hand-off (default: 1 at N=1, 8 per pair at N>1)")

@@ -165,3 +165,51 @@ def decompress_kivi_into_paged(packed: PackedKiviKV, k_cache: torch.Tensor, v_ca
     if stream is not None:  # temporaries were allocated on the current stream
         gs.record_stream(stream)
         rdst.record_stream(stream)
+
+
+class KiviHandoff:
+    """Reusable single-GPU kivi-format hand-off (K1-kivi then K3-kivi), all
+    buffers and index arrays allocated once (bench.py --format kivi)."""
+
+    def __init__(self, kv: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
+                 slot_mapping: torch.Tensor, prec=KvPrecision(4), group_size: int = 32,
+                 seqlens=None):
+        self.src = KVPlanes.dense(kv)
+        self.dst = KVPlanes.paged(k_cache, v_cache, slot_mapping)
+        T = kv.shape[2]
+        seqlens = tuple(int(n) for n in (seqlens if seqlens is not None else (T,)))
+        self.layout = lay = KiviLayout(self.src.n_layers, self.src.n_heads, self.src.head_dim,
+                                       KvPrecision(getattr(prec, "bits", prec)).bits, group_size,
+                                       seqlens)
+        gs, rt = kivi_groups(seqlens, group_size)
+        self.gs = torch.from_numpy(gs).to(kv.device)
+        self.rt = torch.from_numpy(rt).to(kv.device)
+        self.rdst = self.dst.slots[self.rt].contiguous()
+        self.buf = torch.empty(lay.nbytes + 256, dtype=torch.uint8, device=kv.device)
+        self.base = _round_up(self.buf.data_ptr())
+        self.offs = _offsets_arg(lay)
+        self.packed = PackedKiviKV(lay, self.buf, self.base, self.gs, self.rt)
+
+    def run(self, timing: list | None = None) -> None:
+        lay, s = self.layout, torch.cuda.current_stream()
+        ev = None
+        if timing is not None:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record(s)
+        k, v = self.src.ptrs(0)
+        _lib.call("kvx_quant_pack_kivi", k, v, self.src.layer_stride, lay.n_layers, lay.n_tokens,
+                  lay.n_heads, lay.head_dim, lay.group, lay.bits,
+                  self.gs.data_ptr() if self.gs.numel() else None, self.gs.numel(),
+                  self.rt.data_ptr() if self.rt.numel() else None, self.rt.numel(), self.base,
+                  lay.layer_stride, self.offs, _stream_ptr(s))
+        if ev is not None:
+            ev[1].record(s)
+        kc, vc = self.dst.ptrs(0)
+        _lib.call("kvx_dequant_scatter_paged_kivi", self.base, lay.layer_stride, self.offs,
+                  self.dst.slots_ptr, self.gs.data_ptr() if self.gs.numel() else None,
+                  self.gs.numel(), self.rdst.data_ptr() if self.rdst.numel() else None,
+                  self.rdst.numel(), lay.n_layers, lay.n_tokens, lay.n_heads, lay.head_dim,
+                  lay.group, lay.bits, kc, vc, self.dst.layer_stride, _stream_ptr(s))
+        if ev is not None:
+            ev[2].record(s)
+            timing.append({"k1": (ev[0], ev[1]), "k3": (ev[1], ev[2])})
