@@ -349,45 +349,48 @@ template <int BITS, int G>
 #ifndef KVX_K1_MIN_BLOCKS
 #define KVX_K1_MIN_BLOCKS 1
 #endif
+#ifndef KVX_K1_PF
+#define KVX_K1_PF 2  // items prefetched ahead per warp (A/B: profiles/r01_summary.md)
+#endif
 __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo g, ItemGeo ig,
                                                          uint8_t* __restrict__ codes,
                                                          __half* __restrict__ scale,
                                                          __half* __restrict__ zero) {
+  // Ring of PF+1 register buffers: the loads of the next PF items are in
+  // flight while the current one is quantised (all indices compile-time).
+  constexpr int NB = KVX_K1_PF + 1;
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
-  uint32_t wa[16], wb[16];
-  uint32_t item = warp;
-  K1Item a, b;
-  if (item < ig.n_items) {
-    a = k1_item<BITS, G>(g, ig, item, lane, codes, scale, zero);
-    if (a.active) {
-      ld256(a.src, *reinterpret_cast<uint32_t(*)[8]>(&wa[0]));
-      ld256(a.src + 32, *reinterpret_cast<uint32_t(*)[8]>(&wa[8]));
+  uint32_t w[NB][16];
+  K1Item it[NB];
+#pragma unroll
+  for (int i = 0; i < NB - 1; ++i) {
+    const uint32_t itm = warp + i * n_warps;
+    if (itm < ig.n_items) {
+      it[i] = k1_item<BITS, G>(g, ig, itm, lane, codes, scale, zero);
+      if (it[i].active) {
+        ld256(it[i].src, *reinterpret_cast<uint32_t(*)[8]>(&w[i][0]));
+        ld256(it[i].src + 32, *reinterpret_cast<uint32_t(*)[8]>(&w[i][8]));
+      }
     }
   }
-  while (item < ig.n_items) {
-    const uint32_t nxt = item + n_warps;
-    if (nxt < ig.n_items) {
-      b = k1_item<BITS, G>(g, ig, nxt, lane, codes, scale, zero);
-      if (b.active) {
-        ld256(b.src, *reinterpret_cast<uint32_t(*)[8]>(&wb[0]));
-        ld256(b.src + 32, *reinterpret_cast<uint32_t(*)[8]>(&wb[8]));
+  for (uint32_t base = warp; base < ig.n_items; base += NB * n_warps) {
+#pragma unroll
+    for (int st = 0; st < NB; ++st) {
+      const uint32_t cur = base + st * n_warps;
+      if (cur >= ig.n_items) return;  // warp-uniform
+      const uint32_t pre = cur + (NB - 1) * n_warps;
+      const int pb = (st + NB - 1) % NB;
+      if (pre < ig.n_items) {
+        it[pb] = k1_item<BITS, G>(g, ig, pre, lane, codes, scale, zero);
+        if (it[pb].active) {
+          ld256(it[pb].src, *reinterpret_cast<uint32_t(*)[8]>(&w[pb][0]));
+          ld256(it[pb].src + 32, *reinterpret_cast<uint32_t(*)[8]>(&w[pb][8]));
+        }
       }
+      k1_process<BITS, G>(it[st], w[st], lane);
     }
-    k1_process<BITS, G>(a, wa, lane);
-    item = nxt;
-    if (item >= ig.n_items) break;
-    const uint32_t nn = item + n_warps;
-    if (nn < ig.n_items) {
-      a = k1_item<BITS, G>(g, ig, nn, lane, codes, scale, zero);
-      if (a.active) {
-        ld256(a.src, *reinterpret_cast<uint32_t(*)[8]>(&wa[0]));
-        ld256(a.src + 32, *reinterpret_cast<uint32_t(*)[8]>(&wa[8]));
-      }
-    }
-    k1_process<BITS, G>(b, wb, lane);
-    item = nn;
   }
 }
 
@@ -517,37 +520,41 @@ __device__ __forceinline__ void k3_process(const K3Item& it, const K3Data<BITS>&
   st256(it.dst + 32, o[2], o[3]);
 }
 
+#ifndef KVX_K3_PF
+#define KVX_K3_PF 2  // items prefetched ahead per warp (A/B: profiles/r01_summary.md)
+#endif
 template <int BITS, int G>
 __global__ void __launch_bounds__(256) dequant_scatter_kernel(Geo g, ItemGeo ig,
                                                               const uint8_t* __restrict__ codes,
                                                               const __half* __restrict__ scale,
                                                               const __half* __restrict__ zero) {
+  constexpr int NB = KVX_K3_PF + 1;
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
-  uint32_t item = warp;
-  K3Item a, b;
-  K3Data<BITS> da, db;
-  if (item < ig.n_items) {
-    a = k3_item<BITS, G>(g, ig, item, lane, codes, scale, zero);
-    k3_load<BITS>(a, da);
+  K3Item it[NB];
+  K3Data<BITS> d[NB];
+#pragma unroll
+  for (int i = 0; i < NB - 1; ++i) {
+    const uint32_t itm = warp + i * n_warps;
+    if (itm < ig.n_items) {
+      it[i] = k3_item<BITS, G>(g, ig, itm, lane, codes, scale, zero);
+      k3_load<BITS>(it[i], d[i]);
+    }
   }
-  while (item < ig.n_items) {
-    const uint32_t nxt = item + n_warps;
-    if (nxt < ig.n_items) {
-      b = k3_item<BITS, G>(g, ig, nxt, lane, codes, scale, zero);
-      k3_load<BITS>(b, db);
+  for (uint32_t base = warp; base < ig.n_items; base += NB * n_warps) {
+#pragma unroll
+    for (int st = 0; st < NB; ++st) {
+      const uint32_t cur = base + st * n_warps;
+      if (cur >= ig.n_items) return;  // warp-uniform
+      const uint32_t pre = cur + (NB - 1) * n_warps;
+      const int pb = (st + NB - 1) % NB;
+      if (pre < ig.n_items) {
+        it[pb] = k3_item<BITS, G>(g, ig, pre, lane, codes, scale, zero);
+        k3_load<BITS>(it[pb], d[pb]);
+      }
+      k3_process<BITS>(it[st], d[st]);
     }
-    k3_process<BITS>(a, da);
-    item = nxt;
-    if (item >= ig.n_items) break;
-    const uint32_t nn = item + n_warps;
-    if (nn < ig.n_items) {
-      a = k3_item<BITS, G>(g, ig, nn, lane, codes, scale, zero);
-      k3_load<BITS>(a, da);
-    }
-    k3_process<BITS>(b, db);
-    item = nn;
   }
 }
 
