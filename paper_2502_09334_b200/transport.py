@@ -470,6 +470,13 @@ def _verify_last(ch, trace, tok, it, L, H, D, spec, ctrl, kv=None, dec=None):
         c, s_, z = C.quant_pack(np.ascontiguousarray(src).reshape(-1, D), spec.bits, spec.group)
         want = C.unpack_dequant(c, s_, z, spec.bits, spec.group, D).reshape(src.shape)
         ok = bool(np.array_equal(want.view(np.uint16), mine.view(np.uint16)))
+        if not ok and os.environ.get("KVX_VERIFY_DEBUG"):
+            bad = want.view(np.uint16) != mine.view(np.uint16)
+            print(f"[verify] rank {ch.rank}: {int(bad.sum())}/{bad.size} mismatches; per layer "
+                  f"{bad.reshape(len(layers), -1).sum(1).tolist()}; per kv {bad.sum((0, 2, 3, 4)).tolist()}"
+                  f"; per token {bad.sum((0, 1, 3, 4)).tolist()}; max|d| "
+                  f"{float(np.abs(want.astype(np.float32) - mine.astype(np.float32)).max())}",
+                  flush=True)
     return all(exchange(ok, ctrl))
 
 
@@ -518,7 +525,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
         vc = torch.zeros_like(kc)
         if trace is None:
             planes = KVPlanes.paged(kc, vc, slots)
-            step = lambda timing=None: ch.recv(planes, T, timing)  # noqa: E731
+            step = lambda timing=None: ch.recv(planes, next_t(), timing)  # noqa: E731
         else:
             # each batch gets its own random block placement (requests start on
             # a block boundary, as a paged allocator hands them out)
