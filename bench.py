@@ -43,6 +43,7 @@ WORKLOADS = {
     "cfg2_7b_2048x8": (32, 32, 128, 8, 2048),
     "cfg3_13b_2048x8": (40, 40, 128, 8, 2048),
     "cfg4_70b_gqa_pair": (80, 8, 128, 2, 4096),  # one 4P4D pair: 8x4096 tokens / 4 pairs
+    "small_70b_gqa_128x1": (80, 8, 128, 1, 128),  # shortest trace request: latency-bound
 }
 BLOCK = 16
 
@@ -398,6 +399,8 @@ def main():
                     help="reference arm: layers per step (default: ~1 GB of fp16 KV)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true",
+                    help="N>1: launch every hand-off eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-verify", action="store_true",
                     help="skip the full-size sampled bit-exact check (outside the timed region)")
     args = ap.parse_args()

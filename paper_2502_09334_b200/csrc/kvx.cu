@@ -187,12 +187,22 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   if (n_spans >= (int64_t(1) << 31)) return cudaSuccess;
   bg.n_spans = uint32_t(n_spans);
   auto k = kvx::pull_dequant_scatter_kernel<BITS, G, kBulkStages>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  // once per device and instantiation (not a stream op; keeps capture clean)
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  static bool attr_set[kMaxDev] = {false};
+  if (cur_dev < 0 || cur_dev >= kMaxDev) return cudaErrorInvalidDevice;
+  if (!attr_set[cur_dev]) {
+    cudaError_t attr =
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (attr != cudaSuccess) return attr;
+    attr_set[cur_dev] = true;
+  }
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBulkThreads, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
+  cudaGetLastError();
   int dev = 0;
   cudaGetDevice(&dev);
   int64_t grid = int64_t(sm_count(dev)) * per_sm;

@@ -47,7 +47,8 @@ from .datapath import (KVPlanes, PackedKV, PackedLayout, _round_up, _stream_ptr,
 
 MODES = ("pull", "pull_ldg", "push", "copy", "nccl")
 PULL_MODES = ("pull", "pull_ldg")
-FLAG_SLOTS = 256  # doorbells per direction (>= chunks)
+FLAG_SLOTS = 256  # 32-bit doorbells per rank
+PULL_MAX_CHUNKS = 64
 
 
 # ---------------------------------------------------------------------------
@@ -176,7 +177,7 @@ class PairChannel:
     """
 
     def __init__(self, spec: ChannelSpec, rank: int, world: int, control_group=None,
-                 data_group=None):
+                 data_group=None, graphs: bool = True):
         self.spec = spec
         self.rank, self.world = rank, world
         self.role, self.pair, self.peer = role_of(rank, world)
@@ -198,6 +199,16 @@ class PairChannel:
             raise RuntimeError("stream memory operations unavailable: use mode='nccl'")
         # local buffers: doorbells (written by the partner) + payload staging
         self.flags = IpcBuffer(FLAG_SLOTS * 4)
+        self.graphs = bool(graphs) and mode in PULL_MODES
+        self._graphs, self._seen = {}, set()
+        if mode in PULL_MODES:
+            if len(self.chunks) > PULL_MAX_CHUNKS:
+                raise ValueError(f"pull modes support at most {PULL_MAX_CHUNKS} chunks")
+            if self.role == "prefill":  # both queue halves start free
+                one = torch.ones(2, dtype=torch.int32, device=self.device)
+                _lib.call("kvx_copy_peer", self._pfree(self.flags.ptr, 0), self.device.index,
+                          one.data_ptr(), self.device.index, 8, None)
+                torch.cuda.synchronize(self.device)
         stage_here = (self.role == "prefill" and mode in ("pull", "pull_ldg", "copy", "nccl")) or (
             self.role == "decode" and mode in ("push", "copy", "nccl"))
         self.local_payload = None
@@ -234,6 +245,118 @@ class PairChannel:
         """Byte offset of the payload half used by hand-off ``e`` (pull modes)."""
         return (e & 1) * _round_up(self.spec.capacity_bytes)
 
+    # pull-mode doorbells use constant values (0/1) so a hand-off is
+    # graph-capturable: ready[h][c] lives on D (set to 1 by P after K1 of
+    # chunk c into half h, reset to 0 by D after consuming the half);
+    # free[h] lives on P (1 = D is done with half h; P clears it before reuse).
+    def _pready(self, base: int, h: int, c: int) -> int:
+        return base + 4 * (h * PULL_MAX_CHUNKS + c)
+
+    def _pfree(self, base: int, h: int) -> int:
+        return base + 4 * (2 * PULL_MAX_CHUNKS + h)
+
+    def _send_pull(self, src, lay, e, s, cur, timing, stage_in):
+        h = e & 1
+        key = ("send", lay.n_tokens, h, src.k.data_ptr(), src.slots_ptr)
+        if self._graph_ok(key, timing, stage_in):
+            return self._replay(key, s, cur)
+        payload = PackedKV(lay, self.k1_target + self._half(e), self.device)
+
+        def body():
+            wait(self._pfree(self.flags.ptr, h), 1, s)        # D is done with this half
+            signal(self._pfree(self.flags.ptr, h), 0, s)      # claim it
+            for c, (l0, l1) in enumerate(self.chunks):
+                if stage_in is not None:
+                    host, devt = stage_in
+                    self.xfer.wait_event(self.x_done[c])
+                    with torch.cuda.stream(self.xfer):
+                        devt[l0:l1].copy_(host[l0:l1], non_blocking=True)
+                    self.x_ready[c].record(self.xfer)
+                    s.wait_event(self.x_ready[c])
+                ev = _kernel_events(timing, s, "k1")
+                quant_pack_layers(src, payload, l0, l1, s)
+                _kernel_events_end(ev, s)
+                if stage_in is not None:
+                    self.x_done[c].record(s)
+                signal(self._pready(self.peer_flags, h, c), 1, s)
+
+        self._run_or_capture(key, body, s, cur, capturable=timing is None and stage_in is None)
+        if stage_in is not None:
+            cur.wait_stream(self.xfer)
+
+    def _recv_pull(self, dst, lay, e, s, cur, timing, stage_out):
+        h = e & 1
+        key = ("recv", lay.n_tokens, h, dst.slots_ptr, dst.k.data_ptr())
+        if self._graph_ok(key, timing, stage_out):
+            return self._replay(key, s, cur)
+        payload = PackedKV(lay, self.k3_source + self._half(e), self.device)
+        bulk = self.spec.mode == "pull" and pull_supported(lay)
+
+        def body():
+            if stage_out is not None:
+                for c in range(len(self.chunks)):
+                    s.wait_event(self.x_done[c])
+            if bulk:
+                # ONE persistent bulk-pull kernel per hand-off: its producer
+                # threads wait in-kernel for each chunk's doorbell
+                ev = _kernel_events(timing, s, "k3")
+                dequant_scatter_layers(payload, dst, 0, lay.n_layers, s,
+                                       ready=(self._pready(self.flags.ptr, h, 0), 1, self.lpc))
+                _kernel_events_end(ev, s)
+            else:
+                for c, (l0, l1) in enumerate(self.chunks):
+                    wait(self._pready(self.flags.ptr, h, c), 1, s)
+                    ev = _kernel_events(timing, s, "k3")
+                    dequant_scatter_layers(payload, dst, l0, l1, s)
+                    _kernel_events_end(ev, s)
+            _lib.call("kvx_memset_async", self._pready(self.flags.ptr, h, 0), 0,
+                      4 * len(self.chunks), _stream_ptr(s))
+            signal(self._pfree(self.peer_flags, h), 1, s)     # half consumed
+            if stage_out is not None:
+                (dk, dv), (hk, hv) = stage_out
+                self.x_ready[0].record(s)
+                self.xfer.wait_event(self.x_ready[0])
+                with torch.cuda.stream(self.xfer):
+                    hk.copy_(dk, non_blocking=True)
+                    hv.copy_(dv, non_blocking=True)
+                for c in range(len(self.chunks)):
+                    self.x_done[c].record(self.xfer)
+
+        self._run_or_capture(key, body, s, cur, capturable=timing is None and stage_out is None)
+        if stage_out is not None:
+            cur.wait_stream(self.xfer)
+
+    # ---- CUDA graphs: a hand-off of a given size is one graph launch ----------
+    def _graph_ok(self, key, timing, staging) -> bool:
+        return self.graphs and timing is None and staging is None and key in self._graphs
+
+    def _replay(self, key, s, cur):
+        s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            self._graphs[key].replay()
+        cur.wait_stream(s)
+
+    def _run_or_capture(self, key, body, s, cur, capturable: bool):
+        s.wait_stream(cur)
+        if self.graphs and capturable and key in self._seen:
+            g = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
+                    body()
+            except Exception:  # noqa: BLE001 - capture unsupported here: stay eager
+                self.graphs = False
+                body()
+                cur.wait_stream(s)
+                return
+            self._graphs[key] = g
+            with torch.cuda.stream(s):
+                g.replay()
+        else:
+            body()
+            if capturable:
+                self._seen.add(key)  # eager once (attributes, caches), capture next time
+        cur.wait_stream(s)
+
     # flags: slot c = "chunk c of epoch e ready" (written by P into D's flags);
     #        slot FLAG_SLOTS//2 + c = "chunk c of epoch e consumed" (D -> P)
     def _ready(self, base: int, c: int) -> int:
@@ -263,15 +386,12 @@ class PairChannel:
         mode = self.spec.mode
         s, cs = self.stream, self.cstream
         cur = torch.cuda.current_stream(self.device)
-        s.wait_stream(cur)
         if mode in PULL_MODES:
-            payload = PackedKV(lay, self.k1_target + self._half(e), self.device)
-            # the half we fill was last read by hand-off e - 2
-            wait(self._ack(self.flags.ptr, 0), e - 2, s)
-        else:
-            payload = PackedKV(lay, self.k1_target, self.device)
+            return self._send_pull(src, lay, e, s, cur, timing, stage_in)
+        s.wait_stream(cur)
+        payload = PackedKV(lay, self.k1_target, self.device)
         ranges = [(l0 * lay.layer_stride, l1 * lay.layer_stride) for l0, l1 in self.chunks]
-        prev = self._prev_ranges if mode not in PULL_MODES else None
+        prev = self._prev_ranges
         for c, (l0, l1) in enumerate(self.chunks):
             if stage_in is not None:
                 host, devt = stage_in
@@ -294,7 +414,7 @@ class PairChannel:
             if stage_in is not None:
                 self.x_done[c].record(s)
             addr, nbytes = payload.byte_range(l0, l1)
-            if mode in ("pull", "pull_ldg", "push"):
+            if mode == "push":
                 signal(self._ready(self.peer_flags, c), e, s)
                 continue
             self.k_done[c].record(s)
@@ -331,36 +451,11 @@ class PairChannel:
         mode = self.spec.mode
         s, cs = self.stream, self.cstream
         cur = torch.cuda.current_stream(self.device)
+        if mode in PULL_MODES:
+            return self._recv_pull(dst, lay, e, s, cur, timing, stage_out)
         s.wait_stream(cur)
         cs.wait_stream(cur)
-        if mode in PULL_MODES:
-            payload = PackedKV(lay, self.k3_source + self._half(e), self.device)
-            if mode == "pull" and pull_supported(lay):
-                # ONE persistent bulk-pull kernel for the whole hand-off: its
-                # producer threads wait in-kernel for each chunk's doorbell
-                if stage_out is not None:
-                    for c in range(len(self.chunks)):
-                        s.wait_event(self.x_done[c])
-                ev = _kernel_events(timing, s, "k3")
-                dequant_scatter_layers(payload, dst, 0, lay.n_layers, s,
-                                       ready=(self.flags.ptr, e, self.lpc))
-                _kernel_events_end(ev, s)
-                if stage_out is not None:
-                    (dk, dv), (hk, hv) = stage_out
-                    self.x_ready[0].record(s)
-                    self.xfer.wait_event(self.x_ready[0])
-                    with torch.cuda.stream(self.xfer):
-                        hk.copy_(dk, non_blocking=True)
-                        hv.copy_(dv, non_blocking=True)
-                    for c in range(len(self.chunks)):
-                        self.x_done[c].record(self.xfer)
-                signal(self._ack(self.peer_flags, 0), e, s)
-                cur.wait_stream(s)
-                if stage_out is not None:
-                    cur.wait_stream(self.xfer)
-                return
-        else:
-            payload = PackedKV(lay, self.k3_source, self.device)
+        payload = PackedKV(lay, self.k3_source, self.device)
         ranges = [(l0 * lay.layer_stride, l1 * lay.layer_stride) for l0, l1 in self.chunks]
         prev = self._prev_ranges
         for c, (l0, l1) in enumerate(self.chunks):
@@ -381,7 +476,7 @@ class PairChannel:
             if stage_out is not None:
                 s.wait_event(self.x_done[c])  # previous epoch's download of these layers
             ev = _kernel_events(timing, s, "k3")
-            dequant_scatter_layers(payload, dst, l0, l1, s, bulk=(mode == "pull"))
+            dequant_scatter_layers(payload, dst, l0, l1, s)
             _kernel_events_end(ev, s)
             if stage_out is not None:
                 (dk, dv), (hk, hv) = stage_out
@@ -393,10 +488,8 @@ class PairChannel:
                 self.x_done[c].record(self.xfer)
             if mode == "nccl":
                 self.k_done[c].record(s)
-            elif mode not in PULL_MODES:
+            else:
                 signal(self._ack(self.peer_flags, c), e, s)
-        if mode in PULL_MODES:
-            signal(self._ack(self.peer_flags, 0), e, s)  # whole half consumed
         self._prev_ranges = ranges
         cur.wait_stream(s)
         cur.wait_stream(cs)
@@ -504,7 +597,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     mode = args.mode
     n_chunks = args.chunks or 8
     spec = ChannelSpec(L, T, H, D, args.bits, args.group, n_chunks, mode)
-    ch = PairChannel(spec, rank, world, control_group=ctrl)
+    ch = PairChannel(spec, rank, world, control_group=ctrl, graphs=not args.no_graphs)
     lay = spec.layout(T)
     # per step token counts (fixed workload, or the trace's batches)
     tok = [T] * (args.warmup + args.steps + 2) if trace is None else [sum(x) for x in trace]
@@ -551,20 +644,28 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
-    timing = []
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with B.ClockSampler(local) as clk:
         t0.record()
         for _ in range(args.steps):
-            step(timing)
+            step()  # CUDA-graph replay per hand-off once warmed up (pull modes)
         t1.record()
         torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
+    # per-kernel durations: a separate eager pass with CUDA events on the
+    # launching streams (events cannot sit inside the captured graph)
+    timing = []
+    n_kt = max(1, min(args.steps, 5))
+    for _ in range(n_kt):
+        step(timing)
+    torch.cuda.synchronize()
+    dist.barrier()
     kern = {}
     for name, a, b_ in timing:
-        kern[name] = kern.get(name, 0.0) + a.elapsed_time(b_) / args.steps
+        kern[name] = kern.get(name, 0.0) + a.elapsed_time(b_) / n_kt
+    launches = len(timing) / n_kt * args.steps
     # full-size parity (outside the timed region): sampled token rows of the
     # last hand-off, decode cache vs the CPU oracle applied to the source rows
     verified = None
@@ -606,7 +707,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
         e2e_ms = e0.elapsed_time(e1) / n_e2e
         dist.barrier()
     stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0), e2e_ms, h2d, d2h,
-                          len(timing)], dtype=torch.float64, device=dev)
+                          launches], dtype=torch.float64, device=dev)
     gathered = [torch.zeros_like(stats) for _ in range(world)]
     dist.all_gather(gathered, stats)
     clocks = exchange(clk.summary(), ctrl)
@@ -653,6 +754,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
                       "frac_of_nominal_900": round(link_gbs / 900.0, 4),
                       "hbm_peak": hbm},
             extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
+                   "cuda_graphs": bool(ch.graphs),
                    "verified_sampled_rows_bit_exact": verified,
                    **({"trace_batches_timed": tok[args.warmup:args.warmup + args.steps],
                        "trace": "lengths log-uniform [128, 8192], 1-16 req/batch, <=16384 "

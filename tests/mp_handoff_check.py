@@ -26,24 +26,31 @@ def main():
     ctrl = dist.new_group(backend="gloo")
     L, Tmax, H, D, bs = 6, 200, 8, 128, 16
     failures = 0
+    # several hand-offs of varying length; repeated lengths exercise the CUDA
+    # graph capture (2nd time) and replay (3rd time) of the pull modes, on
+    # both halves of the double-buffered queue
+    seq = (Tmax, 77, Tmax, 77, Tmax, 77, 130, Tmax)
     for mode in modes:
         for bits in (4, 8, 16):
             spec = ChannelSpec(L, Tmax, H, D, bits, 64 if bits != 16 else 128, 3, mode)
             ch = PairChannel(spec, rank, world, control_group=ctrl)
             nb = Tmax // bs + 4
+            kv_cap = torch.zeros((L, 2, Tmax, H, D), dtype=torch.float16, device=dev)
+            slots_buf = torch.zeros(Tmax, dtype=torch.int64, device=dev)
             if ch.role == "decode":
                 kc = torch.zeros((L, nb, bs, H, D), dtype=torch.float16, device=dev)
                 vc = torch.zeros_like(kc)
-            for epoch, T in enumerate((Tmax, 77, 130)):  # several hand-offs, varying length
+            for epoch, T in enumerate(seq):
                 seed = 1000 * ch.pair + 10 * epoch + bits
                 if ch.role == "prefill":
-                    kv = torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=seed)).to(dev)
-                    ch.send(KVPlanes.dense(kv), T)
+                    kv_cap[:, :, :T].copy_(torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=seed)))
+                    ch.send(KVPlanes.dense(kv_cap), T)
                     torch.cuda.synchronize()
                 else:
                     slots_np = O.synthetic_slots(T, bs, nb, seed=seed)
+                    slots_buf[:T].copy_(torch.from_numpy(slots_np))
                     kc.zero_(); vc.zero_()
-                    ch.recv(KVPlanes.paged(kc, vc, torch.from_numpy(slots_np).to(dev)), T)
+                    ch.recv(KVPlanes.paged(kc, vc, slots_buf[:T]), T)
                     torch.cuda.synchronize()
                     okc = np.zeros((L, nb, bs, H, D), np.float16); ovc = okc.copy()
                     kv_np = O.synthetic_kv(L, T, H, D, seed=seed)
@@ -55,7 +62,11 @@ def main():
                           and np.array_equal(vc.cpu().numpy().view(np.uint16), ovc.view(np.uint16)))
                     if not ok:
                         failures += 1
-                        print(f"MISMATCH rank={rank} mode={mode} bits={bits} T={T}", flush=True)
+                        print(f"MISMATCH rank={rank} mode={mode} bits={bits} T={T} epoch={epoch}",
+                              flush=True)
+            if mode.startswith("pull") and rank == 0:
+                print(f"{mode} bits={bits}: graphs={ch.graphs} captured={len(ch._graphs)}",
+                      flush=True)
             dist.barrier()
             ch.close()
     # host-buffer path (e2e): pinned host KV -> P, D -> pinned host cache

@@ -21,3 +21,4 @@ def test_modes_over_ipc(cuda, nproc):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "failures=0" in r.stdout
+    assert "pull bits=4: graphs=True" in r.stdout  # hand-offs replayed as CUDA graphs
