@@ -49,6 +49,7 @@ MODES = ("pull", "pull_ldg", "push", "copy", "nccl")
 PULL_MODES = ("pull", "pull_ldg")
 FLAG_SLOTS = 256  # 32-bit doorbells per rank
 PULL_MAX_CHUNKS = 64
+PULL_CHUNK_TARGET = 128 << 20  # min fp16 bytes per pull chunk
 
 
 # ---------------------------------------------------------------------------
@@ -85,6 +86,7 @@ class ChannelSpec:
     group: int = DEFAULT_GROUP
     n_chunks: int = 8
     mode: str = "pull"
+    min_chunk_bytes: int = PULL_CHUNK_TARGET  # pull modes: smaller hand-offs use fewer chunks
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -255,8 +257,19 @@ class PairChannel:
     def _pfree(self, base: int, h: int) -> int:
         return base + 4 * (2 * PULL_MAX_CHUNKS + h)
 
+    def _pull_chunks(self, lay):
+        """Chunking of one pull hand-off: at most spec.n_chunks, and no chunk
+        smaller than PULL_CHUNK_TARGET fp16 bytes -- a short prompt goes as ONE
+        chunk (per-chunk launch and doorbell overhead dominates it otherwise).
+        Both ends derive the same chunks from the token count."""
+        want = max(1, -(-lay.fp16_bytes // max(1, self.spec.min_chunk_bytes)))
+        n = min(self.spec.n_chunks, want)
+        lpc = layers_per_chunk(lay.n_layers, n)
+        return layer_chunks(lay.n_layers, n), lpc
+
     def _send_pull(self, src, lay, e, s, cur, timing, stage_in):
         h = e & 1
+        chunks, _ = self._pull_chunks(lay)
         key = ("send", lay.n_tokens, h, src.k.data_ptr(), src.slots_ptr)
         if self._graph_ok(key, timing, stage_in):
             return self._replay(key, s, cur)
@@ -265,7 +278,7 @@ class PairChannel:
         def body():
             wait(self._pfree(self.flags.ptr, h), 1, s)        # D is done with this half
             signal(self._pfree(self.flags.ptr, h), 0, s)      # claim it
-            for c, (l0, l1) in enumerate(self.chunks):
+            for c, (l0, l1) in enumerate(chunks):
                 if stage_in is not None:
                     host, devt = stage_in
                     self.xfer.wait_event(self.x_done[c])
@@ -286,6 +299,7 @@ class PairChannel:
 
     def _recv_pull(self, dst, lay, e, s, cur, timing, stage_out):
         h = e & 1
+        chunks, lpc = self._pull_chunks(lay)
         key = ("recv", lay.n_tokens, h, dst.slots_ptr, dst.k.data_ptr())
         if self._graph_ok(key, timing, stage_out):
             return self._replay(key, s, cur)
@@ -294,23 +308,23 @@ class PairChannel:
 
         def body():
             if stage_out is not None:
-                for c in range(len(self.chunks)):
+                for c in range(len(chunks)):
                     s.wait_event(self.x_done[c])
             if bulk:
                 # ONE persistent bulk-pull kernel per hand-off: its producer
                 # threads wait in-kernel for each chunk's doorbell
                 ev = _kernel_events(timing, s, "k3")
                 dequant_scatter_layers(payload, dst, 0, lay.n_layers, s,
-                                       ready=(self._pready(self.flags.ptr, h, 0), 1, self.lpc))
+                                       ready=(self._pready(self.flags.ptr, h, 0), 1, lpc))
                 _kernel_events_end(ev, s)
             else:
-                for c, (l0, l1) in enumerate(self.chunks):
+                for c, (l0, l1) in enumerate(chunks):
                     wait(self._pready(self.flags.ptr, h, c), 1, s)
                     ev = _kernel_events(timing, s, "k3")
                     dequant_scatter_layers(payload, dst, l0, l1, s)
                     _kernel_events_end(ev, s)
             _lib.call("kvx_memset_async", self._pready(self.flags.ptr, h, 0), 0,
-                      4 * len(self.chunks), _stream_ptr(s))
+                      4 * len(chunks), _stream_ptr(s))
             signal(self._pfree(self.peer_flags, h), 1, s)     # half consumed
             if stage_out is not None:
                 (dk, dv), (hk, hv) = stage_out
@@ -319,7 +333,7 @@ class PairChannel:
                 with torch.cuda.stream(self.xfer):
                     hk.copy_(dk, non_blocking=True)
                     hv.copy_(dv, non_blocking=True)
-                for c in range(len(self.chunks)):
+                for c in range(len(chunks)):
                     self.x_done[c].record(self.xfer)
 
         self._run_or_capture(key, body, s, cur, capturable=timing is None and stage_out is None)
