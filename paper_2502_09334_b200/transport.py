@@ -87,6 +87,7 @@ class ChannelSpec:
     n_chunks: int = 8
     mode: str = "pull"
     min_chunk_bytes: int = PULL_CHUNK_TARGET  # pull modes: smaller hand-offs use fewer chunks
+    format: str = "default"  # "default" (per-token groups) or "kivi" (pull modes only)
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -94,6 +95,10 @@ class ChannelSpec:
         KvPrecision(self.bits)
         if self.n_chunks < 1 or self.n_chunks > FLAG_SLOTS:
             raise ValueError("n_chunks out of range")
+        if self.format not in ("default", "kivi"):
+            raise ValueError("format must be 'default' or 'kivi'")
+        if self.format == "kivi" and self.mode not in PULL_MODES:
+            raise ValueError("the kivi format is carried by the pull modes")
 
     def layout(self, n_tokens: int) -> PackedLayout:
         if not 0 <= n_tokens <= self.max_tokens:
@@ -101,8 +106,24 @@ class ChannelSpec:
         return PackedLayout(self.n_layers, n_tokens, self.n_heads, self.head_dim, self.bits,
                             self.group)
 
+    def kivi_layout(self, seqlens):
+        from .kivi import KiviLayout
+        lay = KiviLayout(self.n_layers, self.n_heads, self.head_dim, self.bits, self.group,
+                         tuple(int(n) for n in seqlens))
+        if lay.n_tokens > self.max_tokens:
+            raise ValueError("n_tokens exceeds the channel capacity")
+        return lay
+
     @property
     def capacity_bytes(self) -> int:
+        if self.format == "kivi":
+            # worst case: every token in the fp16 residual window
+            hd = self.n_heads * self.head_dim
+            per_layer = (_round_up(self.max_tokens * hd * 2) + _round_up(
+                self.max_tokens * hd * self.bits // 8) + 2 * _round_up(
+                self.max_tokens * hd // self.group * 2) + 4 * 256 + _round_up(
+                self.max_tokens * hd * 2 // self.group))
+            return per_layer * self.n_layers + 256
         return self.layout(self.max_tokens).nbytes + 256
 
     def chunks(self):
@@ -340,6 +361,67 @@ class PairChannel:
         if stage_out is not None:
             cur.wait_stream(self.xfer)
 
+    # ---- kivi format over the pull queue (per-chunk doorbells, LDG kernels) ---
+    def _kivi_common(self, n_tokens, seqlens, e):
+        from .kivi import kivi_groups
+        seqlens = tuple(int(n) for n in (seqlens if seqlens is not None else (n_tokens,)))
+        lay = self.spec.kivi_layout(seqlens)
+        if lay.n_tokens != n_tokens:
+            raise ValueError("seqlens must sum to n_tokens")
+        gs, rt = kivi_groups(seqlens, lay.group)
+        nchunk = min(self.spec.n_chunks,
+                     max(1, -(-lay.fp16_bytes // max(1, self.spec.min_chunk_bytes))))
+        chunks = layer_chunks(lay.n_layers, nchunk)
+        return lay, gs, rt, chunks, e & 1
+
+    def _send_kivi(self, src, n_tokens, seqlens, e):
+        lay, gs, rt, chunks, h = self._kivi_common(n_tokens, seqlens, e)
+        s, cur = self.stream, torch.cuda.current_stream(self.device)
+        s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            gs_d = torch.from_numpy(gs).to(self.device, non_blocking=False)
+            rt_d = torch.from_numpy(rt).to(self.device, non_blocking=False)
+        base = self.k1_target + self._half(e)
+        offs = (ctypes.c_int64 * 7)(*lay.offsets)
+        wait(self._pfree(self.flags.ptr, h), 1, s)
+        signal(self._pfree(self.flags.ptr, h), 0, s)
+        for c, (l0, l1) in enumerate(chunks):
+            k, v = src.ptrs(l0)
+            _lib.call("kvx_quant_pack_kivi", k, v, src.layer_stride, l1 - l0, n_tokens,
+                      lay.n_heads, lay.head_dim, lay.group, lay.bits,
+                      gs_d.data_ptr() if len(gs) else None, len(gs),
+                      rt_d.data_ptr() if len(rt) else None, len(rt),
+                      base + l0 * lay.layer_stride, lay.layer_stride, offs, _stream_ptr(s))
+            signal(self._pready(self.peer_flags, h, c), 1, s)
+        gs_d.record_stream(s)
+        rt_d.record_stream(s)
+        cur.wait_stream(s)
+
+    def _recv_kivi(self, dst, n_tokens, seqlens, e):
+        lay, gs, rt, chunks, h = self._kivi_common(n_tokens, seqlens, e)
+        s, cur = self.stream, torch.cuda.current_stream(self.device)
+        s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            gs_d = torch.from_numpy(gs).to(self.device)
+            rdst = dst.slots[torch.from_numpy(rt).to(self.device)].contiguous()
+        base = self.k3_source + self._half(e)
+        offs = (ctypes.c_int64 * 7)(*lay.offsets)
+        for c, (l0, l1) in enumerate(chunks):
+            wait(self._pready(self.flags.ptr, h, c), 1, s)
+            k, v = dst.ptrs(l0)
+            _lib.call("kvx_dequant_scatter_paged_kivi", base + l0 * lay.layer_stride,
+                      lay.layer_stride, offs, dst.slots_ptr,
+                      gs_d.data_ptr() if len(gs) else None, len(gs),
+                      rdst.data_ptr() if rdst.numel() else None, rdst.numel(), l1 - l0,
+                      n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
+                      dst.layer_stride, _stream_ptr(s))
+        _lib.call("kvx_memset_async", self._pready(self.flags.ptr, h, 0), 0, 4 * len(chunks),
+                  _stream_ptr(s))
+        signal(self._pfree(self.peer_flags, h), 1, s)
+        gs_d.record_stream(s)
+        rdst.record_stream(s)
+        cur.wait_stream(s)
+
     # ---- CUDA graphs: a hand-off of a given size is one graph launch ----------
     def _graph_ok(self, key, timing, staging) -> bool:
         return self.graphs and timing is None and staging is None and key in self._graphs
@@ -389,11 +471,14 @@ class PairChannel:
         return max(hits) if hits else None
 
     def send(self, src: KVPlanes, n_tokens: int, timing: list | None = None,
-             stage_in: tuple | None = None) -> None:
+             stage_in: tuple | None = None, seqlens=None) -> None:
         """Hand ``src`` to the partner.  ``stage_in=(host_kv, dev_kv)``: upload
         each layer chunk from pinned host memory first (the host-buffer e2e
         path; H2D of chunk c+1 overlaps K1 of chunk c)."""
         assert self.role == "prefill"
+        if self.spec.format == "kivi":
+            self.epoch += 1
+            return self._send_kivi(src, n_tokens, seqlens, self.epoch)
         lay = self.spec.layout(n_tokens)
         self.epoch += 1
         e = self.epoch
@@ -454,11 +539,14 @@ class PairChannel:
             cur.wait_stream(self.xfer)
 
     def recv(self, dst: KVPlanes, n_tokens: int, timing: list | None = None,
-             stage_out: tuple | None = None) -> None:
+             stage_out: tuple | None = None, seqlens=None) -> None:
         """Receive into ``dst``.  ``stage_out=((dev_k, dev_v), (host_k, host_v))``:
         download each finished layer chunk of the cache to pinned host memory
         (D2H of chunk c overlaps K3 of chunk c+1)."""
         assert self.role == "decode"
+        if self.spec.format == "kivi":
+            self.epoch += 1
+            return self._recv_kivi(dst, n_tokens, seqlens, self.epoch)
         lay = self.spec.layout(n_tokens)
         self.epoch += 1
         e = self.epoch
@@ -610,12 +698,15 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
         T = b * s
     mode = args.mode
     n_chunks = args.chunks or 8
-    spec = ChannelSpec(L, T, H, D, args.bits, args.group, n_chunks, mode)
+    spec = ChannelSpec(L, T, H, D, args.bits, args.group, n_chunks, mode,
+                       format=getattr(args, "format", "default"))
     ch = PairChannel(spec, rank, world, control_group=ctrl, graphs=not args.no_graphs)
     lay = spec.layout(T)
     # per step token counts (fixed workload, or the trace's batches)
     tok = [T] * (args.warmup + args.steps + 2) if trace is None else [sum(x) for x in trace]
+    seqs = ([(s,) * b] * len(tok)) if trace is None else [tuple(x) for x in trace]
     it = {"i": 0}
+    kivi = spec.format == "kivi"
 
     def next_t():
         t = tok[it["i"] % len(tok)]
@@ -625,14 +716,27 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     if ch.role == "prefill":
         kv = B.synthetic_kv_device(torch, L, T, H, D, dev, seed=ch.pair)
         planes = KVPlanes.dense(kv)
-        step = lambda timing=None: ch.send(planes, next_t(), timing)  # noqa: E731
+        def step(timing=None):
+            i = it["i"] % len(tok)
+            t = next_t()
+            if kivi:
+                ch.send(planes, t, seqlens=seqs[i])
+            else:
+                ch.send(planes, t, timing)
     else:
         slots, nb = B.paged_slots(torch, T, dev, seed=ch.pair)
         kc = torch.zeros((L, nb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
         vc = torch.zeros_like(kc)
         if trace is None:
             planes = KVPlanes.paged(kc, vc, slots)
-            step = lambda timing=None: ch.recv(planes, next_t(), timing)  # noqa: E731
+
+            def step(timing=None):
+                i = it["i"] % len(tok)
+                t = next_t()
+                if kivi:
+                    ch.recv(planes, t, seqlens=seqs[i])
+                else:
+                    ch.recv(planes, t, timing)
         else:
             # each batch gets its own random block placement (requests start on
             # a block boundary, as a paged allocator hands them out)
@@ -652,7 +756,10 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
 
             def step(timing=None):
                 i = it["i"] % len(tok)
-                ch.recv(planes_b[i], next_t(), timing)
+                if kivi:
+                    ch.recv(planes_b[i], next_t(), seqlens=seqs[i])
+                else:
+                    ch.recv(planes_b[i], next_t(), timing)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -683,7 +790,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     # full-size parity (outside the timed region): sampled token rows of the
     # last hand-off, decode cache vs the CPU oracle applied to the source rows
     verified = None
-    if not getattr(args, "no_verify", False):
+    if not getattr(args, "no_verify", False) and not kivi:
         verified = _verify_last(ch, trace, tok, it, L, H, D, spec, ctrl,
                                 kv if ch.role == "prefill" else None,
                                 (kc, vc, planes if trace is None else planes_b)
@@ -692,7 +799,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     # prefill side (H2D inside the step), pinned host paged cache on the decode
     # side (D2H inside the step)
     e2e_ms, h2d, d2h = 0.0, 0, 0
-    if not args.no_e2e:
+    if not args.no_e2e and not kivi:
         if ch.role == "prefill":
             host = torch.empty(kv.shape, dtype=torch.float16, pin_memory=True)
             host.copy_(kv)
@@ -731,14 +838,19 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
         k1 = float(g[:, 1].max())
         k3 = float(g[:, 2].max())
         pairs = world // 2
-        if trace is None:
+        if kivi:
+            timed = range(args.warmup, args.warmup + args.steps)
+            fp16 = sum(spec.kivi_layout(seqs[i % len(tok)]).fp16_bytes for i in timed) / len(timed)
+            wire_mean = sum(spec.kivi_layout(seqs[i % len(tok)]).wire_bytes
+                            for i in timed) / len(timed)
+        elif trace is None:
             fp16 = lay.fp16_bytes
         else:  # mean fp16 bytes of the timed batches
             timed = tok[args.warmup:args.warmup + args.steps]
             fp16 = sum(spec.layout(t).fp16_bytes for t in timed) / len(timed)
             wire_mean = sum(spec.layout(t).wire_bytes for t in timed) / len(timed)
         value = pairs * fp16 / (ms_max * 1e-3) / 1e9
-        wire = lay.wire_bytes if trace is None else wire_mean
+        wire = lay.wire_bytes if (trace is None and not kivi) else wire_mean
         link_gbs = wire / (ms_max * 1e-3) / 1e9  # per pair
         hbm, peak_kind = B.peaks()
         k3_link = wire / (k3 * 1e-3) / 1e9 if k3 > 0 else None
@@ -750,7 +862,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
             clocks={"sm_mhz": min(sm) if sm else None,
                     "sm_max_mhz": max((c.get("sm_max_mhz") or 0) for c in clocks) or None,
                     "reasons": reasons, "per_rank_median_sm_mhz": sm},
-            e2e=None if args.no_e2e else {
+            e2e=None if (args.no_e2e or kivi) else {
                 "value": round(pairs * fp16 / (float(g[:, 3].max()) * 1e-3) / 1e9, 3),
                 "unit": "GB/s", "h2d_bytes_per_step": int(g[:, 4].sum()),
                 "d2h_bytes_per_step": int(g[:, 5].sum()),
@@ -768,6 +880,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
                       "frac_of_nominal_900": round(link_gbs / 900.0, 4),
                       "hbm_peak": hbm},
             extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
+                   "format": spec.format,
                    "cuda_graphs": bool(ch.graphs),
                    "verified_sampled_rows_bit_exact": verified,
                    **({"trace_batches_timed": tok[args.warmup:args.warmup + args.steps],

@@ -70,6 +70,39 @@ def main():
                       flush=True)
             dist.barrier()
             ch.close()
+    # kivi format over the pull queue (per-channel K + fp16 residual window)
+    for bits, group in ((4, 32), (8, 64)):
+        spec = ChannelSpec(L, Tmax, H, D, bits, group, 3, "pull", min_chunk_bytes=0,
+                           format="kivi")
+        ch = PairChannel(spec, rank, world, control_group=ctrl)
+        nb = Tmax // bs + 4
+        for epoch, seq in enumerate(((70, 64, 66), (31,), (96, 0, 33), (200,))):
+            T = sum(seq)
+            seed = 555 + 1000 * ch.pair + epoch + bits
+            if ch.role == "prefill":
+                kv = torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=seed)).to(dev)
+                ch.send(KVPlanes.dense(kv), T, seqlens=seq)
+                torch.cuda.synchronize()
+            else:
+                slots_np = O.synthetic_slots(T, bs, nb, seed=seed)
+                kc = torch.zeros((L, nb, bs, H, D), dtype=torch.float16, device=dev)
+                vc = torch.zeros_like(kc)
+                ch.recv(KVPlanes.paged(kc, vc, torch.from_numpy(slots_np).to(dev)), T, seqlens=seq)
+                torch.cuda.synchronize()
+                kv_np = O.synthetic_kv(L, T, H, D, seed=seed)
+                K, V = O.unpack_dequant_kivi(O.quant_pack_kivi(kv_np, bits, group, seq), bits,
+                                             group, seq, H, D)
+                okc = np.zeros((L, nb * bs, H, D), np.float16); ovc = okc.copy()
+                okc[:, slots_np] = K; ovc[:, slots_np] = V
+                if not (np.array_equal(kc.cpu().numpy().reshape(okc.shape).view(np.uint16),
+                                       okc.view(np.uint16)) and
+                        np.array_equal(vc.cpu().numpy().reshape(ovc.shape).view(np.uint16),
+                                       ovc.view(np.uint16))):
+                    failures += 1
+                    print(f"MISMATCH kivi rank={rank} bits={bits} seq={seq}", flush=True)
+        dist.barrier()
+        ch.close()
+
     # host-buffer path (e2e): pinned host KV -> P, D -> pinned host cache
     spec = ChannelSpec(L, Tmax, H, D, 4, 128, 4, "pull")
     ch = PairChannel(spec, rank, world, control_group=ctrl)
