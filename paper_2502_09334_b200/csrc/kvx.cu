@@ -290,8 +290,9 @@ template <int BITS, int G>
 cudaError_t launch_kchan_dequant(const kvx::KchanGeo& kg, const int64_t* slots, void* kc,
                                         int64_t dst_ls_b, cudaStream_t s) {
   auto k = kvx::dequant_kchan_kernel<BITS, G>;
-  const int64_t rows = kg.n_layers * kg.n_groups * G;
-  k<<<grid_for(k, rows), kThreads, 0, s>>>(kg, slots, static_cast<char*>(kc), dst_ls_b);
+  const int64_t cblk = (kg.row_elems / 32 + 31) / 32;
+  const int64_t items = kg.n_layers * kg.n_groups * cblk;  // one warp per item
+  k<<<grid_for(k, items), kThreads, 0, s>>>(kg, slots, static_cast<char*>(kc), dst_ls_b);
   return cudaGetLastError();
 }
 

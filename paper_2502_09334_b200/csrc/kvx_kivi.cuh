@@ -97,77 +97,102 @@ __global__ void __launch_bounds__(128) quant_pack_kchan_kernel(KchanGeo g) {
 }
 
 // Dequantise per-channel-grouped K rows into the paged cache.  Warp per
-// payload row (group k, token j), lane owns 32 channels: 16 B of codes plus
-// 64 B of scales and 64 B of zeros (shared by the group's G rows, L1 hits).
+// (layer, group k, block of 32 chunks): each lane loads the 32 scales and 32
+// zeros of its channels ONCE (they are shared by the group's G rows -- over
+// NVLink re-reading them per row would cost 8x the code bytes) and then walks
+// the G rows: 16 B of codes in, 64 B of fp16 out per row.
+template <int BITS>
+__device__ __forceinline__ void kchan_dequant_store(const uint32_t (&cw)[BITS], const uint32_t (&sw)[16],
+                                                    const uint32_t (&zw)[16], char* dst) {
+  const __half2 k1024 = u32_as_h2(0x64006400u), kmax = u32_as_h2(0x7BFF7BFFu);
+  U4 o[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {  // 8 elements per output vector
+    uint32_t p[4];
+    if constexpr (BITS == 4) {
+      const uint32_t cc = cw[v];
+      const uint32_t a0 = lop3_and_or(cc, 0x000F000Fu, 0x64006400u);
+      const uint32_t a1 = lop3_and_or(cc >> 4, 0x000F000Fu, 0x64006400u);
+      const uint32_t a2 = lop3_and_or(cc >> 8, 0x000F000Fu, 0x64006400u);
+      const uint32_t a3 = lop3_and_or(cc >> 12, 0x000F000Fu, 0x64006400u);
+      p[0] = prmt(a0, a1, 0x5410);
+      p[1] = prmt(a2, a3, 0x5410);
+      p[2] = prmt(a0, a1, 0x7632);
+      p[3] = prmt(a2, a3, 0x7632);
+    } else {
+      p[0] = prmt(cw[2 * v], 0x64646464u, 0x4140);
+      p[1] = prmt(cw[2 * v], 0x64646464u, 0x4342);
+      p[2] = prmt(cw[2 * v + 1], 0x64646464u, 0x4140);
+      p[3] = prmt(cw[2 * v + 1], 0x64646464u, 0x4342);
+    }
+    uint32_t* ov = &o[v].x;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __half2 qh = __hsub2(u32_as_h2(p[i]), k1024);
+      const __half2 y = __hfma2(qh, u32_as_h2(sw[4 * v + i]), u32_as_h2(zw[4 * v + i]));
+      ov[i] = h2_as_u32(__hmin2(y, kmax));
+    }
+  }
+  st256(dst, o[0], o[1]);
+  st256(dst + 32, o[2], o[3]);
+}
+
+template <int BITS>
+__device__ __forceinline__ void kchan_load_codes(const char* p, uint32_t (&cw)[BITS]) {
+  if constexpr (BITS == 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
+  } else {
+    const uint4 v0 = reinterpret_cast<const uint4*>(p)[0];
+    const uint4 v1 = reinterpret_cast<const uint4*>(p)[1];
+    cw[0] = v0.x; cw[1] = v0.y; cw[2] = v0.z; cw[3] = v0.w;
+    cw[4] = v1.x; cw[5] = v1.y; cw[6] = v1.z; cw[7] = v1.w;
+  }
+}
+
 template <int BITS, int G>
 __global__ void __launch_bounds__(256) dequant_kchan_kernel(KchanGeo g, const int64_t* dst_slots,
                                                            char* k_cache, int64_t dst_layer_stride_b) {
+  constexpr int CB = 32 * BITS / 8;  // code bytes per 32-channel chunk
+  constexpr int U = 4;               // rows in flight per lane
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int cpr = g.row_elems / 32;
-  const int64_t rows = g.n_layers * g.n_groups * G;
-  const __half2 k1024 = u32_as_h2(0x64006400u), kmax = u32_as_h2(0x7BFF7BFFu);
-  for (int64_t r = warp; r < rows; r += n_warps) {
-    const int64_t layer = r / (g.n_groups * G);
-    const int64_t q = r - layer * g.n_groups * G;  // row inside the layer
-    const int64_t k = q / G;
-    const int64_t t = __ldg(g.group_starts + k) + (q - k * G);
-    const int64_t pos = __ldg(dst_slots + t);
-    if (pos < 0) continue;
-    const char* lc = g.codes + layer * g.payload_ls + q * g.row_elems * BITS / 8;
-    const char* ls = g.scale + layer * g.payload_ls + k * g.row_elems * 2;
-    const char* lz = g.zero + layer * g.payload_ls + k * g.row_elems * 2;
-    char* dst = k_cache + layer * dst_layer_stride_b + pos * g.row_elems * 2;
-    for (int c = lane; c < cpr; c += 32) {
-      uint32_t cw[BITS];  // 32 codes
-      if constexpr (BITS == 4) {
-        const uint4 v = *reinterpret_cast<const uint4*>(lc + c * 16);
-        cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
-      } else {
-        const uint4 v0 = reinterpret_cast<const uint4*>(lc + c * 32)[0];
-        const uint4 v1 = reinterpret_cast<const uint4*>(lc + c * 32)[1];
-        cw[0] = v0.x; cw[1] = v0.y; cw[2] = v0.z; cw[3] = v0.w;
-        cw[4] = v1.x; cw[5] = v1.y; cw[6] = v1.z; cw[7] = v1.w;
-      }
-      uint32_t sw[16], zw[16];  // half2 (scale, zero) pairs for the 32 channels
+  const int cblk = (cpr + 31) / 32;
+  const int64_t items = g.n_layers * g.n_groups * cblk;
+  for (int64_t it = warp; it < items; it += n_warps) {
+    const int64_t lg = it / cblk;
+    const int c = int(it - lg * cblk) * 32 + lane;
+    const int64_t layer = lg / g.n_groups;
+    const int64_t k = lg - layer * g.n_groups;
+    if (c >= cpr) continue;
+    const char* lc = g.codes + layer * g.payload_ls;
+    const char* ls = g.scale + layer * g.payload_ls + (k * g.row_elems + c * 32) * 2;
+    const char* lz = g.zero + layer * g.payload_ls + (k * g.row_elems + c * 32) * 2;
+    uint32_t sw[16], zw[16];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint4 a = reinterpret_cast<const uint4*>(ls + c * 64)[i];
-        const uint4 b = reinterpret_cast<const uint4*>(lz + c * 64)[i];
-        sw[4 * i] = a.x; sw[4 * i + 1] = a.y; sw[4 * i + 2] = a.z; sw[4 * i + 3] = a.w;
-        zw[4 * i] = b.x; zw[4 * i + 1] = b.y; zw[4 * i + 2] = b.z; zw[4 * i + 3] = b.w;
-      }
-      U4 o[4];
+    for (int i = 0; i < 4; ++i) {
+      const uint4 a = reinterpret_cast<const uint4*>(ls)[i];
+      const uint4 b = reinterpret_cast<const uint4*>(lz)[i];
+      sw[4 * i] = a.x; sw[4 * i + 1] = a.y; sw[4 * i + 2] = a.z; sw[4 * i + 3] = a.w;
+      zw[4 * i] = b.x; zw[4 * i + 1] = b.y; zw[4 * i + 2] = b.z; zw[4 * i + 3] = b.w;
+    }
+    const int64_t t0 = __ldg(g.group_starts + k);
+    char* kplane = k_cache + layer * dst_layer_stride_b;
+    for (int j0 = 0; j0 < G; j0 += U) {
+      uint32_t cw[U][BITS];
+      int64_t pos[U];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {  // 8 elements per output vector
-        uint32_t p[4];
-        if constexpr (BITS == 4) {
-          const uint32_t cc = cw[v];
-          const uint32_t a0 = lop3_and_or(cc, 0x000F000Fu, 0x64006400u);
-          const uint32_t a1 = lop3_and_or(cc >> 4, 0x000F000Fu, 0x64006400u);
-          const uint32_t a2 = lop3_and_or(cc >> 8, 0x000F000Fu, 0x64006400u);
-          const uint32_t a3 = lop3_and_or(cc >> 12, 0x000F000Fu, 0x64006400u);
-          p[0] = prmt(a0, a1, 0x5410);
-          p[1] = prmt(a2, a3, 0x5410);
-          p[2] = prmt(a0, a1, 0x7632);
-          p[3] = prmt(a2, a3, 0x7632);
-        } else {
-          p[0] = prmt(cw[2 * v], 0x64646464u, 0x4140);
-          p[1] = prmt(cw[2 * v], 0x64646464u, 0x4342);
-          p[2] = prmt(cw[2 * v + 1], 0x64646464u, 0x4140);
-          p[3] = prmt(cw[2 * v + 1], 0x64646464u, 0x4342);
-        }
-        uint32_t* ov = &o[v].x;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const __half2 qh = __hsub2(u32_as_h2(p[i]), k1024);
-          const __half2 y = __hfma2(qh, u32_as_h2(sw[4 * v + i]), u32_as_h2(zw[4 * v + i]));
-          ov[i] = h2_as_u32(__hmin2(y, kmax));
-        }
+      for (int u = 0; u < U; ++u) {
+        const int64_t row = k * G + j0 + u;
+        pos[u] = __ldg(dst_slots + t0 + j0 + u);
+        kchan_load_codes<BITS>(lc + (row * g.row_elems) * BITS / 8 + int64_t(c) * CB, cw[u]);
       }
-      st256(dst + c * 64, o[0], o[1]);
-      st256(dst + c * 64 + 32, o[2], o[3]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (pos[u] >= 0)
+          kchan_dequant_store<BITS>(cw[u], sw, zw, kplane + pos[u] * g.row_elems * 2 + int64_t(c) * 64);
     }
   }
 }
