@@ -66,7 +66,7 @@ def _time_handoff(src_dev, dst_dev, L, T, H, D, bits, reps=5):
     kc = torch.zeros((L, nb, 16, H, D), dtype=torch.float16, device=dst_dev)
     vc = torch.zeros_like(kc)
     plan = HandoffPlan(KVPlanes.dense(kv), KVPlanes.paged(kc, vc, slots), T, KvPrecision(bits),
-                       128, mode="pull", n_chunks=min(8, L))
+                       128, mode="pull", n_chunks=min(8, L), min_chunk_bytes=128 << 20)
     for _ in range(2):
         plan.run()
     torch.cuda.synchronize(src_dev)

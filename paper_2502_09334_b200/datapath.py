@@ -379,7 +379,7 @@ class HandoffPlan:
 
     def __init__(self, src: KVPlanes, dst: KVPlanes, n_tokens: int, prec=KvPrecision(4),
                  group_size: int = DEFAULT_GROUP, mode: str = "pull", n_chunks: int = 8,
-                 bulk: bool | None = None):
+                 bulk: bool | None = None, min_chunk_bytes: int = 0):
         self.src, self.dst = src, dst
         # TMA bulk-staged K3 by default when the payload is read over NVLink
         self.bulk = (mode == "pull") if bulk is None else bool(bulk)
@@ -396,6 +396,8 @@ class HandoffPlan:
         else:
             enable_peer(self.p_dev.index, self.d_dev.index)
         self.mode = mode
+        if min_chunk_bytes:  # short hand-offs: fewer, larger chunks (launch overhead)
+            n_chunks = min(n_chunks, max(1, -(-self.layout.fp16_bytes // min_chunk_bytes)))
         self.chunks = layer_chunks(self.layout.n_layers, n_chunks)
         # push: payload lives on D (K1 writes it remotely); pull/local: on P;
         # copy: one buffer on each side.
@@ -505,6 +507,8 @@ class HostHandoff:
         bits = _bits_of(prec)
         self.layout = _layout_for(self.src, kv_host.shape[2], bits, group_size)
         self.packed = alloc_packed(self.layout, self.device)
+        if min_chunk_bytes:  # short hand-offs: fewer, larger chunks (launch overhead)
+            n_chunks = min(n_chunks, max(1, -(-self.layout.fp16_bytes // min_chunk_bytes)))
         self.chunks = layer_chunks(self.layout.n_layers, n_chunks)
         with torch.cuda.device(self.device):
             self.h2d, self.comp, self.d2h = (torch.cuda.Stream() for _ in range(3))
