@@ -507,8 +507,6 @@ class HostHandoff:
         bits = _bits_of(prec)
         self.layout = _layout_for(self.src, kv_host.shape[2], bits, group_size)
         self.packed = alloc_packed(self.layout, self.device)
-        if min_chunk_bytes:  # short hand-offs: fewer, larger chunks (launch overhead)
-            n_chunks = min(n_chunks, max(1, -(-self.layout.fp16_bytes // min_chunk_bytes)))
         self.chunks = layer_chunks(self.layout.n_layers, n_chunks)
         with torch.cuda.device(self.device):
             self.h2d, self.comp, self.d2h = (torch.cuda.Stream() for _ in range(3))
