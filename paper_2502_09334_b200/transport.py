@@ -130,6 +130,16 @@ class ChannelSpec:
         return layer_chunks(self.n_layers, self.n_chunks)
 
 
+def pull_chunk_plan(n_layers: int, fp16_bytes: int, n_chunks: int, min_chunk_bytes: int):
+    """(chunks, layers_per_chunk) of one pull hand-off: at most ``n_chunks``
+    uniform layer chunks, none carrying less than ``min_chunk_bytes`` of fp16
+    KV -- a short prompt goes as ONE chunk (per-chunk launch and doorbell
+    overhead would dominate it).  Both ends derive it from the token count."""
+    want = max(1, -(-int(fp16_bytes) // max(1, int(min_chunk_bytes))))
+    n = max(1, min(int(n_chunks), want))
+    return layer_chunks(n_layers, n), layers_per_chunk(n_layers, n)
+
+
 def exchange(obj, group=None):
     """all_gather_object over the control group (gloo)."""
     import torch.distributed as dist
@@ -279,14 +289,8 @@ class PairChannel:
         return base + 4 * (2 * PULL_MAX_CHUNKS + h)
 
     def _pull_chunks(self, lay):
-        """Chunking of one pull hand-off: at most spec.n_chunks, and no chunk
-        smaller than PULL_CHUNK_TARGET fp16 bytes -- a short prompt goes as ONE
-        chunk (per-chunk launch and doorbell overhead dominates it otherwise).
-        Both ends derive the same chunks from the token count."""
-        want = max(1, -(-lay.fp16_bytes // max(1, self.spec.min_chunk_bytes)))
-        n = min(self.spec.n_chunks, want)
-        lpc = layers_per_chunk(lay.n_layers, n)
-        return layer_chunks(lay.n_layers, n), lpc
+        return pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
+                               self.spec.min_chunk_bytes)
 
     def _send_pull(self, src, lay, e, s, cur, timing, stage_in):
         h = e & 1
@@ -369,9 +373,8 @@ class PairChannel:
         if lay.n_tokens != n_tokens:
             raise ValueError("seqlens must sum to n_tokens")
         gs, rt = kivi_groups(seqlens, lay.group)
-        nchunk = min(self.spec.n_chunks,
-                     max(1, -(-lay.fp16_bytes // max(1, self.spec.min_chunk_bytes))))
-        chunks = layer_chunks(lay.n_layers, nchunk)
+        chunks, _ = pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
+                                    self.spec.min_chunk_bytes)
         return lay, gs, rt, chunks, e & 1
 
     def _send_kivi(self, src, n_tokens, seqlens, e):

@@ -85,3 +85,44 @@ def test_handle_exchange_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert all(res.values()) and len(res) == world
+
+
+def test_pull_chunk_plan():
+    from paper_2502_09334_b200.transport import pull_chunk_plan
+    # config 4 pair (2.68 GB fp16): the full 8 chunks of 10 layers
+    chunks, lpc = pull_chunk_plan(80, 2_684_354_560, 8, 128 << 20)
+    assert lpc == 10 and len(chunks) == 8 and chunks[-1] == (70, 80)
+    # a 128-token 70B-GQA prompt (42 MB): one chunk
+    chunks, lpc = pull_chunk_plan(80, 41_943_040, 8, 128 << 20)
+    assert chunks == [(0, 80)] and lpc == 80
+    # min_chunk_bytes=0 keeps the requested chunking (tests exercise the pipeline)
+    chunks, lpc = pull_chunk_plan(6, 10_000, 3, 0)
+    assert chunks == [(0, 2), (2, 4), (4, 6)] and lpc == 2
+    # the in-kernel doorbell rule (chunk of layer l = l // lpc) matches the list
+    for L, n in ((40, 8), (33, 7), (80, 16), (5, 8)):
+        chunks, lpc = pull_chunk_plan(L, 1 << 40, n, 1)
+        for c, (l0, l1) in enumerate(chunks):
+            assert all(l // lpc == c for l in range(l0, l1))
+
+
+def test_kivi_capacity_covers_every_split():
+    from hypothesis import given, settings, strategies as st
+
+    spec = ChannelSpec(5, 300, 4, 128, 4, 32, 3, "pull", format="kivi")
+
+    @settings(max_examples=200, deadline=None)
+    @given(st.lists(st.integers(0, 300), min_size=1, max_size=16))
+    def check(lens):
+        total, seq = 0, []
+        for n in lens:
+            if total + n > 300:
+                break
+            seq.append(n)
+            total += n
+        if not seq:
+            return
+        assert spec.kivi_layout(seq).nbytes <= spec.capacity_bytes
+
+    check()
+    with pytest.raises(ValueError):
+        ChannelSpec(5, 300, 4, 128, 4, 32, 3, "push", format="kivi")
