@@ -92,6 +92,21 @@ int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_strid
                    int64_t payload_layer_stride, void* stream);
 
 /*
+ * K1 with device-side doorbells (fused quantise -> NVLink pull pipeline):
+ * same contract as kvx_quant_pack (bits 2/4/8), plus for every chunk of
+ * layers_per_chunk layers the kernel itself sets peer_ready_flags[chunk] = 1
+ * (a peer/IPC-mapped address on the decode GPU; fence.sys + st.release.sys)
+ * as soon as the chunk's payload is complete, while it keeps quantising later
+ * layers.  counters: n_chunks u32 of scratch on this GPU (zeroed by the call).
+ */
+int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                          const int64_t* src_slots, int64_t n_layers, int64_t n_tokens,
+                          int n_heads, int head_dim, int group, int bits, void* codes,
+                          void* scale, void* zero, int64_t payload_layer_stride,
+                          void* counters, void* peer_ready_flags, int layers_per_chunk,
+                          void* stream);
+
+/*
  * K3: unpack + dequantise + scatter into the decode side's paged KV cache.
  * Replaces the ready = prefill_done + kv_delay step (simulate.py:235) with the
  * real decode-side enrolment.  codes/scale/zero may be peer pointers (fused

@@ -123,15 +123,37 @@ cudaError_t make_items(const kvx::Geo& g, kvx::ItemGeo& ig) {
   return cudaSuccess;
 }
 
+// Doorbell request for kvx_quant_pack_signal (null peer_flags = plain K1).
+struct SignalReq {
+  uint32_t* counters = nullptr;
+  uint32_t* peer_flags = nullptr;
+  int layers_per_chunk = 1;
+  int64_t n_layers = 0;
+};
+
 template <int BITS, int G>
-cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero, cudaStream_t s) {
+cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero, cudaStream_t s,
+                         const SignalReq& rq = SignalReq()) {
   kvx::ItemGeo ig;
   cudaError_t e = make_items(g, ig);
   if (e != cudaSuccess) return e;
+  kvx::SignalGeo sig;
+  sig.counters = rq.counters;
+  sig.peer_flags = rq.peer_flags;
+  sig.items_per_chunk = 1;
+  if (rq.peer_flags) {
+    const int64_t per_layer = ig.n_items / (rq.n_layers > 0 ? rq.n_layers : 1);
+    const int64_t ipc = per_layer * rq.layers_per_chunk;
+    if (ipc <= 0 || ipc >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    sig.items_per_chunk = uint32_t(ipc);
+    const int64_t n_chunks = (ig.n_items + ipc - 1) / ipc;
+    e = cudaMemsetAsync(rq.counters, 0, size_t(n_chunks) * 4, s);
+    if (e != cudaSuccess) return e;
+  }
   auto k = kvx::quant_pack_kernel<BITS, G>;
   k<<<grid_for(k, ig.n_items), kThreads, 0, s>>>(g, ig, static_cast<uint8_t*>(codes),
                                                  static_cast<__half*>(scale),
-                                                 static_cast<__half*>(zero));
+                                                 static_cast<__half*>(zero), sig);
   return cudaGetLastError();
 }
 
@@ -226,11 +248,12 @@ cudaError_t dispatch_pull(int group, const kvx::Geo& g, const void* c, const voi
 }
 
 template <int BITS>
-cudaError_t dispatch_quant(int group, const kvx::Geo& g, void* c, void* sc, void* z, cudaStream_t s) {
+cudaError_t dispatch_quant(int group, const kvx::Geo& g, void* c, void* sc, void* z, cudaStream_t s,
+                           const SignalReq& rq = SignalReq()) {
   switch (group) {
-    case 32: return launch_quant<BITS, 32>(g, c, sc, z, s);
-    case 64: return launch_quant<BITS, 64>(g, c, sc, z, s);
-    default: return launch_quant<BITS, 128>(g, c, sc, z, s);
+    case 32: return launch_quant<BITS, 32>(g, c, sc, z, s, rq);
+    case 64: return launch_quant<BITS, 64>(g, c, sc, z, s, rq);
+    default: return launch_quant<BITS, 128>(g, c, sc, z, s, rq);
   }
 }
 
@@ -362,6 +385,38 @@ int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_strid
     case 2: return dispatch_quant<2>(group, g, codes, scale, zero, s);
     case 8: return dispatch_quant<8>(group, g, codes, scale, zero, s);
     default: return dispatch_quant<4>(group, g, codes, scale, zero, s);
+  }
+}
+
+int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                          const int64_t* src_slots, int64_t n_layers, int64_t n_tokens,
+                          int n_heads, int head_dim, int group, int bits, void* codes,
+                          void* scale, void* zero, int64_t payload_layer_stride,
+                          void* counters, void* peer_ready_flags, int layers_per_chunk,
+                          void* stream) {
+  int rc = valid_format(head_dim, group, bits);
+  if (rc) return rc;
+  if (bits == 16 || !counters || !peer_ready_flags || layers_per_chunk < 1 ||
+      !aligned(counters, 4) || !aligned(peer_ready_flags, 4))
+    return KVX_ERR_INVALID_ARG;
+  kvx::Geo g;
+  rc = make_geo(g, k_src, v_src, src_layer_stride, src_slots, n_layers, n_tokens, n_heads, head_dim,
+                group, bits, payload_layer_stride);
+  if (rc) return rc;
+  if (g.n_token_rows == 0) return KVX_OK;
+  if (!codes || !scale || !zero || !aligned(codes, 8 * bits) || !aligned(scale, 2) ||
+      !aligned(zero, 2) || !aligned(k_src, 32) || !aligned(v_src, 32) || (src_layer_stride * 2) % 32)
+    return KVX_ERR_INVALID_ARG;
+  SignalReq rq;
+  rq.counters = static_cast<uint32_t*>(counters);
+  rq.peer_flags = static_cast<uint32_t*>(peer_ready_flags);
+  rq.layers_per_chunk = layers_per_chunk;
+  rq.n_layers = n_layers;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (bits) {
+    case 2: return dispatch_quant<2>(group, g, codes, scale, zero, s, rq);
+    case 8: return dispatch_quant<8>(group, g, codes, scale, zero, s, rq);
+    default: return dispatch_quant<4>(group, g, codes, scale, zero, s, rq);
   }
 }
 

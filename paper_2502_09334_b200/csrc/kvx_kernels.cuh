@@ -345,17 +345,48 @@ __device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)
   }
 }
 
-template <int BITS, int G>
 #ifndef KVX_K1_MIN_BLOCKS
 #define KVX_K1_MIN_BLOCKS 1
 #endif
 #ifndef KVX_K1_PF
 #define KVX_K1_PF 2  // items prefetched ahead per warp (A/B: profiles/r01_summary.md)
 #endif
+// Device-side doorbells for the fused quantise -> NVLink-pull pipeline: with
+// `sig.peer_flags` set, every warp arrives once per layer chunk it touched,
+// right after its last item of that chunk; the last arriving warp publishes
+// the chunk to the decode GPU (fence.sys + st.release.sys into the peer's
+// ready flag).  Warps walk items in global order, so chunks complete
+// progressively while the kernel is still running: ONE launch feeds the
+// decode side layer by layer, no per-chunk launches or host round trips.
+struct SignalGeo {
+  uint32_t* counters;    // [n_chunks] arrivals (zeroed before the launch)
+  uint32_t* peer_flags;  // [n_chunks] decode-side ready flags (IPC/peer mapped), or null
+  uint32_t items_per_chunk;
+};
+
+__device__ __forceinline__ void chunk_arrive(const SignalGeo& sig, uint32_t c, uint32_t n_items,
+                                             uint32_t n_warps, int lane) {
+  __threadfence();  // this lane's payload stores, device-wide
+  __syncwarp();
+  if (lane == 0) {
+    const uint32_t a = c * sig.items_per_chunk;
+    const uint32_t b = min(n_items, a + sig.items_per_chunk);
+    const uint32_t expected = min(n_warps, b - a);  // warps owning >= 1 item of the chunk
+    const uint32_t old = atomicAdd(sig.counters + c, 1u);
+    if (old + 1 == expected) {
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags + c), "r"(1u)
+                   : "memory");
+    }
+  }
+}
+
+template <int BITS, int G>
 __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo g, ItemGeo ig,
                                                          uint8_t* __restrict__ codes,
                                                          __half* __restrict__ scale,
-                                                         __half* __restrict__ zero) {
+                                                         __half* __restrict__ zero,
+                                                         SignalGeo sig) {
   // Ring of PF+1 register buffers: the loads of the next PF items are in
   // flight while the current one is quantised (all indices compile-time).
   constexpr int NB = KVX_K1_PF + 1;
@@ -390,6 +421,12 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
         }
       }
       k1_process<BITS, G>(it[st], w[st], lane);
+      if (sig.peer_flags) {
+        const uint32_t c = cur / sig.items_per_chunk;
+        const uint32_t nxt = cur + n_warps;
+        if (nxt >= ig.n_items || nxt / sig.items_per_chunk != c)
+          chunk_arrive(sig, c, ig.n_items, n_warps, lane);
+      }
     }
   }
 }

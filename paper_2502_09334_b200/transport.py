@@ -88,6 +88,7 @@ class ChannelSpec:
     mode: str = "pull"
     min_chunk_bytes: int = PULL_CHUNK_TARGET  # pull modes: smaller hand-offs use fewer chunks
     format: str = "default"  # "default" (per-token groups) or "kivi" (pull modes only)
+    device_doorbells: bool = True  # "pull": K1 itself rings per-chunk doorbells (one launch)
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -233,6 +234,7 @@ class PairChannel:
         # local buffers: doorbells (written by the partner) + payload staging
         self.flags = IpcBuffer(FLAG_SLOTS * 4)
         self.graphs = bool(graphs) and mode in PULL_MODES
+        self.counters = torch.zeros(PULL_MAX_CHUNKS, dtype=torch.int32, device=self.device)
         self._graphs, self._seen = {}, set()
         if mode in PULL_MODES:
             if len(self.chunks) > PULL_MAX_CHUNKS:
@@ -288,21 +290,42 @@ class PairChannel:
     def _pfree(self, base: int, h: int) -> int:
         return base + 4 * (2 * PULL_MAX_CHUNKS + h)
 
+    def _fused(self, lay) -> bool:
+        """One K1 launch ringing device-side doorbells -> one K3-bulk launch
+        waiting on them (both ends decide identically from the layout)."""
+        return (self.spec.mode == "pull" and self.spec.device_doorbells and
+                pull_supported(lay))
+
     def _pull_chunks(self, lay):
+        if self._fused(lay):  # chunks cost nothing here: layer-granular doorbells
+            n = min(lay.n_layers, PULL_MAX_CHUNKS)
+            return layer_chunks(lay.n_layers, n), layers_per_chunk(lay.n_layers, n)
         return pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
                                self.spec.min_chunk_bytes)
 
     def _send_pull(self, src, lay, e, s, cur, timing, stage_in):
         h = e & 1
-        chunks, _ = self._pull_chunks(lay)
+        chunks, lpc = self._pull_chunks(lay)
         key = ("send", lay.n_tokens, h, src.k.data_ptr(), src.slots_ptr)
         if self._graph_ok(key, timing, stage_in):
             return self._replay(key, s, cur)
         payload = PackedKV(lay, self.k1_target + self._half(e), self.device)
 
+        fused = self._fused(lay) and stage_in is None
+
         def body():
             wait(self._pfree(self.flags.ptr, h), 1, s)        # D is done with this half
             signal(self._pfree(self.flags.ptr, h), 0, s)      # claim it
+            if fused:
+                ev = _kernel_events(timing, s, "k1")
+                k, v = src.ptrs(0)
+                c0, sc0, z0 = payload.ptrs(0)
+                _lib.call("kvx_quant_pack_signal", k, v, src.layer_stride, src.slots_ptr,
+                          lay.n_layers, lay.n_tokens, lay.n_heads, lay.head_dim, lay.group,
+                          lay.bits, c0, sc0, z0, lay.layer_stride, self.counters.data_ptr(),
+                          self._pready(self.peer_flags, h, 0), lpc, _stream_ptr(s))
+                _kernel_events_end(ev, s)
+                return
             for c, (l0, l1) in enumerate(chunks):
                 if stage_in is not None:
                     host, devt = stage_in

@@ -32,8 +32,12 @@ def main():
     seq = (Tmax, 77, Tmax, 77, Tmax, 77, 130, Tmax)
     for mode in modes:
         for bits in (4, 8, 16):
-            spec = ChannelSpec(L, Tmax, H, D, bits, 64 if bits != 16 else 128, 3, mode,
-                               min_chunk_bytes=0)  # always 3 chunks: exercise the pipeline
+            # "pull_hostdb": pull with host-enqueued per-chunk doorbells instead
+            # of the fused K1 ringing them from the device
+            spec = ChannelSpec(L, Tmax, H, D, bits, 64 if bits != 16 else 128, 3,
+                               "pull" if mode == "pull_hostdb" else mode,
+                               min_chunk_bytes=0,  # always 3 chunks: exercise the pipeline
+                               device_doorbells=(mode != "pull_hostdb"))
             ch = PairChannel(spec, rank, world, control_group=ctrl)
             nb = Tmax // bs + 4
             kv_cap = torch.zeros((L, 2, Tmax, H, D), dtype=torch.float16, device=dev)

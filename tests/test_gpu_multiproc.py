@@ -17,7 +17,7 @@ def test_modes_over_ipc(cuda, nproc):
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29533",
-           os.path.join(HERE, "mp_handoff_check.py"), "pull,pull_ldg,push,copy,nccl"]
+           os.path.join(HERE, "mp_handoff_check.py"), "pull,pull_hostdb,pull_ldg,push,copy,nccl"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "failures=0" in r.stdout
