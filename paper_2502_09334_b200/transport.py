@@ -223,11 +223,12 @@ class PairChannel:
         self._prev_ranges = None
         self.chunks = spec.chunks()
         self.lpc = layers_per_chunk(spec.n_layers, spec.n_chunks)
-        self.k_done = [torch.cuda.Event() for _ in self.chunks]
-        self.comm_done = [torch.cuda.Event() for _ in self.chunks]
+        n_ev = PULL_MAX_CHUNKS if mode in PULL_MODES else len(self.chunks)
+        self.k_done = [torch.cuda.Event() for _ in range(n_ev)]
+        self.comm_done = [torch.cuda.Event() for _ in range(n_ev)]
         self.xfer = torch.cuda.Stream(self.device)      # host <-> device staging
-        self.x_ready = [torch.cuda.Event() for _ in self.chunks]
-        self.x_done = [torch.cuda.Event() for _ in self.chunks]
+        self.x_ready = [torch.cuda.Event() for _ in range(n_ev)]
+        self.x_done = [torch.cuda.Event() for _ in range(n_ev)]
         mode = spec.mode
         if mode != "nccl" and not memops_supported():
             raise RuntimeError("stream memory operations unavailable: use mode='nccl'")
