@@ -50,6 +50,7 @@ PULL_MODES = ("pull", "pull_ldg")
 FLAG_SLOTS = 256  # 32-bit doorbells per rank
 PULL_MAX_CHUNKS = 64
 PULL_CHUNK_TARGET = 128 << 20  # min fp16 bytes per pull chunk
+K1_WARPS_EST = 148 * 2 * 8     # resident K1 warps on a B200 (2 x 256-thread CTAs per SM)
 
 
 # ---------------------------------------------------------------------------
@@ -298,8 +299,12 @@ class PairChannel:
                 pull_supported(lay))
 
     def _pull_chunks(self, lay):
-        if self._fused(lay):  # chunks cost nothing here: layer-granular doorbells
-            n = min(lay.n_layers, PULL_MAX_CHUNKS)
+        if self._fused(lay):
+            # layer-granular doorbells, but every K1 warp should own several
+            # items per chunk (one fence + atomic per warp per chunk)
+            cpr = lay.n_heads * lay.head_dim // 32
+            items = lay.n_layers * 2 * lay.n_tokens * (-(-cpr // 32))
+            n = max(1, min(lay.n_layers, PULL_MAX_CHUNKS, items // (4 * K1_WARPS_EST)))
             return layer_chunks(lay.n_layers, n), layers_per_chunk(lay.n_layers, n)
         return pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
                                self.spec.min_chunk_bytes)
