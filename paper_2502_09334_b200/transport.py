@@ -224,7 +224,7 @@ class PairChannel:
         self._prev_ranges = None
         self.chunks = spec.chunks()
         self.lpc = layers_per_chunk(spec.n_layers, spec.n_chunks)
-        n_ev = PULL_MAX_CHUNKS if mode in PULL_MODES else len(self.chunks)
+        n_ev = PULL_MAX_CHUNKS if spec.mode in PULL_MODES else len(self.chunks)
         self.k_done = [torch.cuda.Event() for _ in range(n_ev)]
         self.comm_done = [torch.cuda.Event() for _ in range(n_ev)]
         self.xfer = torch.cuda.Stream(self.device)      # host <-> device staging
