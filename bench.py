@@ -444,6 +444,8 @@ def emit(args, r, world):
         "clocks": r["clocks"],
         "gpu_launches": r["launches"],
     }
+    if r.get("calibration"):
+        out["calibration"] = r["calibration"]
     print(json.dumps(out), flush=True)
 
 

@@ -707,6 +707,22 @@ def _verify_last(ch, trace, tok, it, L, H, D, spec, ctrl, kv=None, dec=None):
     return all(exchange(ok, ctrl))
 
 
+def _calibration(spec, T, ms_large, ms_small, t_small=16):
+    """(alpha, beta) of t = alpha + V/beta with V the reference's modelled
+    volume 2*b*s*h*bits/8*L (costs.py:102) -- what calibrate.cluster_dict and
+    measured_kv_comm_cost consume."""
+    from .calibrate import fit_alpha_beta
+    v_large = spec.layout(T).fp16_bytes * spec.bits / 16
+    v_small = spec.layout(t_small).fp16_bytes * spec.bits / 16
+    try:
+        alpha, beta = fit_alpha_beta(ms_small * 1e-3, v_small, ms_large * 1e-3, v_large)
+    except ValueError:
+        return None
+    return {"alpha_us": round(alpha * 1e6, 2), "beta_GBps_of_modelled_volume": round(beta / 1e9, 1),
+            "small_handoff_us": round(ms_small * 1e3, 2), "small_tokens": t_small,
+            "note": "t = alpha + (2*b*s*h*bits/8*L)/beta, per pair, CUDA-graph replayed"}
+
+
 def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
     """Weak-scaling pair benchmark: every pair hands off the same workload."""
     import json
@@ -827,6 +843,31 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
                                 kv if ch.role == "prefill" else None,
                                 (kc, vc, planes if trace is None else planes_b)
                                 if ch.role == "decode" else None)
+    # alpha-beta calibration of this very channel (graph-replayed pull): a
+    # 16-token hand-off against the main one -> kv_comm_cost's (alpha, beta)
+    # for the reference's volume at this bit-width
+    cal_small_ms = 0.0
+    if trace is None and not kivi:
+        t_small = 16
+        if ch.role == "prefill":
+            small = lambda: ch.send(planes, t_small)  # noqa: E731
+        else:
+            sl_small = KVPlanes.paged(kc, vc, planes.slots[:t_small])
+            small = lambda: ch.recv(sl_small, t_small)  # noqa: E731
+        for _ in range(3):
+            small()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_cal = 50
+        c0.record()
+        for _ in range(n_cal):
+            small()
+        c1.record()
+        torch.cuda.synchronize()
+        cal_small_ms = c0.elapsed_time(c1) / n_cal
+        dist.barrier()
     # e2e through the same public API with host buffers: pinned host KV on the
     # prefill side (H2D inside the step), pinned host paged cache on the decode
     # side (D2H inside the step)
@@ -860,7 +901,7 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
         e2e_ms = e0.elapsed_time(e1) / n_e2e
         dist.barrier()
     stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0), e2e_ms, h2d, d2h,
-                          launches], dtype=torch.float64, device=dev)
+                          launches, cal_small_ms], dtype=torch.float64, device=dev)
     gathered = [torch.zeros_like(stats) for _ in range(world)]
     dist.all_gather(gathered, stats)
     clocks = exchange(clk.summary(), ctrl)
@@ -911,6 +952,8 @@ def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
                       "k3_link_gbs": round(k3_link, 1) if k3_link else None,
                       "frac_of_nominal_900": round(link_gbs / 900.0, 4),
                       "hbm_peak": hbm},
+            calibration=_calibration(spec, T, ms_max, float(g[:, 7].max())) if (
+                trace is None and not kivi) else None,
             extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
                    "format": spec.format,
                    "cuda_graphs": bool(ch.graphs),
