@@ -299,7 +299,8 @@ int kivi_check(int head_dim, int group, int bits) {
 
 template <int BITS, int G>
 cudaError_t launch_kchan_quant(const kvx::KchanGeo& kg, cudaStream_t s) {
-  const int cblocks = (kg.row_elems + 255) / 256;
+  constexpr int cta_ch = 4 * (32 / (G / 16)) * 8;  // matches quant_pack_kchan_kernel
+  const int cblocks = (kg.row_elems + cta_ch - 1) / cta_ch;
   const int64_t items = kg.n_layers * kg.n_groups * cblocks;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -22,74 +22,120 @@ struct KchanGeo {
   int64_t payload_ls;       // bytes between payload layers
 };
 
-// One thread = 2 adjacent channels x G tokens (G half2 registers): one pass,
-// min/max along tokens, then quantise from registers.  A block of 128
-// threads covers 256 channels of one (layer, group).
+// G/16 lanes own 8 adjacent channels x G tokens: each lane loads 16 of the
+// group's tokens with 16-byte loads (a warp reads 256-byte row segments),
+// min/max is reduced over its tokens and then across the lanes with
+// log2(G/16) shuffles, and each lane quantises its own tokens from registers
+// (8 nibbles = one 32-bit store per token at 4-bit).
 template <int BITS, int G>
 __global__ void __launch_bounds__(128) quant_pack_kchan_kernel(KchanGeo g) {
   constexpr uint32_t QMAX = (1u << BITS) - 1u;
   constexpr float QMAXF = float(QMAX);
-  const int cblocks = (g.row_elems + 255) / 256;
+  constexpr int TH = 16;      // tokens per lane (16 x 16 B = 64 registers of data)
+  constexpr int LPC = G / TH;  // lanes sharing one 8-channel block (2 at G=32, 4 at G=64)
+  constexpr int CTA_CH = 4 * (32 / LPC) * 8;  // channels per 128-thread CTA
+  const int lane = threadIdx.x & 31;
+  const int half = lane % LPC;  // which TH-token slice of the group
+  const int cbw = (threadIdx.x >> 5) * (32 / LPC) + lane / LPC;  // 8-channel block in the CTA
+  const int cblocks = (g.row_elems + CTA_CH - 1) / CTA_CH;
   const int64_t n_items = g.n_layers * g.n_groups * cblocks;
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int64_t lg = item / cblocks;
     const int cb = int(item - lg * cblocks);
     const int64_t layer = lg / g.n_groups;
     const int64_t k = lg - layer * g.n_groups;
-    const int ch = cb * 256 + threadIdx.x * 2;
+    const int ch = cb * CTA_CH + cbw * 8;
     const bool active = ch < g.row_elems;
-    const int64_t t0 = __ldg(g.group_starts + k);
+    const int64_t t0 = __ldg(g.group_starts + k) + half * TH;
     const char* src = g.k_plane + layer * g.layer_stride_b + (t0 * g.row_elems + ch) * 2;
-    uint32_t w[G];
+    uint4 w[TH];
 #pragma unroll
-    for (int j = 0; j < G; ++j)
-      w[j] = active ? __ldg(reinterpret_cast<const uint32_t*>(src + int64_t(j) * g.row_elems * 2))
-                    : 0u;
-    __half2 mn = u32_as_h2(w[0]), mx = u32_as_h2(w[0]);
-#pragma unroll
-    for (int j = 1; j < G; ++j) {
-      mn = __hmin2(mn, u32_as_h2(w[j]));
-      mx = __hmax2(mx, u32_as_h2(w[j]));
+    for (int j = 0; j < TH; ++j) {
+      if (active) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(w[j].x), "=r"(w[j].y), "=r"(w[j].z), "=r"(w[j].w)
+                     : "l"(src + int64_t(j) * g.row_elems * 2));
+      } else {
+        w[j] = make_uint4(0, 0, 0, 0);
+      }
     }
-    float zf[2], inv[2];
-    __half z16[2], s16[2];
+    __half2 mn[4], mx[4];
+    mn[0] = mx[0] = u32_as_h2(w[0].x);
+    mn[1] = mx[1] = u32_as_h2(w[0].y);
+    mn[2] = mx[2] = u32_as_h2(w[0].z);
+    mn[3] = mx[3] = u32_as_h2(w[0].w);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float fmn = h ? __high2float(mn) : __low2float(mn);
-      const float fmx = h ? __high2float(mx) : __low2float(mx);
-      z16[h] = __float2half_rn(__fadd_rn(fmn, 0.0f));
-      s16[h] = __float2half_rn(__fadd_rn(__fdiv_rn(__fsub_rn(fmx, fmn), QMAXF), 0.0f));
-      const float s = __half2float(s16[h]);
-      inv[h] = (s != 0.0f) ? __frcp_rn(s) : 0.0f;
-      zf[h] = __half2float(z16[h]);
+    for (int j = 1; j < TH; ++j) {
+      const uint32_t v[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        mn[i] = __hmin2(mn[i], u32_as_h2(v[i]));
+        mx[i] = __hmax2(mx[i], u32_as_h2(v[i]));
+      }
     }
-    const bool sub = active && ((__half2float(s16[0]) != 0.0f && __half2float(s16[0]) < 6.103515625e-05f) ||
-                                (__half2float(s16[1]) != 0.0f && __half2float(s16[1]) < 6.103515625e-05f));
-    const bool clamp = __any_sync(0xffffffffu, sub);
+#pragma unroll
+    for (int off = 1; off < LPC; off <<= 1)  // combine the lanes' token slices
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        mn[i] = __hmin2(mn[i], u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(mn[i]), off)));
+        mx[i] = __hmax2(mx[i], u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(mx[i]), off)));
+      }
+    float zf[8], inv[8];
+    __half z16[8], s16[8];
+    bool sub = false;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float fmn = (c & 1) ? __high2float(mn[c >> 1]) : __low2float(mn[c >> 1]);
+      const float fmx = (c & 1) ? __high2float(mx[c >> 1]) : __low2float(mx[c >> 1]);
+      z16[c] = __float2half_rn(__fadd_rn(fmn, 0.0f));
+      s16[c] = __float2half_rn(__fadd_rn(__fdiv_rn(__fsub_rn(fmx, fmn), QMAXF), 0.0f));
+      const float sv = __half2float(s16[c]);
+      inv[c] = (sv != 0.0f) ? __frcp_rn(sv) : 0.0f;
+      zf[c] = __half2float(z16[c]);
+      sub |= sv != 0.0f && sv < 6.103515625e-05f;
+    }
+    const bool clamp = __any_sync(0xffffffffu, active && sub);
     if (active) {
       char* lc = g.codes + layer * g.payload_ls;
-      const int64_t meta = (k * g.row_elems + ch) * 2;
-      *reinterpret_cast<__half2*>(g.scale + layer * g.payload_ls + meta) = __halves2half2(s16[0], s16[1]);
-      *reinterpret_cast<__half2*>(g.zero + layer * g.payload_ls + meta) = __halves2half2(z16[0], z16[1]);
-      unsigned long long invv;
-      asm("mov.b64 %0, {%1, %2};" : "=l"(invv) : "f"(inv[0]), "f"(inv[1]));
+      if (half == 0) {  // one lane of the pair writes the 8 scales / zeros (16 B each)
+        const int64_t meta = (k * g.row_elems + ch) * 2;
+        uint4 sv, zv;
+        sv.x = h2_as_u32(__halves2half2(s16[0], s16[1])); sv.y = h2_as_u32(__halves2half2(s16[2], s16[3]));
+        sv.z = h2_as_u32(__halves2half2(s16[4], s16[5])); sv.w = h2_as_u32(__halves2half2(s16[6], s16[7]));
+        zv.x = h2_as_u32(__halves2half2(z16[0], z16[1])); zv.y = h2_as_u32(__halves2half2(z16[2], z16[3]));
+        zv.z = h2_as_u32(__halves2half2(z16[4], z16[5])); zv.w = h2_as_u32(__halves2half2(z16[6], z16[7]));
+        *reinterpret_cast<uint4*>(g.scale + layer * g.payload_ls + meta) = sv;
+        *reinterpret_cast<uint4*>(g.zero + layer * g.payload_ls + meta) = zv;
+      }
+      unsigned long long invv[4];
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        unsigned long long x, r;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(sub_lo(w[j], zf[0])), "f"(sub_hi(w[j], zf[1])));
-        asm("{.reg .b64 mg; mov.b64 mg, {%3, %3}; fma.rn.f32x2 %0, %1, %2, mg;}"
-            : "=l"(r) : "l"(x), "l"(invv), "f"(8388608.0f));
-        uint32_t b0 = uint32_t(r), b1 = uint32_t(r >> 32);
-        if (clamp) {
-          b0 = min(b0 - 0x4B000000u, QMAX);
-          b1 = min(b1 - 0x4B000000u, QMAX);
+      for (int i = 0; i < 4; ++i)
+        asm("mov.b64 %0, {%1, %2};" : "=l"(invv[i]) : "f"(inv[2 * i]), "f"(inv[2 * i + 1]));
+#pragma unroll
+      for (int j = 0; j < TH; ++j) {
+        const uint32_t v[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
+        uint32_t b[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          unsigned long long x, r;
+          asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(sub_lo(v[i], zf[2 * i])), "f"(sub_hi(v[i], zf[2 * i + 1])));
+          asm("{.reg .b64 mg; mov.b64 mg, {%3, %3}; fma.rn.f32x2 %0, %1, %2, mg;}"
+              : "=l"(r) : "l"(x), "l"(invv[i]), "f"(8388608.0f));
+          b[2 * i] = uint32_t(r);
+          b[2 * i + 1] = uint32_t(r >> 32);
         }
-        const int64_t row = k * G + j;  // group-major payload row
+        if (clamp) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) b[i] = min(b[i] - 0x4B000000u, QMAX);
+        }
+        const int64_t row = k * G + half * TH + j;  // group-major payload row
+        char* dst = lc + (row * g.row_elems + ch) * BITS / 8;
         if constexpr (BITS == 4) {
-          lc[(row * g.row_elems + ch) / 2] = char(lea4(b1, b0));
+          *reinterpret_cast<uint32_t*>(dst) =
+              bytes4(lea4(b[1], b[0]), lea4(b[3], b[2]), lea4(b[5], b[4]), lea4(b[7], b[6]));
         } else {
-          *reinterpret_cast<uint16_t*>(lc + row * g.row_elems + ch) =
-              uint16_t(prmt(b0, b1, 0x0040u));
+          *reinterpret_cast<uint2*>(dst) =
+              make_uint2(bytes4(b[0], b[1], b[2], b[3]), bytes4(b[4], b[5], b[6], b[7]));
         }
       }
     }
