@@ -665,305 +665,3 @@ def _kernel_events_end(ev, stream):
 # ---------------------------------------------------------------------------
 # bench.py N > 1
 # ---------------------------------------------------------------------------
-
-def _verify_last(ch, trace, tok, it, L, H, D, spec, ctrl, kv=None, dec=None):
-    """Bit-exact check of 3 layers x 32 sampled tokens of the last hand-off at
-    full size: the prefill rank ships its source rows, the decode rank runs the
-    C oracle on them and compares with its paged cache.  Returns the AND over
-    all pairs (every rank gets it)."""
-    import numpy as np
-
-    last = (it["i"] - 1) % len(tok)
-    T_last = tok[last]
-    rng = np.random.default_rng(1234 + last)
-    toks = np.sort(rng.choice(T_last, size=min(32, T_last), replace=False))
-    layers = sorted({0, L // 2, L - 1})
-    mine = None
-    if ch.role == "prefill":
-        rows = kv[layers][:, :, torch.from_numpy(toks).to(kv.device)]  # [nl, 2, n, H, D]
-        mine = rows.cpu().numpy()
-    else:
-        kc, vc, pl = dec
-        planes = pl if trace is None else pl[last]
-        sl = planes.slots[torch.from_numpy(toks).to(kc.device)]
-        ks = kc[layers].reshape(len(layers), -1, H, D)[:, sl]
-        vs = vc[layers].reshape(len(layers), -1, H, D)[:, sl]
-        mine = torch.stack([ks, vs], 1).cpu().numpy()
-    allv = exchange(mine, ctrl)
-    ok = True
-    if ch.role == "decode":
-        from oracle import kvq_oracle_c as C  # the checker, never the measured path
-        src = allv[ch.peer]
-        c, s_, z = C.quant_pack(np.ascontiguousarray(src).reshape(-1, D), spec.bits, spec.group)
-        want = C.unpack_dequant(c, s_, z, spec.bits, spec.group, D).reshape(src.shape)
-        ok = bool(np.array_equal(want.view(np.uint16), mine.view(np.uint16)))
-        if not ok and os.environ.get("KVX_VERIFY_DEBUG"):
-            bad = want.view(np.uint16) != mine.view(np.uint16)
-            print(f"[verify] rank {ch.rank}: {int(bad.sum())}/{bad.size} mismatches; per layer "
-                  f"{bad.reshape(len(layers), -1).sum(1).tolist()}; per kv {bad.sum((0, 2, 3, 4)).tolist()}"
-                  f"; per token {bad.sum((0, 1, 3, 4)).tolist()}; max|d| "
-                  f"{float(np.abs(want.astype(np.float32) - mine.astype(np.float32)).max())}",
-                  flush=True)
-    return all(exchange(ok, ctrl))
-
-
-def _calibration(spec, T, ms_large, ms_small, t_small=16):
-    """(alpha, beta) of t = alpha + V/beta with V the reference's modelled
-    volume 2*b*s*h*bits/8*L (costs.py:102) -- what calibrate.cluster_dict and
-    measured_kv_comm_cost consume."""
-    from .calibrate import fit_alpha_beta
-    v_large = spec.layout(T).fp16_bytes * spec.bits / 16
-    v_small = spec.layout(t_small).fp16_bytes * spec.bits / 16
-    try:
-        alpha, beta = fit_alpha_beta(ms_small * 1e-3, v_small, ms_large * 1e-3, v_large)
-    except ValueError:
-        return None
-    return {"alpha_us": round(alpha * 1e6, 2), "beta_GBps_of_modelled_volume": round(beta / 1e9, 1),
-            "small_handoff_us": round(ms_small * 1e3, 2), "small_tokens": t_small,
-            "note": "t = alpha + (2*b*s*h*bits/8*L)/beta, per pair, CUDA-graph replayed"}
-
-
-def bench_pairs(args, torch_mod, rank: int, world: int, emit) -> None:
-    """Weak-scaling pair benchmark: every pair hands off the same workload."""
-    import json
-    import torch.distributed as dist
-
-    import bench as B
-
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    ctrl = dist.new_group(backend="gloo")
-    wl = args.workload or B.default_pair_workload(world)
-    trace = None
-    if wl in B.TRACE_MODELS:
-        L, H, D = B.TRACE_MODELS[wl]
-        trace = B.make_trace(args.warmup + args.steps + 2, seed=0)
-        T = B.TRACE_CAP
-    else:
-        L, H, D, b, s = B.WORKLOADS[wl]
-        T = b * s
-    mode = args.mode
-    n_chunks = args.chunks or 8
-    spec = ChannelSpec(L, T, H, D, args.bits, args.group, n_chunks, mode,
-                       format=getattr(args, "format", "default"))
-    ch = PairChannel(spec, rank, world, control_group=ctrl, graphs=not args.no_graphs)
-    lay = spec.layout(T)
-    # per step token counts (fixed workload, or the trace's batches)
-    tok = [T] * (args.warmup + args.steps + 2) if trace is None else [sum(x) for x in trace]
-    seqs = ([(s,) * b] * len(tok)) if trace is None else [tuple(x) for x in trace]
-    it = {"i": 0}
-    kivi = spec.format == "kivi"
-
-    def next_t():
-        t = tok[it["i"] % len(tok)]
-        it["i"] += 1
-        return t
-
-    if ch.role == "prefill":
-        kv = B.synthetic_kv_device(torch, L, T, H, D, dev, seed=ch.pair)
-        planes = KVPlanes.dense(kv)
-        def step(timing=None):
-            i = it["i"] % len(tok)
-            t = next_t()
-            if kivi:
-                ch.send(planes, t, seqlens=seqs[i])
-            else:
-                ch.send(planes, t, timing)
-    else:
-        slots, nb = B.paged_slots(torch, T, dev, seed=ch.pair)
-        kc = torch.zeros((L, nb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
-        vc = torch.zeros_like(kc)
-        if trace is None:
-            planes = KVPlanes.paged(kc, vc, slots)
-
-            def step(timing=None):
-                i = it["i"] % len(tok)
-                t = next_t()
-                if kivi:
-                    ch.recv(planes, t, seqlens=seqs[i])
-                else:
-                    ch.recv(planes, t, timing)
-        else:
-            # each batch gets its own random block placement (requests start on
-            # a block boundary, as a paged allocator hands them out)
-            import numpy as np
-            rng = np.random.default_rng(ch.pair + 7)
-            per_batch = []
-            for lens in trace:
-                nblk = sum((n + B.BLOCK - 1) // B.BLOCK for n in lens)
-                blocks = rng.permutation(nb)[:nblk]
-                sl, bi = [], 0
-                for n in lens:
-                    t = np.arange(n)
-                    sl.append(blocks[bi + t // B.BLOCK] * B.BLOCK + t % B.BLOCK)
-                    bi += (n + B.BLOCK - 1) // B.BLOCK
-                per_batch.append(torch.from_numpy(np.concatenate(sl).astype(np.int64)).to(dev))
-            planes_b = [KVPlanes.paged(kc, vc, sl) for sl in per_batch]
-
-            def step(timing=None):
-                i = it["i"] % len(tok)
-                if kivi:
-                    ch.recv(planes_b[i], next_t(), seqlens=seqs[i])
-                else:
-                    ch.recv(planes_b[i], next_t(), timing)
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with B.ClockSampler(local) as clk:
-        t0.record()
-        for _ in range(args.steps):
-            step()  # CUDA-graph replay per hand-off once warmed up (pull modes)
-        t1.record()
-        torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1) / args.steps
-    # per-kernel durations: a separate eager pass with CUDA events on the
-    # launching streams (events cannot sit inside the captured graph)
-    timing = []
-    n_kt = max(1, min(args.steps, 5))
-    for _ in range(n_kt):
-        step(timing)
-    torch.cuda.synchronize()
-    dist.barrier()
-    kern = {}
-    for name, a, b_ in timing:
-        kern[name] = kern.get(name, 0.0) + a.elapsed_time(b_) / n_kt
-    launches = len(timing) / n_kt * args.steps
-    # full-size parity (outside the timed region): sampled token rows of the
-    # last hand-off, decode cache vs the CPU oracle applied to the source rows
-    verified = None
-    if not getattr(args, "no_verify", False) and not kivi:
-        verified = _verify_last(ch, trace, tok, it, L, H, D, spec, ctrl,
-                                kv if ch.role == "prefill" else None,
-                                (kc, vc, planes if trace is None else planes_b)
-                                if ch.role == "decode" else None)
-    # alpha-beta calibration of this very channel (graph-replayed pull): a
-    # 16-token hand-off against the main one -> kv_comm_cost's (alpha, beta)
-    # for the reference's volume at this bit-width (SURVEY 8(f)1)
-    cal_small_ms = 0.0
-    if trace is None and not kivi:
-        t_small = 16
-        if ch.role == "prefill":
-            small = lambda: ch.send(planes, t_small)  # noqa: E731
-        else:
-            sl_small = KVPlanes.paged(kc, vc, planes.slots[:t_small])
-            small = lambda: ch.recv(sl_small, t_small)  # noqa: E731
-        for _ in range(3):
-            small()
-        torch.cuda.synchronize()
-        dist.barrier()
-        torch.cuda.synchronize()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n_cal = 50
-        c0.record()
-        for _ in range(n_cal):
-            small()
-        c1.record()
-        torch.cuda.synchronize()
-        cal_small_ms = c0.elapsed_time(c1) / n_cal
-        dist.barrier()
-    # e2e through the same public API with host buffers: pinned host KV on the
-    # prefill side (H2D inside the step), pinned host paged cache on the decode
-    # side (D2H inside the step)
-    e2e_ms, h2d, d2h = 0.0, 0, 0
-    if not args.no_e2e and not kivi:
-        if ch.role == "prefill":
-            host = torch.empty(kv.shape, dtype=torch.float16, pin_memory=True)
-            host.copy_(kv)
-            stage = dict(stage_in=(host, kv))
-            h2d = host.numel() * 2
-            e2e_step = lambda: ch.send(planes, next_t(), None, **stage)  # noqa: E731
-        else:
-            hk = torch.empty(kc.shape, dtype=torch.float16, pin_memory=True)
-            hv = torch.empty(vc.shape, dtype=torch.float16, pin_memory=True)
-            stage = dict(stage_out=((kc, vc), (hk, hv)))
-            d2h = (hk.numel() + hv.numel()) * 2
-            e2e_step = (lambda: ch.recv(planes, next_t(), None, **stage)) if trace is None else (
-                lambda: ch.recv(planes_b[it["i"] % len(tok)], next_t(), None, **stage))
-        n_e2e = max(1, min(args.steps, args.e2e_steps))
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(n_e2e):
-            e2e_step()
-        e1.record()
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / n_e2e
-        dist.barrier()
-    stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0), e2e_ms, h2d, d2h,
-                          launches, cal_small_ms], dtype=torch.float64, device=dev)
-    gathered = [torch.zeros_like(stats) for _ in range(world)]
-    dist.all_gather(gathered, stats)
-    clocks = exchange(clk.summary(), ctrl)
-    if rank == 0:
-        g = torch.stack(gathered).cpu()
-        ms_max = float(g[:, 0].max())
-        k1 = float(g[:, 1].max())
-        k3 = float(g[:, 2].max())
-        pairs = world // 2
-        if kivi:
-            timed = range(args.warmup, args.warmup + args.steps)
-            fp16 = sum(spec.kivi_layout(seqs[i % len(tok)]).fp16_bytes for i in timed) / len(timed)
-            wire_mean = sum(spec.kivi_layout(seqs[i % len(tok)]).wire_bytes
-                            for i in timed) / len(timed)
-        elif trace is None:
-            fp16 = lay.fp16_bytes
-        else:  # mean fp16 bytes of the timed batches
-            timed = tok[args.warmup:args.warmup + args.steps]
-            fp16 = sum(spec.layout(t).fp16_bytes for t in timed) / len(timed)
-            wire_mean = sum(spec.layout(t).wire_bytes for t in timed) / len(timed)
-        value = pairs * fp16 / (ms_max * 1e-3) / 1e9
-        wire = lay.wire_bytes if (trace is None and not kivi) else wire_mean
-        link_gbs = wire / (ms_max * 1e-3) / 1e9  # per pair
-        hbm, peak_kind = B.peaks()
-        k3_link = wire / (k3 * 1e-3) / 1e9 if k3 > 0 else None
-        sm = [c["sm_mhz"] for c in clocks if c.get("sm_mhz")]
-        reasons = sorted({r for c in clocks for r in c.get("reasons", [])})
-        r = dict(
-            value=value, ms=ms_max, workload=wl, fp16_bytes=fp16 * pairs, wire_bytes=wire * pairs,
-            launches=int(g[:, 6].sum()),  # kvx kernels launched in the timed region
-            clocks={"sm_mhz": min(sm) if sm else None,
-                    "sm_max_mhz": max((c.get("sm_max_mhz") or 0) for c in clocks) or None,
-                    "reasons": reasons, "per_rank_median_sm_mhz": sm},
-            e2e=None if (args.no_e2e or kivi) else {
-                "value": round(pairs * fp16 / (float(g[:, 3].max()) * 1e-3) / 1e9, 3),
-                "unit": "GB/s", "h2d_bytes_per_step": int(g[:, 4].sum()),
-                "d2h_bytes_per_step": int(g[:, 5].sum()),
-                "ms_per_step": round(float(g[:, 3].max()), 3),
-                "path": "pinned host KV -(H2D)-> K1 on P -(NVLink)-> K3 on D -(D2H)-> pinned "
-                        "host paged cache, per layer chunk"},
-            cpu=None,
-            roofline={"bound": "nvlink", "kernel": "pull_dequant_scatter_paged (TMA bulk pull "
-                      "over NVLink)" if mode == "pull" else f"hand-off ({mode})",
-                      "achieved": round(link_gbs, 1), "peak": B.NVLINK_GBS,
-                      "peak_kind": "measured peer copy, B200_PROFILING.md (900 nominal)",
-                      "unit": "GB/s", "frac": round(link_gbs / B.NVLINK_GBS, 4), "traffic": None,
-                      "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
-                      "k3_link_gbs": round(k3_link, 1) if k3_link else None,
-                      "frac_of_nominal_900": round(link_gbs / 900.0, 4),
-                      "hbm_peak": hbm},
-            calibration=_calibration(spec, T, ms_max, float(g[:, 7].max())) if (
-                trace is None and not kivi) else None,
-            extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
-                   "format": spec.format,
-                   "cuda_graphs": bool(ch.graphs),
-                   "verified_sampled_rows_bit_exact": verified,
-                   **({"trace_batches_timed": tok[args.warmup:args.warmup + args.steps],
-                       "trace": "lengths log-uniform [128, 8192], 1-16 req/batch, <=16384 "
-                                "tokens/batch, rng(0)"} if trace is not None else {}),
-                   "pairing": pairing(world), "parallelism": f"{pairs}P{pairs}D"},
-        )
-        emit(args, r, world)
-    dist.barrier()
-    ch.close()
-    dist.destroy_process_group()
