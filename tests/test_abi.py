@@ -102,6 +102,8 @@ def test_no_cpu_fallback(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(ImportError):
         _lib.load(str(tmp_path / "missing.so"))
-    import paper_2502_09334_b200.datapath as dp
-    src = open(dp.__file__).read()
-    assert "oracle" not in src.replace("no CPU path", "")
+    import glob
+    pkg = os.path.join(ROOT, "paper_2502_09334_b200")
+    for f in glob.glob(os.path.join(pkg, "*.py")):
+        src = open(f).read()
+        assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), f
