@@ -131,13 +131,18 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
  * kvx_stream_signal).  Without flags, shapes whose rows are not 16-byte
  * multiples fall back to the per-lane kernel; with flags they return
  * KVX_ERR_UNSUPPORTED (see kvx_pull_supported).
+ * done_counter / peer_free_flag (nullable, together): in-kernel completion --
+ * the last CTA resets ready_flags[0..n_ready) to 0, zeroes *done_counter (a
+ * u32 on this GPU, 0 before the first call) and sets *peer_free_flag = 1
+ * (a peer/IPC-mapped u32 on the prefill GPU: "queue half consumed").
  */
 int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
                                    int64_t payload_layer_stride, const int64_t* dst_slots,
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
                                    int64_t dst_layer_stride, const void* ready_flags,
-                                   uint32_t epoch, int layers_per_chunk, void* stream);
+                                   uint32_t epoch, int layers_per_chunk, void* done_counter,
+                                   void* peer_free_flag, int n_ready, void* stream);
 
 /* 1 if kvx_pull_dequant_scatter_paged can bulk-stage this shape. */
 int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, int bits);

@@ -180,14 +180,23 @@ constexpr int kBulkStages = KVX_BULK_STAGES;
 constexpr int kBulkThreads = 288;
 constexpr int kBulkStageTarget = KVX_BULK_STAGE_BYTES;  // code bytes per stage
 
+struct PullDone {  // optional in-kernel completion of a pull hand-off
+  uint32_t* done_counter = nullptr;
+  uint32_t* peer_free = nullptr;
+  int n_ready = 0;
+};
+
 template <int BITS, int G>
 cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale, const void* zero,
                         cudaStream_t s, bool* ok, const uint32_t* ready, uint32_t epoch,
-                        int layers_per_chunk) {
+                        int layers_per_chunk, const PullDone& done = PullDone()) {
   *ok = false;
   kvx::BulkGeo bg;
   bg.ready = ready;
   bg.epoch = epoch;
+  bg.done_counter = done.done_counter;
+  bg.peer_free = done.peer_free;
+  bg.n_ready = done.n_ready;
   bg.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
   bg.code_row_bytes = int(int64_t(g.row_elems) * BITS / 8);
   bg.meta_row_bytes = int(int64_t(g.row_elems) / G * 2);
@@ -239,11 +248,11 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
 template <int BITS>
 cudaError_t dispatch_pull(int group, const kvx::Geo& g, const void* c, const void* sc,
                           const void* z, cudaStream_t s, bool* ok, const uint32_t* ready,
-                          uint32_t epoch, int lpc) {
+                          uint32_t epoch, int lpc, const PullDone& done) {
   switch (group) {
-    case 32: return launch_pull<BITS, 32>(g, c, sc, z, s, ok, ready, epoch, lpc);
-    case 64: return launch_pull<BITS, 64>(g, c, sc, z, s, ok, ready, epoch, lpc);
-    default: return launch_pull<BITS, 128>(g, c, sc, z, s, ok, ready, epoch, lpc);
+    case 32: return launch_pull<BITS, 32>(g, c, sc, z, s, ok, ready, epoch, lpc, done);
+    case 64: return launch_pull<BITS, 64>(g, c, sc, z, s, ok, ready, epoch, lpc, done);
+    default: return launch_pull<BITS, 128>(g, c, sc, z, s, ok, ready, epoch, lpc, done);
   }
 }
 
@@ -457,7 +466,8 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
                                    int64_t dst_layer_stride, const void* ready_flags,
-                                   uint32_t epoch, int layers_per_chunk, void* stream) {
+                                   uint32_t epoch, int layers_per_chunk, void* done_counter,
+                                   void* peer_free_flag, int n_ready, void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
   kvx::Geo g;
@@ -466,6 +476,14 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
   if (rc) return rc;
   if (g.n_token_rows == 0) return KVX_OK;
   if (ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) return KVX_ERR_INVALID_ARG;
+  if ((done_counter != nullptr) != (peer_free_flag != nullptr) ||
+      (done_counter && (!ready_flags || n_ready < 0 || !aligned(done_counter, 4) ||
+                        !aligned(peer_free_flag, 4))))
+    return KVX_ERR_INVALID_ARG;
+  PullDone done;
+  done.done_counter = static_cast<uint32_t*>(done_counter);
+  done.peer_free = static_cast<uint32_t*>(peer_free_flag);
+  done.n_ready = n_ready;
   if (bits != 16 && codes && scale && zero && k_cache && aligned(k_cache, 32) &&
       aligned(v_cache, 32) && (dst_layer_stride * 2) % 32 == 0) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -473,16 +491,16 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
     bool ok = false;
     cudaError_t e;
     switch (bits) {
-      case 2: e = dispatch_pull<2>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk); break;
-      case 8: e = dispatch_pull<8>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk); break;
-      default: e = dispatch_pull<4>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk); break;
+      case 2: e = dispatch_pull<2>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk, done); break;
+      case 8: e = dispatch_pull<8>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk, done); break;
+      default: e = dispatch_pull<4>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk, done); break;
     }
     if (e != cudaSuccess) return e;
     if (ok) return KVX_OK;
   }
   // shapes the bulk path cannot stage (16-bit, unaligned rows): per-lane loads,
   // which cannot wait in-kernel -- callers pass ready_flags only for bulk shapes
-  if (ready_flags) return KVX_ERR_UNSUPPORTED;
+  if (ready_flags || done_counter) return KVX_ERR_UNSUPPORTED;
   return kvx_dequant_scatter_paged(codes, scale, zero, payload_layer_stride, dst_slots, n_layers,
                                    n_tokens, n_heads, head_dim, group, bits, k_cache, v_cache,
                                    dst_layer_stride, stream);

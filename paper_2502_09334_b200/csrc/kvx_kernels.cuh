@@ -642,6 +642,12 @@ __global__ void __launch_bounds__(256) scatter16_kernel(Geo g, const uint8_t* __
 struct BulkGeo {
   const uint32_t* ready; // per-chunk doorbells (nullable): wait ready[c] >= epoch
   uint32_t epoch;
+  // in-kernel completion (nullable): the last CTA to finish resets the n_ready
+  // doorbells to 0 and sets *peer_free = 1 on the prefill GPU (queue half
+  // consumed) -- no memset / stream-memop nodes after the kernel
+  uint32_t* done_counter;
+  uint32_t* peer_free;
+  int n_ready;
   int layers_per_chunk;
   int rows_per_span;     // R
   int spans_per_layer;   // ceil(2T / R)
@@ -750,9 +756,7 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
                  &full[st]);
       }
     }
-    return;
-  }
-
+  } else {
   // ---- consumers
   uint32_t k = 0;
   for (uint32_t sp = blockIdx.x; sp < bg.n_spans; sp += gridDim.x, ++k) {
@@ -800,6 +804,21 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  }  // consumers
+
+  if (bg.done_counter) {
+    __syncthreads();  // this CTA has consumed every span it owned
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(bg.done_counter, 1u) == gridDim.x - 1) {  // last CTA of the launch
+        uint32_t* rr = const_cast<uint32_t*>(bg.ready);
+        for (int c = 0; c < bg.n_ready; ++c) rr[c] = 0u;
+        *bg.done_counter = 0u;
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(bg.peer_free), "r"(1u) : "memory");
+      }
+    }
   }
 }
 

@@ -252,11 +252,13 @@ def quant_pack_layers(src: KVPlanes, packed: PackedKV, l0: int, l1: int, stream=
 
 
 def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
-                           stream=None, bulk: bool = False, ready: tuple | None = None) -> None:
+                           stream=None, bulk: bool = False, ready: tuple | None = None,
+                           done: tuple | None = None) -> None:
     """K3 on layers [l0, l1).  ``bulk``: TMA bulk-staged variant (for payloads
     read over NVLink).  ``ready=(flags_addr, epoch, layers_per_chunk)``: the
     bulk kernel waits in-kernel for each chunk's doorbell (one launch per
-    hand-off)."""
+    hand-off).  ``done=(counter_addr, peer_free_addr, n_ready)``: in-kernel
+    completion (reset the doorbells, free the prefill-side queue half)."""
     lay = packed.layout
     k, v = dst.ptrs(l0)
     c, s, z = packed.ptrs(l0)
@@ -264,8 +266,9 @@ def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
             lay.head_dim, lay.group, lay.bits, k, v, dst.layer_stride)
     if bulk or ready is not None:
         rf, epoch, lpc = ready if ready is not None else (None, 0, 1)
-        _lib.call("kvx_pull_dequant_scatter_paged", *args, rf, epoch & 0xFFFFFFFF, lpc,
-                  _stream_ptr(stream))
+        dc, pf, nr = done if done is not None else (None, None, 0)
+        _lib.call("kvx_pull_dequant_scatter_paged", *args, rf, epoch & 0xFFFFFFFF, lpc, dc, pf,
+                  nr, _stream_ptr(stream))
     else:
         _lib.call("kvx_dequant_scatter_paged", *args, _stream_ptr(stream))
 

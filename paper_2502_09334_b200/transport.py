@@ -237,6 +237,7 @@ class PairChannel:
         self.flags = IpcBuffer(FLAG_SLOTS * 4)
         self.graphs = bool(graphs) and mode in PULL_MODES
         self.counters = torch.zeros(PULL_MAX_CHUNKS, dtype=torch.int32, device=self.device)
+        self.done_counter = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._graphs, self._seen = {}, set()
         if mode in PULL_MODES:
             if len(self.chunks) > PULL_MAX_CHUNKS:
@@ -369,7 +370,9 @@ class PairChannel:
                 # threads wait in-kernel for each chunk's doorbell
                 ev = _kernel_events(timing, s, "k3")
                 dequant_scatter_layers(payload, dst, 0, lay.n_layers, s,
-                                       ready=(self._pready(self.flags.ptr, h, 0), 1, lpc))
+                                       ready=(self._pready(self.flags.ptr, h, 0), 1, lpc),
+                                       done=(self.done_counter.data_ptr(),
+                                             self._pfree(self.peer_flags, h), len(chunks)))
                 _kernel_events_end(ev, s)
             else:
                 for c, (l0, l1) in enumerate(chunks):
@@ -377,9 +380,10 @@ class PairChannel:
                     ev = _kernel_events(timing, s, "k3")
                     dequant_scatter_layers(payload, dst, l0, l1, s)
                     _kernel_events_end(ev, s)
-            _lib.call("kvx_memset_async", self._pready(self.flags.ptr, h, 0), 0,
-                      4 * len(chunks), _stream_ptr(s))
-            signal(self._pfree(self.peer_flags, h), 1, s)     # half consumed
+            if not bulk:  # (the bulk kernel resets the doorbells and frees the half itself)
+                _lib.call("kvx_memset_async", self._pready(self.flags.ptr, h, 0), 0,
+                          4 * len(chunks), _stream_ptr(s))
+                signal(self._pfree(self.peer_flags, h), 1, s)  # half consumed
             if stage_out is not None:
                 (dk, dv), (hk, hv) = stage_out
                 self.x_ready[0].record(s)
