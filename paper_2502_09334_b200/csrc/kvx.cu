@@ -147,6 +147,7 @@ cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero
     if (ipc <= 0 || ipc >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     sig.items_per_chunk = uint32_t(ipc);
     const int64_t n_chunks = (ig.n_items + ipc - 1) / ipc;
+    if (n_chunks > kvx::kMaxSignalChunks) return cudaErrorInvalidValue;
     e = cudaMemsetAsync(rq.counters, 0, size_t(n_chunks) * 4, s);
     if (e != cudaSuccess) return e;
   }

@@ -346,7 +346,7 @@ __device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)
 }
 
 #ifndef KVX_K1_MIN_BLOCKS
-#define KVX_K1_MIN_BLOCKS 1
+#define KVX_K1_MIN_BLOCKS 2  // keep 2 CTAs (16 warps) per SM: <= 128 registers
 #endif
 #ifndef KVX_K1_PF
 #define KVX_K1_PF 2  // items prefetched ahead per warp (A/B: profiles/r01_summary.md)
@@ -358,25 +358,56 @@ __device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)
 // ready flag).  Warps walk items in global order, so chunks complete
 // progressively while the kernel is still running: ONE launch feeds the
 // decode side layer by layer, no per-chunk launches or host round trips.
+constexpr int kMaxSignalChunks = 64;  // = transport.PULL_MAX_CHUNKS
+
 struct SignalGeo {
   uint32_t* counters;    // [n_chunks] arrivals (zeroed before the launch)
   uint32_t* peer_flags;  // [n_chunks] decode-side ready flags (IPC/peer mapped), or null
   uint32_t items_per_chunk;
 };
 
-__device__ __forceinline__ void chunk_arrive(const SignalGeo& sig, uint32_t c, uint32_t n_items,
-                                             uint32_t n_warps, int lane) {
+// Warps w in [lo, hi) that own at least one item i in [a, b) (item i -> warp i % W).
+__device__ __forceinline__ uint32_t warps_owning(uint32_t a, uint32_t b, uint32_t W, uint32_t lo,
+                                                 uint32_t hi) {
+  auto ov = [](uint32_t x0, uint32_t x1, uint32_t y0, uint32_t y1) -> uint32_t {
+    const uint32_t l = max(x0, y0), h = min(x1, y1);
+    return h > l ? h - l : 0u;
+  };
+  if (b - a >= W) return hi - lo;
+  const uint32_t w0 = a % W, w1 = (b - 1) % W;
+  if (w0 <= w1) return ov(w0, w1 + 1, lo, hi);
+  return ov(w0, W, lo, hi) + ov(0, w1 + 1, lo, hi);
+}
+
+// CTAs (8 warps each) owning at least one item of [a, b).
+__device__ __forceinline__ uint32_t ctas_owning(uint32_t a, uint32_t b, uint32_t W) {
+  if (b - a >= W) return W / 8;
+  const uint32_t w0 = a % W, w1 = (b - 1) % W;
+  if (w0 <= w1) return (w1 >> 3) - (w0 >> 3) + 1;
+  const uint32_t c0 = ((W - 1) >> 3) - (w0 >> 3) + 1, c1 = (w1 >> 3) + 1;
+  const uint32_t dup = (w1 >> 3) >= (w0 >> 3) ? (w1 >> 3) - (w0 >> 3) + 1 : 0u;
+  return c0 + c1 - dup;
+}
+
+// Two-level arrival: warps count in shared memory, the CTA's last warp adds
+// one to the global chunk counter, the last CTA rings the peer's doorbell
+// (a same-address global atomic per warp would serialise for small hand-offs).
+__device__ __forceinline__ void chunk_arrive(const SignalGeo& sig, uint32_t* cta_cnt, uint32_t c,
+                                             uint32_t n_items, uint32_t n_warps, int lane) {
   __threadfence();  // this lane's payload stores, device-wide
   __syncwarp();
   if (lane == 0) {
     const uint32_t a = c * sig.items_per_chunk;
     const uint32_t b = min(n_items, a + sig.items_per_chunk);
-    const uint32_t expected = min(n_warps, b - a);  // warps owning >= 1 item of the chunk
-    const uint32_t old = atomicAdd(sig.counters + c, 1u);
-    if (old + 1 == expected) {
-      __threadfence_system();
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags + c), "r"(1u)
-                   : "memory");
+    const uint32_t lo = blockIdx.x * (blockDim.x >> 5);
+    const uint32_t mine = warps_owning(a, b, n_warps, lo, lo + (blockDim.x >> 5));
+    if (atomicAdd_block(cta_cnt + c, 1u) + 1 == mine) {
+      __threadfence();
+      if (atomicAdd(sig.counters + c, 1u) + 1 == ctas_owning(a, b, n_warps)) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags + c), "r"(1u)
+                     : "memory");
+      }
     }
   }
 }
@@ -393,6 +424,11 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+  __shared__ uint32_t cta_cnt[kMaxSignalChunks];
+  if (sig.peer_flags) {
+    for (int i = threadIdx.x; i < kMaxSignalChunks; i += blockDim.x) cta_cnt[i] = 0u;
+    __syncthreads();
+  }
   uint32_t w[NB][16];
   K1Item it[NB];
 #pragma unroll
@@ -425,7 +461,7 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
         const uint32_t c = cur / sig.items_per_chunk;
         const uint32_t nxt = cur + n_warps;
         if (nxt >= ig.n_items || nxt / sig.items_per_chunk != c)
-          chunk_arrive(sig, c, ig.n_items, n_warps, lane);
+          chunk_arrive(sig, cta_cnt, c, ig.n_items, n_warps, lane);
       }
     }
   }
