@@ -463,10 +463,7 @@ class PairChannel:
         return self.graphs and timing is None and staging is None and key in self._graphs
 
     def _replay(self, key, s, cur):
-        s.wait_stream(cur)
-        with torch.cuda.stream(s):
-            self._graphs[key].replay()
-        cur.wait_stream(s)
+        self._graphs[key].replay()  # graph launches are ordered on the current stream
 
     def _run_or_capture(self, key, body, s, cur, capturable: bool):
         s.wait_stream(cur)
@@ -481,8 +478,9 @@ class PairChannel:
                 cur.wait_stream(s)
                 return
             self._graphs[key] = g
-            with torch.cuda.stream(s):
-                g.replay()
+            cur.wait_stream(s)
+            g.replay()
+            return
         else:
             body()
             if capturable:
@@ -512,6 +510,15 @@ class PairChannel:
         each layer chunk from pinned host memory first (the host-buffer e2e
         path; H2D of chunk c+1 overlaps K1 of chunk c)."""
         assert self.role == "prefill"
+        if timing is None and stage_in is None and self._graphs:
+            # fast path: a captured hand-off of this size/half/buffers is ONE
+            # graph launch on the caller's stream (no extra stream syncs)
+            g = self._graphs.get(("send", n_tokens, (self.epoch + 1) & 1, src.k.data_ptr(),
+                                  src.slots_ptr))
+            if g is not None:
+                self.epoch += 1
+                g.replay()
+                return
         if self.spec.format == "kivi":
             self.epoch += 1
             return self._send_kivi(src, n_tokens, seqlens, self.epoch)
@@ -580,6 +587,13 @@ class PairChannel:
         download each finished layer chunk of the cache to pinned host memory
         (D2H of chunk c overlaps K3 of chunk c+1)."""
         assert self.role == "decode"
+        if timing is None and stage_out is None and self._graphs:
+            g = self._graphs.get(("recv", n_tokens, (self.epoch + 1) & 1, dst.slots_ptr,
+                                  dst.k.data_ptr()))
+            if g is not None:
+                self.epoch += 1
+                g.replay()
+                return
         if self.spec.format == "kivi":
             self.epoch += 1
             return self._recv_kivi(dst, n_tokens, seqlens, self.epoch)
