@@ -85,11 +85,14 @@ int kvx_device_count(int* count);
  * writes the dense packed payload.  codes/scale/zero may be peer pointers
  * (fused NVLink push).  bits in {2,4,8} (16 = passthrough copy, scale/zero
  * ignored); group in {32,64,128} dividing head_dim; head_dim % 8 == 0.
+ * Head window (TP head shards): the source planes' token rows
+ * hold plane_heads heads (0 = n_heads); only heads [head_offset,
+ * head_offset + n_heads) are packed.  The payload rows then hold n_heads.
  */
 int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_stride,
                    const int64_t* src_slots, int64_t n_layers, int64_t n_tokens, int n_heads,
                    int head_dim, int group, int bits, void* codes, void* scale, void* zero,
-                   int64_t payload_layer_stride, void* stream);
+                   int64_t payload_layer_stride, int plane_heads, int head_offset, void* stream);
 
 /*
  * K1 with device-side doorbells (fused quantise -> NVLink pull pipeline):
@@ -103,21 +106,25 @@ int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_laye
                           const int64_t* src_slots, int64_t n_layers, int64_t n_tokens,
                           int n_heads, int head_dim, int group, int bits, void* codes,
                           void* scale, void* zero, int64_t payload_layer_stride,
-                          void* counters, void* peer_ready_flags, int layers_per_chunk,
-                          void* stream);
+                          int plane_heads, int head_offset, void* counters,
+                          void* peer_ready_flags, int layers_per_chunk, void* stream);
 
 /*
  * K3: unpack + dequantise + scatter into the decode side's paged KV cache.
  * Replaces the ready = prefill_done + kv_delay step (simulate.py:235) with the
  * real decode-side enrolment.  codes/scale/zero may be peer pointers (fused
  * NVLink pull).  dst_slots[t] < 0 skips token t.  block_size is implied by the
- * slot values (pos = block*block_size + offset).
+ * slot values (pos = block*block_size + offset).  Head window as in
+ * kvx_quant_pack: the cache's token rows hold plane_heads heads and this
+ * payload's n_heads land at head_offset (a decode TP rank receiving part of
+ * its heads from each of several prefill ranks).
  */
 int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
                               int64_t payload_layer_stride, const int64_t* dst_slots,
                               int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                               int group, int bits, void* k_cache, void* v_cache,
-                              int64_t dst_layer_stride, void* stream);
+                              int64_t dst_layer_stride, int plane_heads, int head_offset,
+                              void* stream);
 
 /*
  * K3 with TMA bulk staging: same contract as kvx_dequant_scatter_paged, but
@@ -140,9 +147,10 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
                                    int64_t payload_layer_stride, const int64_t* dst_slots,
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
-                                   int64_t dst_layer_stride, const void* ready_flags,
-                                   uint32_t epoch, int layers_per_chunk, void* done_counter,
-                                   void* peer_free_flag, int n_ready, void* stream);
+                                   int64_t dst_layer_stride, int plane_heads, int head_offset,
+                                   const void* ready_flags, uint32_t epoch, int layers_per_chunk,
+                                   void* done_counter, void* peer_free_flag, int n_ready,
+                                   void* stream);
 
 /* 1 if kvx_pull_dequant_scatter_paged can bulk-stage this shape. */
 int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, int bits);

@@ -31,13 +31,13 @@ SIGNATURES = {
     "kvx_version": [],
     "kvx_strerror": [_I],
     "kvx_device_count": [ctypes.POINTER(_I)],
-    "kvx_quant_pack": [_P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _I64, _P],
+    "kvx_quant_pack": [_P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _I64, _I, _I, _P],
     "kvx_quant_pack_signal": [_P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _I64,
-                              _P, _P, _I, _P],
+                              _I, _I, _P, _P, _I, _P],
     "kvx_dequant_scatter_paged": [_P, _P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _I64,
-                                  _P],
+                                  _I, _I, _P],
     "kvx_pull_dequant_scatter_paged": [_P, _P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P,
-                                       _I64, _P, _U32, _I, _P, _P, _I, _P],
+                                       _I64, _I, _I, _P, _U32, _I, _P, _P, _I, _P],
     "kvx_pull_supported": [_I64, _I, _I, _I, _I],
     "kvx_quant_pack_kivi": [_P, _P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _I64, _P,
                             _I64, _P, _P],

@@ -64,8 +64,17 @@ int valid_format(int head_dim, int group, int bits) {
 
 int make_geo(kvx::Geo& g, const void* k, const void* v, int64_t layer_stride, const int64_t* slots,
              int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim, int group, int bits,
-             int64_t payload_layer_stride, int planes = 2, int plane0 = 0) {
+             int64_t payload_layer_stride, int planes = 2, int plane0 = 0, int plane_heads = 0,
+             int head_offset = 0) {
   if (n_layers < 0 || n_tokens < 0 || n_heads <= 0) return KVX_ERR_INVALID_ARG;
+  if (plane_heads == 0) plane_heads = n_heads;
+  if (head_offset < 0 || head_offset + n_heads > plane_heads) return KVX_ERR_INVALID_ARG;
+  g.plane_row_b = int64_t(plane_heads) * head_dim * 2;
+  g.head_off_b = int64_t(head_offset) * head_dim * 2;
+  if (g.head_off_b % 32 || g.plane_row_b % 32) {
+    if (n_layers > 0 && n_tokens > 0 && (g.head_off_b % 16 || g.plane_row_b % 16))
+      return KVX_ERR_INVALID_ARG;
+  }
   const int64_t row_elems = int64_t(n_heads) * head_dim;
   if (row_elems > (int64_t(1) << 30)) return KVX_ERR_INVALID_ARG;
   if (n_layers > 0 && n_tokens > 0) {
@@ -372,12 +381,12 @@ int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t*
 int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_stride,
                    const int64_t* src_slots, int64_t n_layers, int64_t n_tokens, int n_heads,
                    int head_dim, int group, int bits, void* codes, void* scale, void* zero,
-                   int64_t payload_layer_stride, void* stream) {
+                   int64_t payload_layer_stride, int plane_heads, int head_offset, void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
   kvx::Geo g;
   rc = make_geo(g, k_src, v_src, src_layer_stride, src_slots, n_layers, n_tokens, n_heads, head_dim,
-                group, bits, payload_layer_stride);
+                group, bits, payload_layer_stride, 2, 0, plane_heads, head_offset);
   if (rc) return rc;
   if (g.n_token_rows == 0) return KVX_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -390,7 +399,8 @@ int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_strid
   if (!codes || !scale || !zero || !aligned(codes, 8 * bits) || !aligned(scale, 2) ||
       !aligned(zero, 2))
     return KVX_ERR_INVALID_ARG;
-  if (k_src && (!aligned(k_src, 32) || !aligned(v_src, 32) || (src_layer_stride * 2) % 32))
+  if (k_src && (!aligned(k_src, 32) || !aligned(v_src, 32) || (src_layer_stride * 2) % 32 ||
+                g.plane_row_b % 32 || g.head_off_b % 32))
     return KVX_ERR_INVALID_ARG;  // 256-bit loads
   switch (bits) {
     case 2: return dispatch_quant<2>(group, g, codes, scale, zero, s);
@@ -403,8 +413,8 @@ int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_laye
                           const int64_t* src_slots, int64_t n_layers, int64_t n_tokens,
                           int n_heads, int head_dim, int group, int bits, void* codes,
                           void* scale, void* zero, int64_t payload_layer_stride,
-                          void* counters, void* peer_ready_flags, int layers_per_chunk,
-                          void* stream) {
+                          int plane_heads, int head_offset, void* counters,
+                          void* peer_ready_flags, int layers_per_chunk, void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
   if (bits == 16 || !counters || !peer_ready_flags || layers_per_chunk < 1 ||
@@ -412,11 +422,12 @@ int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_laye
     return KVX_ERR_INVALID_ARG;
   kvx::Geo g;
   rc = make_geo(g, k_src, v_src, src_layer_stride, src_slots, n_layers, n_tokens, n_heads, head_dim,
-                group, bits, payload_layer_stride);
+                group, bits, payload_layer_stride, 2, 0, plane_heads, head_offset);
   if (rc) return rc;
   if (g.n_token_rows == 0) return KVX_OK;
   if (!codes || !scale || !zero || !aligned(codes, 8 * bits) || !aligned(scale, 2) ||
-      !aligned(zero, 2) || !aligned(k_src, 32) || !aligned(v_src, 32) || (src_layer_stride * 2) % 32)
+      !aligned(zero, 2) || !aligned(k_src, 32) || !aligned(v_src, 32) || (src_layer_stride * 2) % 32 ||
+      g.plane_row_b % 32 || g.head_off_b % 32)
     return KVX_ERR_INVALID_ARG;
   SignalReq rq;
   rq.counters = static_cast<uint32_t*>(counters);
@@ -435,12 +446,13 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
                               int64_t payload_layer_stride, const int64_t* dst_slots,
                               int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                               int group, int bits, void* k_cache, void* v_cache,
-                              int64_t dst_layer_stride, void* stream) {
+                              int64_t dst_layer_stride, int plane_heads, int head_offset,
+                              void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
   kvx::Geo g;
   rc = make_geo(g, k_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
-                head_dim, group, bits, payload_layer_stride);
+                head_dim, group, bits, payload_layer_stride, 2, 0, plane_heads, head_offset);
   if (rc) return rc;
   if (g.n_token_rows == 0) return KVX_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -453,7 +465,8 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
   if (!codes || !scale || !zero || !aligned(codes, 8 * bits) || !aligned(scale, 2) ||
       !aligned(zero, 2))
     return KVX_ERR_INVALID_ARG;
-  if (k_cache && (!aligned(k_cache, 32) || !aligned(v_cache, 32) || (dst_layer_stride * 2) % 32))
+  if (k_cache && (!aligned(k_cache, 32) || !aligned(v_cache, 32) || (dst_layer_stride * 2) % 32 ||
+                  g.plane_row_b % 32 || g.head_off_b % 32))
     return KVX_ERR_INVALID_ARG;  // 256-bit stores
   switch (bits) {
     case 2: return dispatch_dequant<2>(group, g, codes, scale, zero, s);
@@ -466,14 +479,15 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
                                    int64_t payload_layer_stride, const int64_t* dst_slots,
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
-                                   int64_t dst_layer_stride, const void* ready_flags,
-                                   uint32_t epoch, int layers_per_chunk, void* done_counter,
-                                   void* peer_free_flag, int n_ready, void* stream) {
+                                   int64_t dst_layer_stride, int plane_heads, int head_offset,
+                                   const void* ready_flags, uint32_t epoch, int layers_per_chunk,
+                                   void* done_counter, void* peer_free_flag, int n_ready,
+                                   void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
   kvx::Geo g;
   rc = make_geo(g, k_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
-                head_dim, group, bits, payload_layer_stride);
+                head_dim, group, bits, payload_layer_stride, 2, 0, plane_heads, head_offset);
   if (rc) return rc;
   if (g.n_token_rows == 0) return KVX_OK;
   if (ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) return KVX_ERR_INVALID_ARG;
@@ -486,7 +500,8 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
   done.peer_free = static_cast<uint32_t*>(peer_free_flag);
   done.n_ready = n_ready;
   if (bits != 16 && codes && scale && zero && k_cache && aligned(k_cache, 32) &&
-      aligned(v_cache, 32) && (dst_layer_stride * 2) % 32 == 0) {
+      aligned(v_cache, 32) && (dst_layer_stride * 2) % 32 == 0 && g.plane_row_b % 32 == 0 &&
+      g.head_off_b % 32 == 0) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint32_t* rf = static_cast<const uint32_t*>(ready_flags);
     bool ok = false;
@@ -504,7 +519,7 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
   if (ready_flags || done_counter) return KVX_ERR_UNSUPPORTED;
   return kvx_dequant_scatter_paged(codes, scale, zero, payload_layer_stride, dst_slots, n_layers,
                                    n_tokens, n_heads, head_dim, group, bits, k_cache, v_cache,
-                                   dst_layer_stride, stream);
+                                   dst_layer_stride, plane_heads, head_offset, stream);
 }
 
 int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, int bits) {

@@ -129,7 +129,15 @@ struct Geo {
   int vecs;                // row_elems / 8
   int planes;              // planes per layer in this launch: 2 (K and V) or 1
   int plane0;              // first plane: 0 = K, 1 = V (planes == 1: which one)
+  int64_t plane_row_b;     // bytes per token row on the paged side (all its heads)
+  int64_t head_off_b;      // byte offset of this launch's head window in that row
 };
+
+// Token row `pos` of a plane, at this launch's head window (TP head shards:
+// a prefill rank packs, or a decode rank scatters, a sub-range of heads).
+__device__ __forceinline__ const char* row_ptr(const Geo& g, const char* plane, int64_t pos) {
+  return plane + pos * g.plane_row_b + g.head_off_b;
+}
 
 __device__ __forceinline__ const char* plane_ptr(const Geo& g, int kv, int64_t layer) {
   return (kv ? g.v_plane : g.k_plane) + layer * g.layer_stride_b;
@@ -285,7 +293,7 @@ __device__ __forceinline__ K1Item k1_item(const Geo& g, const ItemGeo& ig, uint3
   const int64_t pos = pos_of(g, t);
   const char* plane = plane_ptr(g, kv, layer);
   it.active = c < ig.cpr;
-  it.src = plane + pos * int64_t(g.row_elems) * 2 + int64_t(c) * 64;
+  it.src = row_ptr(g, plane, pos) + int64_t(c) * 64;
   it.codes = reinterpret_cast<char*>(codes) + int64_t(layer) * g.codes_ls +
              (int64_t(lrow) * ig.cpr + c) * CB;
   const int64_t gi = (int64_t(lrow) * ig.cpr + c) * 32 / G;
@@ -479,7 +487,7 @@ __global__ void __launch_bounds__(256) pack16_kernel(Geo g, uint8_t* __restrict_
     split_tr(g, tr, kv, t, layer, lrow);
     const int64_t pos = pos_of(g, t);
     const char* plane = plane_ptr(g, kv, layer);
-    const U4* src = reinterpret_cast<const U4*>(plane + pos * int64_t(g.row_elems) * 2);
+    const U4* src = reinterpret_cast<const U4*>(row_ptr(g, plane, pos));
     U4* dst = reinterpret_cast<U4*>(out + layer * g.codes_ls) + lrow * g.vecs;
     for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
       U4 v[UNROLL];
@@ -529,7 +537,7 @@ __device__ __forceinline__ K3Item k3_item(const Geo& g, const ItemGeo& ig, uint3
   const int64_t pos = pos_of(g, t);
   char* plane = const_cast<char*>(plane_ptr(g, kv, layer));
   it.active = (c < ig.cpr) && (pos >= 0);  // pos < 0: padding token, skipped
-  it.dst = plane + pos * int64_t(g.row_elems) * 2 + int64_t(c) * 64;
+  it.dst = const_cast<char*>(row_ptr(g, plane, pos)) + int64_t(c) * 64;
   it.codes = reinterpret_cast<const char*>(codes) + int64_t(layer) * g.codes_ls +
              (int64_t(lrow) * ig.cpr + c) * CB;
   const int64_t gi = (int64_t(lrow) * ig.cpr + c) * 32 / G;
@@ -644,7 +652,7 @@ __global__ void __launch_bounds__(256) scatter16_kernel(Geo g, const uint8_t* __
     const int64_t pos = pos_of(g, t);
     if (pos < 0) continue;
     char* plane = const_cast<char*>(plane_ptr(g, kv, layer));
-    U4* dst = reinterpret_cast<U4*>(plane + pos * int64_t(g.row_elems) * 2);
+    U4* dst = reinterpret_cast<U4*>(const_cast<char*>(row_ptr(g, plane, pos)));
     const U4* src = reinterpret_cast<const U4*>(in + layer * g.codes_ls) + lrow * g.vecs;
     for (int base = 0; base < g.vecs; base += 32 * UNROLL) {
       U4 v[UNROLL];
@@ -811,7 +819,7 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
       const int64_t t = lrow - p * g.n_tokens;
       const int64_t pos = pos_of(g, t);
       if (pos < 0) continue;  // padding token
-      char* dst = const_cast<char*>(plane_ptr(g, kv, layer)) + pos * int64_t(g.row_elems) * 2;
+      char* dst = const_cast<char*>(row_ptr(g, plane_ptr(g, kv, layer), pos));
       const uint8_t* crow = buf + r * bg.code_row_bytes;
       const int gpr = bg.meta_row_bytes / 2;
       for (int c = lane; c < bg.cpr; c += 32) {

@@ -196,6 +196,22 @@ class KVPlanes:
     n_heads: int
     head_dim: int
     slots: torch.Tensor | None = None
+    plane_heads: int = 0    # heads per token row of the planes (0 = n_heads)
+    head_offset: int = 0    # first head of this window
+
+    def window(self, head_offset: int, n_heads: int) -> "KVPlanes":
+        """The same planes restricted to heads [head_offset, head_offset + n_heads)
+        (a TP head shard: packed by a prefill rank or filled by a decode rank)."""
+        full = self.plane_heads or self.n_heads
+        h0 = self.head_offset + head_offset
+        if head_offset < 0 or n_heads < 1 or h0 + n_heads > full:
+            raise ValueError("head window outside the planes")
+        return KVPlanes(self.k, self.v, self.layer_stride, self.n_layers, n_heads,
+                        self.head_dim, self.slots, full, h0)
+
+    @property
+    def window_args(self):
+        return (self.plane_heads or self.n_heads, self.head_offset)
 
     @staticmethod
     def dense(kv: torch.Tensor) -> "KVPlanes":
@@ -248,7 +264,7 @@ def quant_pack_layers(src: KVPlanes, packed: PackedKV, l0: int, l1: int, stream=
     c, s, z = packed.ptrs(l0)
     _lib.call("kvx_quant_pack", k, v, src.layer_stride, src.slots_ptr, l1 - l0, lay.n_tokens,
               lay.n_heads, lay.head_dim, lay.group, lay.bits, c, s, z, lay.layer_stride,
-              _stream_ptr(stream))
+              *src.window_args, _stream_ptr(stream))
 
 
 def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
@@ -263,7 +279,7 @@ def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
     k, v = dst.ptrs(l0)
     c, s, z = packed.ptrs(l0)
     args = (c, s, z, lay.layer_stride, dst.slots_ptr, l1 - l0, lay.n_tokens, lay.n_heads,
-            lay.head_dim, lay.group, lay.bits, k, v, dst.layer_stride)
+            lay.head_dim, lay.group, lay.bits, k, v, dst.layer_stride, *dst.window_args)
     if bulk or ready is not None:
         rf, epoch, lpc = ready if ready is not None else (None, 0, 1)
         dc, pf, nr = done if done is not None else (None, None, 0)

@@ -329,7 +329,8 @@ class PairChannel:
                 c0, sc0, z0 = payload.ptrs(0)
                 _lib.call("kvx_quant_pack_signal", k, v, src.layer_stride, src.slots_ptr,
                           lay.n_layers, lay.n_tokens, lay.n_heads, lay.head_dim, lay.group,
-                          lay.bits, c0, sc0, z0, lay.layer_stride, self.counters.data_ptr(),
+                          lay.bits, c0, sc0, z0, lay.layer_stride, *src.window_args,
+                          self.counters.data_ptr(),
                           self._pready(self.peer_flags, h, 0), lpc, _stream_ptr(s))
                 _kernel_events_end(ev, s)
                 return

@@ -68,25 +68,32 @@ def test_packed_sizes(lib):
 @pytest.mark.parametrize("bits,group,head_dim", [(5, 128, 128), (4, 96, 128), (4, 128, 64),
                                                  (4, 64, 100), (3, 32, 128)])
 def test_invalid_format_rejected_before_cuda(lib, bits, group, head_dim):
-    rc = lib.kvx_quant_pack(16, 16, 0, None, 1, 1, 1, head_dim, group, bits, 16, 16, 16, 0, None)
+    rc = lib.kvx_quant_pack(16, 16, 0, None, 1, 1, 1, head_dim, group, bits, 16, 16, 16, 0, 0, 0,
+                            None)
     assert rc == _lib.KVX_ERR_INVALID_ARG
     rc = lib.kvx_dequant_scatter_paged(16, 16, 16, 0, None, 1, 1, 1, head_dim, group, bits, 16, 16,
-                                       0, None)
+                                       0, 0, 0, None)
     assert rc == _lib.KVX_ERR_INVALID_ARG
     with pytest.raises(ValueError):
         _lib.check(rc)
 
 
 def test_misaligned_pointers_rejected(lib):
-    rc = lib.kvx_quant_pack(8, 16, 0, None, 1, 1, 1, 128, 128, 4, 16, 16, 16, 0, None)
+    rc = lib.kvx_quant_pack(8, 16, 0, None, 1, 1, 1, 128, 128, 4, 16, 16, 16, 0, 0, 0, None)
+    assert rc == _lib.KVX_ERR_INVALID_ARG
+
+
+def test_head_window_out_of_range_rejected(lib):
+    # window [3, 3+2) does not fit 4 heads per row
+    rc = lib.kvx_quant_pack(256, 256, 0, None, 1, 1, 2, 128, 128, 4, 256, 256, 256, 0, 4, 3, None)
     assert rc == _lib.KVX_ERR_INVALID_ARG
 
 
 def test_empty_is_a_noop(lib):
     assert lib.kvx_quant_pack(None, None, 0, None, 0, 0, 1, 128, 128, 4, None, None, None, 0,
-                              None) == 0
+                              0, 0, None) == 0
     assert lib.kvx_dequant_scatter_paged(None, None, None, 0, None, 4, 0, 8, 128, 128, 4, None,
-                                         None, 0, None) == 0
+                                         None, 0, 0, 0, None) == 0
 
 
 def test_no_gpu_reports_zero_devices(lib):

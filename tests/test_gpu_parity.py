@@ -195,3 +195,34 @@ def test_invalid_args_raise(cuda):
         compress(kv, 4, 96)
     with pytest.raises(ValueError):
         compress(kv.float(), 4)
+
+
+@pytest.mark.parametrize("bulk", [False, True])
+@pytest.mark.parametrize("bits", [4, 8])
+def test_head_windows(cuda, bits, bulk):
+    """TP head shards: pack heads [2, 5) of an 8-head source, scatter them to
+    heads [1, 4) of a 6-head cache (SURVEY 8(e) head-range remap)."""
+    from paper_2502_09334_b200.datapath import (KVPlanes, PackedLayout, alloc_packed,
+                                                dequant_scatter_layers, quant_pack_layers)
+    torch = cuda
+    L, T, H, D, bs = 3, 70, 8, 128, 16
+    kv = O.synthetic_kv(L, T, H, D, seed=11)
+    src = KVPlanes.dense(torch.from_numpy(kv).cuda()).window(2, 3)
+    lay = PackedLayout(L, T, 3, D, bits, 128)
+    p = alloc_packed(lay, "cuda")
+    quant_pack_layers(src, p, 0, L)
+    nb = (T + bs - 1) // bs + 1
+    slots = O.synthetic_slots(T, bs, nb, seed=11)
+    kc = torch.full((L, nb, bs, 6, D), -2.0, dtype=torch.float16, device="cuda")
+    vc = torch.full_like(kc, -2.0)
+    dst = KVPlanes.paged(kc, vc, torch.from_numpy(slots).cuda()).window(1, 3)
+    dequant_scatter_layers(p, dst, 0, L, bulk=bulk)
+    torch.cuda.synchronize()
+    sub = np.ascontiguousarray(kv[:, :, :, 2:5])
+    c, s, z = O.quant_pack(sub.reshape(-1, D), bits, 128)
+    assert np.array_equal(p.codes().cpu().numpy().reshape(c.shape), c)
+    rows = O.unpack_dequant(c, s, z, bits, 128, D).reshape(L, 2, T, 3, D)
+    okc = np.full((L, nb * bs, 6, D), -2.0, np.float16); ovc = okc.copy()
+    okc[:, slots, 1:4] = rows[:, 0]; ovc[:, slots, 1:4] = rows[:, 1]
+    assert np.array_equal(h16(kc.cpu().numpy().reshape(okc.shape)), h16(okc))
+    assert np.array_equal(h16(vc.cpu().numpy().reshape(ovc.shape)), h16(ovc))
