@@ -190,6 +190,17 @@ constexpr int kBulkStages = KVX_BULK_STAGES;
 constexpr int kBulkThreads = 288;
 constexpr int kBulkStageTarget = KVX_BULK_STAGE_BYTES;  // code bytes per stage
 
+// Smallest row count whose code and metadata bytes are both 16-byte multiples.
+int64_t bulk_row_multiple(int64_t code_row_bytes, int64_t meta_row_bytes) {
+  auto need = [](int64_t b) {
+    int64_t k = 1;
+    while ((k * b) % 16) k *= 2;
+    return k;
+  };
+  const int64_t a = need(code_row_bytes), b = need(meta_row_bytes);
+  return a > b ? a : b;  // powers of two: the max is the lcm
+}
+
 struct PullDone {  // optional in-kernel completion of a pull hand-off
   uint32_t* done_counter = nullptr;
   uint32_t* peer_free = nullptr;
@@ -211,12 +222,17 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   bg.code_row_bytes = int(int64_t(g.row_elems) * BITS / 8);
   bg.meta_row_bytes = int(int64_t(g.row_elems) / G * 2);
   bg.cpr = g.row_elems / 32;
-  if (bg.code_row_bytes % 16 || bg.meta_row_bytes % 16 || !aligned(codes, 16) ||
-      !aligned(scale, 16) || !aligned(zero, 16) || g.codes_ls % 16 || g.meta_ls % 16)
-    return cudaSuccess;  // not bulk-copyable: caller falls back to the LDG kernel
   const int64_t two_t = int64_t(g.planes) * g.n_tokens;
+  // every bulk copy (a span of R rows, or the layer's last partial span) must
+  // be a multiple of 16 bytes at a 16-byte aligned offset
+  const int64_t m = bulk_row_multiple(bg.code_row_bytes, bg.meta_row_bytes);
+  if ((two_t * bg.code_row_bytes) % 16 || (two_t * bg.meta_row_bytes) % 16 ||
+      !aligned(codes, 16) || !aligned(scale, 16) || !aligned(zero, 16) || g.codes_ls % 16 ||
+      g.meta_ls % 16)
+    return cudaSuccess;  // not bulk-copyable: caller falls back to the LDG kernel
   int64_t r = kBulkStageTarget / bg.code_row_bytes;
-  if (r < 1) r = 1;
+  r = r / m * m;
+  if (r < m) r = m;
   if (r > two_t) r = two_t;
   bg.rows_per_span = int(r);
   bg.stage_bytes = bg.rows_per_span * (bg.code_row_bytes + 2 * bg.meta_row_bytes);
@@ -525,7 +541,7 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
 int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, int bits) {
   if (valid_format(head_dim, group, bits) || bits == 16 || n_tokens < 1) return 0;
   const int64_t row = int64_t(n_heads) * head_dim;
-  return (row * bits / 8) % 16 == 0 && (row / group * 2) % 16 == 0;
+  return (2 * n_tokens * row * bits / 8) % 16 == 0 && (2 * n_tokens * (row / group) * 2) % 16 == 0;
 }
 
 // ---- "kivi" format: per-channel K groups + fp16 residual window, V per token --

@@ -212,10 +212,25 @@ class PairChannel:
     """
 
     def __init__(self, spec: ChannelSpec, rank: int, world: int, control_group=None,
-                 data_group=None, graphs: bool = True):
+                 data_group=None, graphs: bool = True, edge: tuple | None = None):
+        """``edge=(prefill_rank, decode_rank)`` overrides the default pairing
+        (TP regroups, see TPHandoff).  Construction is collective over the
+        control group: ranks outside the edge take part in the handle exchange
+        and get an inert channel (``role is None``)."""
         self.spec = spec
         self.rank, self.world = rank, world
-        self.role, self.pair, self.peer = role_of(rank, world)
+        if edge is None:
+            self.role, self.pair, self.peer = role_of(rank, world)
+        else:
+            p, d = edge
+            self.pair = p
+            self.role = "prefill" if rank == p else "decode" if rank == d else None
+            self.peer = d if rank == p else p
+            if self.role is None:
+                exchange(None, control_group)
+                self.graphs, self.flags, self.local_payload = False, None, None
+                self.peer_flags = self._peer_payload_map = 0
+                return
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.stream = torch.cuda.Stream(self.device)    # kernels
         self.cstream = torch.cuda.Stream(self.device)   # copy engine / NCCL
@@ -651,6 +666,8 @@ class PairChannel:
 
     def close(self):
         """Unmap the partner's buffers and free ours (call after a barrier)."""
+        if self.role is None:
+            return
         torch.cuda.synchronize(self.device)
         if self.peer_flags:
             _lib.call("kvx_ipc_close", self.peer_flags)
@@ -684,3 +701,51 @@ def _kernel_events_end(ev, stream):
 # ---------------------------------------------------------------------------
 # bench.py N > 1
 # ---------------------------------------------------------------------------
+
+
+class TPHandoff:
+    """Hand-off between TP-sharded replicas with possibly different TP degrees
+    (SURVEY.md 8(e)).  KV heads are split evenly by TP rank on both sides;
+    every (prefill rank, decode rank) pair whose head ranges overlap becomes
+    one point-to-point edge (a PairChannel over the overlap): the prefill rank
+    packs its head window, the decode rank pulls it and scatters it into its
+    own head window -- the head-range remap on the pull side, no collective.
+    Matched TP degrees reduce to one edge per rank pair.  Construct on every
+    rank of the control group (collective)."""
+
+    def __init__(self, n_layers: int, max_tokens: int, n_kv_heads: int, head_dim: int,
+                 prefill_ranks, decode_ranks, rank: int, world: int, control_group=None,
+                 bits: int = 4, group: int = DEFAULT_GROUP, n_chunks: int = 8,
+                 mode: str = "pull", graphs: bool = True):
+        tp_p, tp_d = len(prefill_ranks), len(decode_ranks)
+        if n_kv_heads % tp_p or n_kv_heads % tp_d:
+            raise ValueError("KV heads must split evenly over both TP groups")
+        hp, hd = n_kv_heads // tp_p, n_kv_heads // tp_d
+        self.rank = rank
+        self.edges = []  # (channel, src window offset, dst window offset, n heads)
+        for i, pr in enumerate(prefill_ranks):
+            for j, dr in enumerate(decode_ranks):
+                a, b = max(i * hp, j * hd), min((i + 1) * hp, (j + 1) * hd)
+                if a >= b:
+                    continue
+                spec = ChannelSpec(n_layers, max_tokens, b - a, head_dim, bits, group, n_chunks,
+                                   mode)
+                ch = PairChannel(spec, rank, world, control_group, graphs=graphs,
+                                 edge=(pr, dr))
+                self.edges.append((ch, a - i * hp, a - j * hd, b - a))
+
+    def send(self, src: KVPlanes, n_tokens: int) -> None:
+        """Prefill rank: ``src`` holds this rank's hp heads."""
+        for ch, so, _, n in self.edges:
+            if ch.role == "prefill":
+                ch.send(src.window(so, n), n_tokens)
+
+    def recv(self, dst: KVPlanes, n_tokens: int) -> None:
+        """Decode rank: ``dst`` is this rank's paged cache (hd heads per token row)."""
+        for ch, _, do, n in self.edges:
+            if ch.role == "decode":
+                ch.recv(dst.window(do, n), n_tokens)
+
+    def close(self) -> None:
+        for ch, *_ in self.edges:
+            ch.close()

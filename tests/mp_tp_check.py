@@ -1,0 +1,70 @@
+"""torchrun worker (4 ranks) for tests/test_gpu_multiproc.py::test_tp_regroup:
+TP-sharded replicas with mismatched TP degrees -- every
+decode rank's paged cache must equal the oracle on its own heads."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import kvq_oracle as O  # noqa: E402
+from paper_2502_09334_b200.datapath import KVPlanes  # noqa: E402
+from paper_2502_09334_b200.transport import TPHandoff  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    ctrl = dist.new_group(backend="gloo")
+    L, H, D, bs = 4, 8, 128, 16
+    failures = 0
+    scenarios = [([0], [1, 2]), ([0, 1], [2]), ([0, 1], [2, 3]), ([3], [0, 1, 2])]
+    for si, (pr, dr) in enumerate(scenarios):
+        for mode in ("pull", "pull_ldg"):
+            tp = TPHandoff(L, 256, H, D, pr, dr, rank, world, ctrl, n_chunks=2, mode=mode)
+            for epoch, T in enumerate((256, 100, 256)):
+                seed = 31 * si + epoch
+                kv_full = O.synthetic_kv(L, T, H, D, seed=seed)
+                if rank in pr:
+                    i = pr.index(rank)
+                    hp = H // len(pr)
+                    mine = np.ascontiguousarray(kv_full[:, :, :, i * hp:(i + 1) * hp])
+                    tp.send(KVPlanes.dense(torch.from_numpy(mine).to(dev)), T)
+                    torch.cuda.synchronize()
+                if rank in dr:
+                    j = dr.index(rank)
+                    hd = H // len(dr)
+                    nb = T // bs + 2
+                    slots = O.synthetic_slots(T, bs, nb, seed=seed)
+                    kc = torch.zeros((L, nb, bs, hd, D), dtype=torch.float16, device=dev)
+                    vc = torch.zeros_like(kc)
+                    tp.recv(KVPlanes.paged(kc, vc, torch.from_numpy(slots).to(dev)), T)
+                    torch.cuda.synchronize()
+                    sub = np.ascontiguousarray(kv_full[:, :, :, j * hd:(j + 1) * hd])
+                    c, s, z = O.quant_pack(sub.reshape(-1, D), 4, 128)
+                    rows = O.unpack_dequant(c, s, z, 4, 128, D).reshape(L, 2, T, hd, D)
+                    okc = np.zeros((L, nb, bs, hd, D), np.float16); ovc = okc.copy()
+                    O.scatter_paged(rows, slots, okc, ovc)
+                    if not (np.array_equal(kc.cpu().numpy().view(np.uint16), okc.view(np.uint16))
+                            and np.array_equal(vc.cpu().numpy().view(np.uint16), ovc.view(np.uint16))):
+                        failures += 1
+                        print(f"MISMATCH tp {pr}->{dr} mode={mode} rank={rank} T={T}", flush=True)
+            dist.barrier()
+            tp.close()
+    f = torch.tensor([failures], device=dev)
+    dist.all_reduce(f)
+    if rank == 0:
+        print(f"mp_tp_check failures={int(f.item())}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if f.item() else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -36,3 +36,15 @@ def test_fullsize_pairs(cuda, nproc):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "failures=0" in r.stdout and "bit-exact" in r.stdout
+
+
+def test_tp_regroup(cuda):
+    """Mismatched TP degrees (1->2, 2->1, 2->2, 1->3) via per-overlap edges."""
+    if cuda.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr=127.0.0.1", "--master-port=29535",
+           os.path.join(HERE, "mp_tp_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "failures=0" in r.stdout
