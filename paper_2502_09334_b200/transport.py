@@ -728,6 +728,8 @@ class TPHandoff:
                 a, b = max(i * hp, j * hd), min((i + 1) * hp, (j + 1) * hd)
                 if a >= b:
                     continue
+                if pr == dr:
+                    raise ValueError("a rank cannot hand heads to itself: use datapath.HandoffPlan")
                 spec = ChannelSpec(n_layers, max_tokens, b - a, head_dim, bits, group, n_chunks,
                                    mode)
                 ch = PairChannel(spec, rank, world, control_group, graphs=graphs,

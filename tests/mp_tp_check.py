@@ -25,7 +25,7 @@ def main():
     ctrl = dist.new_group(backend="gloo")
     L, H, D, bs = 4, 8, 128, 16
     failures = 0
-    scenarios = [([0], [1, 2]), ([0, 1], [2]), ([0, 1], [2, 3]), ([3], [0, 1, 2])]
+    scenarios = [([0], [1, 2]), ([0, 1], [2]), ([0, 1], [2, 3]), ([3], [0, 1]), ([1, 2, 3, 0], [0, 2])]
     for si, (pr, dr) in enumerate(scenarios):
         for mode in ("pull", "pull_ldg"):
             tp = TPHandoff(L, 256, H, D, pr, dr, rank, world, ctrl, n_chunks=2, mode=mode)

@@ -39,7 +39,7 @@ def test_fullsize_pairs(cuda, nproc):
 
 
 def test_tp_regroup(cuda):
-    """Mismatched TP degrees (1->2, 2->1, 2->2, 1->3) via per-overlap edges."""
+    """Mismatched TP degrees (1->2, 2->1, 2->2, 4->2 with shared ranks) via per-overlap edges."""
     if cuda.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
