@@ -354,7 +354,7 @@ def plan_chunks(args, L):
     return layer_chunks(L, args.chunks)
 
 
-def _calibration(spec, T, ms_large, ms_small, t_small=16):
+def _calibration(spec, T, ms_large, ms_small, t_small=16, host_us=None):
     """(alpha, beta) of t = alpha + V/beta with V the reference's modelled
     volume 2*b*s*h*bits/8*L (costs.py:102) -- what calibrate.cluster_dict and
     measured_kv_comm_cost consume."""
@@ -367,6 +367,7 @@ def _calibration(spec, T, ms_large, ms_small, t_small=16):
         return None
     return {"alpha_us": round(alpha * 1e6, 2), "beta_GBps_of_modelled_volume": round(beta / 1e9, 1),
             "small_handoff_us": round(ms_small * 1e3, 2), "small_tokens": t_small,
+            "host_enqueue_us_per_handoff": round(host_us, 2) if host_us is not None else None,
             "note": "t = alpha + (2*b*s*h*bits/8*L)/beta, per pair, CUDA-graph replayed"}
 
 
@@ -487,7 +488,7 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
     # alpha-beta calibration of this very channel (graph-replayed pull): a
     # 16-token hand-off against the main one -> kv_comm_cost's (alpha, beta)
     # for the reference's volume at this bit-width
-    cal_small_ms = 0.0
+    cal_small_ms, host_us = 0.0, 0.0
     if trace is None and not kivi:
         t_small = 16
         if ch.role == "prefill":
@@ -502,10 +503,12 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
         torch.cuda.synchronize()
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n_cal = 50
+        h0 = time.perf_counter()
         c0.record()
         for _ in range(n_cal):
             small()
         c1.record()
+        host_us = (time.perf_counter() - h0) / n_cal * 1e6  # enqueue cost per hand-off
         torch.cuda.synchronize()
         cal_small_ms = c0.elapsed_time(c1) / n_cal
         dist.barrier()
@@ -542,7 +545,7 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
         e2e_ms = e0.elapsed_time(e1) / n_e2e
         dist.barrier()
     stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0), e2e_ms, h2d, d2h,
-                          launches, cal_small_ms], dtype=torch.float64, device=dev)
+                          launches, cal_small_ms, host_us], dtype=torch.float64, device=dev)
     gathered = [torch.zeros_like(stats) for _ in range(world)]
     dist.all_gather(gathered, stats)
     clocks = exchange(clk.summary(), ctrl)
@@ -593,7 +596,8 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                       "k3_link_gbs": round(k3_link, 1) if k3_link else None,
                       "frac_of_nominal_900": round(link_gbs / 900.0, 4),
                       "hbm_peak": hbm},
-            calibration=_calibration(spec, T, ms_max, float(g[:, 7].max())) if (
+            calibration=_calibration(spec, T, ms_max, float(g[:, 7].max()),
+                                     host_us=float(g[:, 8].max())) if (
                 trace is None and not kivi) else None,
             extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
                    "format": spec.format,
