@@ -24,6 +24,7 @@ aligned, so any layer range is one contiguous byte range.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -32,6 +33,23 @@ from . import _lib
 from .costs import DEFAULT_GROUP, KvPrecision
 
 _ALIGN = 256
+
+# NVTX ranges around every hand-off stage when KVX_NVTX=1 (for nsys/ncu
+# timelines; off by default so the hot path pays nothing).
+_NVTX = os.environ.get("KVX_NVTX", "0") == "1"
+
+
+class nvtx_range:
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        if _NVTX:
+            torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *a):
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
 
 
 def _round_up(x: int, a: int = _ALIGN) -> int:
@@ -259,6 +277,11 @@ class KVPlanes:
 # ---------------------------------------------------------------------------
 
 def quant_pack_layers(src: KVPlanes, packed: PackedKV, l0: int, l1: int, stream=None) -> None:
+    with nvtx_range(f"kvx.K1 layers[{l0},{l1})"):
+        _quant_pack_layers(src, packed, l0, l1, stream)
+
+
+def _quant_pack_layers(src: KVPlanes, packed: PackedKV, l0: int, l1: int, stream=None) -> None:
     lay = packed.layout
     k, v = src.ptrs(l0)
     c, s, z = packed.ptrs(l0)
@@ -275,6 +298,11 @@ def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
     bulk kernel waits in-kernel for each chunk's doorbell (one launch per
     hand-off).  ``done=(counter_addr, peer_free_addr, n_ready)``: in-kernel
     completion (reset the doorbells, free the prefill-side queue half)."""
+    with nvtx_range(f"kvx.K3 layers[{l0},{l1})"):
+        _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done)
+
+
+def _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done) -> None:
     lay = packed.layout
     k, v = dst.ptrs(l0)
     c, s, z = packed.ptrs(l0)
