@@ -90,6 +90,7 @@ class ChannelSpec:
     min_chunk_bytes: int = PULL_CHUNK_TARGET  # pull modes: smaller hand-offs use fewer chunks
     format: str = "default"  # "default" (per-token groups) or "kivi" (pull modes only)
     device_doorbells: bool = True  # "pull": K1 itself rings per-chunk doorbells (one launch)
+    layerwise: bool = False  # pull: layer-granular chunks (<= 64) for open_send streaming
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -315,6 +316,9 @@ class PairChannel:
                 pull_supported(lay))
 
     def _pull_chunks(self, lay):
+        if self.spec.layerwise:  # streaming during prefill: publish as layers finish
+            n = min(lay.n_layers, PULL_MAX_CHUNKS)
+            return layer_chunks(lay.n_layers, n), layers_per_chunk(lay.n_layers, n)
         if self._fused(lay):
             # layer-granular doorbells, but every K1 warp should own several
             # items per chunk (one fence + atomic per warp per chunk)
@@ -367,6 +371,17 @@ class PairChannel:
         self._run_or_capture(key, body, s, cur, capturable=timing is None and stage_in is None)
         if stage_in is not None:
             cur.wait_stream(self.xfer)
+
+    def open_send(self, src: KVPlanes, n_tokens: int) -> "SendSession":
+        """Layer-wise hand-off during prefill (pull modes; SURVEY.md 8(f)3,
+        PAPER.md:859): returns a session whose ``layers_ready(n)`` quantises
+        and publishes every chunk whose layers are all < n, ordered after the
+        caller's current stream (the prefill compute that produced them) but
+        running on the channel's stream, so it overlaps the next layers'
+        compute.  The decode side calls ``recv`` as usual: its one K3-bulk
+        launch consumes the chunks as their doorbells ring."""
+        assert self.role == "prefill" and self.spec.mode in PULL_MODES
+        return SendSession(self, src, n_tokens)
 
     def _recv_pull(self, dst, lay, e, s, cur, timing, stage_out):
         h = e & 1
@@ -701,6 +716,36 @@ def _kernel_events_end(ev, stream):
 # ---------------------------------------------------------------------------
 # bench.py N > 1
 # ---------------------------------------------------------------------------
+
+
+class SendSession:
+    """See PairChannel.open_send."""
+
+    def __init__(self, ch: PairChannel, src: KVPlanes, n_tokens: int):
+        self.ch, self.src = ch, src
+        self.lay = ch.spec.layout(n_tokens)
+        ch.epoch += 1
+        self.h = ch.epoch & 1
+        self.chunks, _ = ch._pull_chunks(self.lay)
+        self.payload = PackedKV(self.lay, ch.k1_target + ch._half(ch.epoch), ch.device)
+        self.next = 0
+        s = ch.stream
+        s.wait_stream(torch.cuda.current_stream(ch.device))
+        wait(ch._pfree(ch.flags.ptr, self.h), 1, s)    # decode side done with this half
+        signal(ch._pfree(ch.flags.ptr, self.h), 0, s)  # claim it
+
+    def layers_ready(self, n_layers_done: int) -> None:
+        ch, s = self.ch, self.ch.stream
+        s.wait_stream(torch.cuda.current_stream(ch.device))  # after the layers' producer
+        while self.next < len(self.chunks) and self.chunks[self.next][1] <= n_layers_done:
+            l0, l1 = self.chunks[self.next]
+            quant_pack_layers(self.src, self.payload, l0, l1, s)
+            signal(ch._pready(ch.peer_flags, self.h, self.next), 1, s)
+            self.next += 1
+
+    def close(self) -> None:
+        self.layers_ready(self.lay.n_layers)
+        torch.cuda.current_stream(self.ch.device).wait_stream(self.ch.stream)
 
 
 class TPHandoff:

@@ -74,6 +74,41 @@ def main():
                       flush=True)
             dist.barrier()
             ch.close()
+    # layer-wise hand-off during prefill: the prefill side publishes chunks as
+    # "layers" become ready (a sleep kernel stands in for each layer's compute)
+    spec = ChannelSpec(L, Tmax, H, D, 4, 128, 3, "pull", layerwise=True)
+    ch = PairChannel(spec, rank, world, control_group=ctrl)
+    nb = Tmax // bs + 4
+    for epoch, T in enumerate((Tmax, 90, Tmax)):
+        seed = 4242 + 1000 * ch.pair + epoch
+        if ch.role == "prefill":
+            kv_np = O.synthetic_kv(L, T, H, D, seed=seed)
+            kv = torch.zeros((L, 2, T, H, D), dtype=torch.float16, device=dev)
+            sess = ch.open_send(KVPlanes.dense(kv), T)
+            for l in range(L):
+                torch.cuda._sleep(20000)  # "layer l of prefill"
+                kv[l].copy_(torch.from_numpy(kv_np[l]))  # its KV lands in HBM
+                sess.layers_ready(l + 1)
+            sess.close()
+            torch.cuda.synchronize()
+        else:
+            slots_np = O.synthetic_slots(T, bs, nb, seed=seed)
+            kc = torch.zeros((L, nb, bs, H, D), dtype=torch.float16, device=dev)
+            vc = torch.zeros_like(kc)
+            ch.recv(KVPlanes.paged(kc, vc, torch.from_numpy(slots_np).to(dev)), T)
+            torch.cuda.synchronize()
+            kv_np = O.synthetic_kv(L, T, H, D, seed=seed)
+            okc = np.zeros((L, nb, bs, H, D), np.float16); ovc = okc.copy()
+            c, s_, z = O.quant_pack(kv_np.reshape(-1, D), 4, 128)
+            O.scatter_paged(O.unpack_dequant(c, s_, z, 4, 128, D).reshape(L, 2, T, H, D),
+                            slots_np, okc, ovc)
+            if not (np.array_equal(kc.cpu().numpy().view(np.uint16), okc.view(np.uint16)) and
+                    np.array_equal(vc.cpu().numpy().view(np.uint16), ovc.view(np.uint16))):
+                failures += 1
+                print(f"MISMATCH layer-wise rank={rank} T={T}", flush=True)
+    dist.barrier()
+    ch.close()
+
     # kivi format over the pull queue (per-channel K + fp16 residual window)
     for bits, group in ((4, 32), (8, 64)):
         spec = ChannelSpec(L, Tmax, H, D, bits, group, 3, "pull", min_chunk_bytes=0,
