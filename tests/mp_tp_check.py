@@ -58,6 +58,51 @@ def main():
                         print(f"MISMATCH tp {pr}->{dr} mode={mode} rank={rank} T={T}", flush=True)
             dist.barrier()
             tp.close()
+    # routing (the reference's x/y fractions, simulate.py:112-127): every
+    # prefill rank sends a different request subset to each decode rank over
+    # its own edge channel; decode ranks receive from both prefill ranks into
+    # disjoint slots of one paged cache
+    from paper_2502_09334_b200.transport import ChannelSpec, PairChannel
+    P, Dr = [0, 1], [2, 3]
+    edges = [(p, d) for p in P for d in Dr]
+    chans = {e: PairChannel(ChannelSpec(L, 256, H, D, 4, 128, 2, "pull"), rank, world, ctrl,
+                            edge=e) for e in edges}
+    T_req = 64  # tokens per request; each prefill rank holds 4 requests
+    nb = 2 * len(P) * T_req // bs + 4
+    for epoch in range(3):
+        if rank in P:
+            i = P.index(rank)
+            kv = O.synthetic_kv(L, 4 * T_req, H, D, seed=900 + 10 * epoch + i)
+            kvd = torch.from_numpy(kv).to(dev)
+            kc_src = kvd[:, 0]  # dense planes viewed as a "paged" source with token gather
+            for j, d in enumerate(Dr):
+                # requests 2j, 2j+1 of this prefill rank go to decode rank d
+                toks = torch.arange(2 * j * T_req, (2 * j + 2) * T_req, device=dev)
+                src = KVPlanes(kvd[:, 0], kvd[:, 1], kvd.stride(0), L, H, D, toks)
+                chans[(rank, d)].send(src, 2 * T_req)
+            torch.cuda.synchronize()
+        if rank in Dr:
+            j = Dr.index(rank)
+            kc = torch.zeros((L, nb, bs, H, D), dtype=torch.float16, device=dev)
+            vc = torch.zeros_like(kc)
+            okc = np.zeros((L, nb, bs, H, D), np.float16); ovc = okc.copy()
+            for i, p in enumerate(P):
+                slots = np.arange(2 * T_req, dtype=np.int64) + (i * 2 * T_req)  # disjoint
+                chans[(p, rank)].recv(KVPlanes.paged(kc, vc, torch.from_numpy(slots).to(dev)),
+                                      2 * T_req)
+                kv = O.synthetic_kv(L, 4 * T_req, H, D, seed=900 + 10 * epoch + i)
+                sub = np.ascontiguousarray(kv[:, :, 2 * j * T_req:(2 * j + 2) * T_req])
+                c, s_, z = O.quant_pack(sub.reshape(-1, D), 4, 128)
+                O.scatter_paged(O.unpack_dequant(c, s_, z, 4, 128, D).reshape(sub.shape), slots,
+                                okc, ovc)
+            torch.cuda.synchronize()
+            if not (np.array_equal(kc.cpu().numpy().view(np.uint16), okc.view(np.uint16)) and
+                    np.array_equal(vc.cpu().numpy().view(np.uint16), ovc.view(np.uint16))):
+                failures += 1
+                print(f"MISMATCH routed rank={rank} epoch={epoch}", flush=True)
+    dist.barrier()
+    for ch in chans.values():
+        ch.close()
     f = torch.tensor([failures], device=dev)
     dist.all_reduce(f)
     if rank == 0:
