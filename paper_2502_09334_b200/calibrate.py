@@ -103,12 +103,41 @@ def measure(n_gpus: int, bits: int = 4, L: int = 32, H: int = 8, D: int = 128,
     return alpha, beta
 
 
+def cluster_from_bench_line(line: dict, n_gpus: int, peaks: dict | None = None) -> dict:
+    """Uniform NVSwitch cluster from a bench.py N>1 JSON line's live
+    calibration (multi-process, CUDA-graph replayed pull channel): every
+    ordered GPU pair gets the measured (alpha, beta)."""
+    cal = line["calibration"]
+    alpha = cal["alpha_us"] * 1e-6
+    beta = cal["beta_GBps_of_modelled_volume"] * 1e9
+    a = [[alpha] * n_gpus for _ in range(n_gpus)]
+    b = [[beta] * n_gpus for _ in range(n_gpus)]
+    pk = peaks or {}
+    hbm = float(pk.get("hbm_gbs", 6650.0)) * 1e9
+    flops = float(pk.get("bf16_tflops_sustained", 1400.0)) * 1e12
+    return cluster_dict(a, b, local_beta=hbm, mem_bandwidth=hbm, peak_flops=flops)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
     ap.add_argument("--bits", type=int, default=4)
     ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--from-bench", default=None,
+                    help="build the cluster from a bench.py N>1 JSON line instead of measuring")
     args = ap.parse_args()
+    if args.from_bench:
+        line = [json.loads(x) for x in open(args.from_bench) if x.startswith("{")][-1]
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        try:
+            peaks = json.load(open(os.path.join(root, "MEASURED_PEAKS.json")))
+        except Exception:  # noqa: BLE001
+            peaks = None
+        d = cluster_from_bench_line(line, args.gpus or line["n_gpus"], peaks)
+        with open(args.out, "w") as f:
+            json.dump(d, f, indent=2, sort_keys=True)
+        print(json.dumps(line["calibration"]))
+        return
     n = args.gpus or torch.cuda.device_count()
     if n < 2:
         raise SystemExit("calibration needs >= 2 GPUs")
