@@ -24,12 +24,18 @@ prefill replicas' GPU memory (``PAPER.md:859``).  Here:
     "copy" - K1 local, copy-engine cudaMemcpyAsync into D's landing buffer,
              K3 local (the non-fused baseline).
     "nccl" - K1 local, torch.distributed (NCCL) send/recv per chunk, K3 local.
-* chunk pipeline: layers are cut into chunks; per chunk P signals a 32-bit
-  doorbell in D's memory (cuStreamWriteValue32, fenced) and D's stream waits on
-  it in the front-end (cuStreamWaitValue32 GEQ epoch), so K1 of chunk c+1, the
-  link and K3 of chunk c overlap.  D acks each chunk back into P's memory so
-  the next hand-off never overwrites a chunk still being read.  No spinning
-  kernels, no host round trips per chunk.
+* chunk pipeline: layers are cut into chunks and every chunk has a 32-bit
+  doorbell in D's memory, so K1 of chunk c+1, the link and K3 of chunk c
+  overlap.  In the default "pull" mode ONE K1 launch rings the doorbells from
+  the device (fence + st.release.sys over NVLink, by the last warp to finish
+  the chunk) and ONE K3-bulk launch waits for them in-kernel (bounded
+  ld.acquire polling by its producer warps); its last CTA resets the doorbells
+  and releases the queue half back to P.  P's queue is double-buffered
+  (hand-off e uses half e % 2).  The flags take constant values (0/1), so both
+  ends of a hand-off are captured once as CUDA graphs and replayed.  The other
+  modes use stream memory operations (cuStreamWriteValue32 /
+  cuStreamWaitValue32) for the same doorbells, in the GPU front-end.  No
+  host round trips per chunk.
 """
 from __future__ import annotations
 

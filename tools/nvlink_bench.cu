@@ -105,12 +105,15 @@ int main() {
   cudaSetDevice(1); cudaFuncSetAttribute(pull_bulk<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * CH);
   cudaSetDevice(0); cudaFuncSetAttribute(push_bulk<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * CH);
   const size_t n16 = bytes / 16, nch = bytes / CH;
-  struct R { const char* name; float ms; } r[5];
+  struct R { const char* name; float ms; } r[8];
   r[0] = {"pull_ldg (GPU1 LDG.128 from GPU0)", timeit(1, [&] { copy_ldg<<<sms * 8, 256>>>((const uint4*)g0a, (uint4*)g1a, n16); })};
   r[1] = {"pull_bulk (GPU1 cp.async.bulk from GPU0, 16 KB)", timeit(1, [&] { pull_bulk<CH><<<sms * 2, 256, 4 * CH>>>(g0a, g1a, nch); })};
   r[2] = {"push_stg (GPU0 STG.128 into GPU1)", timeit(0, [&] { copy_ldg<<<sms * 8, 256>>>((const uint4*)g0a, (uint4*)g1b, n16); })};
   r[3] = {"push_bulk (GPU0 cp.async.bulk store into GPU1, 16 KB)", timeit(0, [&] { push_bulk<CH><<<sms * 2, 256, 2 * CH>>>(g0a, g1b, nch); })};
   r[4] = {"ce_peer (cudaMemcpyPeerAsync GPU0 -> GPU1)", timeit(0, [&] { cudaMemcpyPeerAsync(g1b, 1, g0a, 0, bytes, 0); })};
+  r[5] = {"ce_pull (cudaMemcpyPeerAsync issued on GPU1, GPU0 -> GPU1)", timeit(1, [&] { cudaMemcpyPeerAsync(g1b, 1, g0a, 0, bytes, 0); })};
+  r[6] = {"ce_pull_default (cudaMemcpyAsync Default on GPU1, GPU0 -> GPU1)", timeit(1, [&] { cudaMemcpyAsync(g1b, g0a, bytes, cudaMemcpyDefault, 0); })};
+  r[7] = {"ce_pull_samedev (cudaMemcpyPeerAsync(dst,1,src,1) on GPU1)", timeit(1, [&] { cudaMemcpyPeerAsync(g1b, 1, g0a, 1, bytes, 0); })};
   for (auto& x : r) printf("{\"path\": \"%s\", \"ms\": %.4f, \"GBps\": %.1f}\n", x.name, x.ms, bytes / (x.ms * 1e-3) / 1e9);
   cudaError_t e = cudaGetLastError();
   printf("{\"status\": \"%s\"}\n", cudaGetErrorString(e));
