@@ -97,17 +97,30 @@ int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_strid
 /*
  * K1 with device-side doorbells (fused quantise -> NVLink pull pipeline):
  * same contract as kvx_quant_pack (bits 2/4/8), plus for every chunk of
- * layers_per_chunk layers the kernel itself sets peer_ready_flags[chunk] = 1
- * (a peer/IPC-mapped address on the decode GPU; fence.sys + st.release.sys)
- * as soon as the chunk's payload is complete, while it keeps quantising later
- * layers.  counters: n_chunks u32 of scratch on this GPU (zeroed by the call).
+ * layers_per_chunk layers the kernel itself sets peer_ready_flags[chunk] =
+ * p ^ 1 (a peer/IPC-mapped address on the decode GPU; fence.sys +
+ * st.release.sys) as soon as the chunk's payload is complete, while it keeps
+ * quantising later layers.
+ * counters: 65 u32 of scratch on this GPU, zero before the first call (the
+ * kernel leaves them zero again).
+ * parity_state (nullable = parity 0, never flipped): a u32 on this GPU
+ * holding the queue half's parity p; the last CTA to exit flips it.
+ * free_flag (nullable, this GPU's memory): before storing anything, every
+ * CTA waits (bounded, in-kernel) until *free_flag == p -- the decode side's
+ * "queue half consumed" flag -- so a hand-off needs no stream-memop nodes.
+ * Transport protocol (every flag value is read from device state, so a
+ * captured CUDA graph replays unchanged; no flag is ever reset, so there is
+ * no lost wake-up): the u-th use of a queue half has p = u & 1, rings
+ * ready = p ^ 1 and, once the decode side has consumed it, finds
+ * free = p ^ 1 -- which is what the half's next use (parity p ^ 1) waits for.
  */
 int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_layer_stride,
                           const int64_t* src_slots, int64_t n_layers, int64_t n_tokens,
                           int n_heads, int head_dim, int group, int bits, void* codes,
                           void* scale, void* zero, int64_t payload_layer_stride,
                           int plane_heads, int head_offset, void* counters,
-                          void* peer_ready_flags, int layers_per_chunk, void* stream);
+                          void* peer_ready_flags, int layers_per_chunk, const void* free_flag,
+                          void* parity_state, void* stream);
 
 /*
  * K3: unpack + dequantise + scatter into the decode side's paged KV cache.
@@ -132,24 +145,25 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
  * per span of token rows) -- the fused NVLink-pull variant for a payload that
  * lives in the prefill GPU's HBM.
  * ready_flags (nullable, this GPU's memory): the kernel itself waits, per
- * chunk of layers_per_chunk layers, until ready_flags[chunk] >= epoch
- * (wrap-safe), so ONE launch consumes a whole hand-off while the prefill GPU
- * is still producing it (the producer publishes chunks with
- * kvx_stream_signal).  Without flags, shapes whose rows are not 16-byte
- * multiples fall back to the per-lane kernel; with flags they return
- * KVX_ERR_UNSUPPORTED (see kvx_pull_supported).
+ * chunk of layers_per_chunk layers, until ready_flags[chunk] == p ^ 1 (p =
+ * *parity_state, or 0 without one), so ONE launch consumes a whole hand-off
+ * while the prefill GPU is still producing it (kvx_quant_pack_signal, or
+ * kvx_stream_signal after each chunk's K1).  Without flags, shapes whose rows
+ * are not 16-byte multiples fall back to the per-lane kernel; with flags they
+ * return KVX_ERR_UNSUPPORTED (see kvx_pull_supported).
  * done_counter / peer_free_flag (nullable, together): in-kernel completion --
- * the last CTA resets ready_flags[0..n_ready) to 0, zeroes *done_counter (a
- * u32 on this GPU, 0 before the first call) and sets *peer_free_flag = 1
- * (a peer/IPC-mapped u32 on the prefill GPU: "queue half consumed").
+ * the last CTA zeroes *done_counter (a u32 on this GPU, 0 before the first
+ * call), sets *peer_free_flag = p ^ 1 (a peer/IPC-mapped u32 on the prefill
+ * GPU: "queue half consumed") and flips *parity_state (this GPU's parity of
+ * the half; requires done_counter).
  */
 int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
                                    int64_t payload_layer_stride, const int64_t* dst_slots,
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
                                    int64_t dst_layer_stride, int plane_heads, int head_offset,
-                                   const void* ready_flags, uint32_t epoch, int layers_per_chunk,
-                                   void* done_counter, void* peer_free_flag, int n_ready,
+                                   const void* ready_flags, int layers_per_chunk,
+                                   void* done_counter, void* peer_free_flag, void* parity_state,
                                    void* stream);
 
 /* 1 if kvx_pull_dequant_scatter_paged can bulk-stage this shape. */
@@ -211,13 +225,15 @@ int kvx_ipc_get_handle(void* ptr, void* handle_out);
 int kvx_ipc_open(const void* handle, void** ptr_out);
 int kvx_ipc_close(void* ptr);
 
-/* Stream-ordered 32-bit flags (cuStreamWriteValue32 / cuStreamWaitValue32
- * GEQ) used as cross-GPU chunk doorbells: the producer signals after the
- * chunk's kernel (with a memory barrier), the consumer's stream blocks in the
- * front-end (no spinning kernel) until flag >= value.  flag may be a local,
- * peer or IPC-mapped device address. */
+/* Stream-ordered 32-bit flags (cuStreamWriteValue32 / cuStreamWaitValue32)
+ * used as cross-GPU chunk doorbells: the producer signals after the chunk's
+ * kernel (with a memory barrier), the consumer's stream blocks in the
+ * front-end (no spinning kernel) until flag >= value (wrap-safe), or, for
+ * kvx_stream_wait_eq, until flag == value.  flag may be a local, peer or
+ * IPC-mapped device address. */
 int kvx_stream_signal(void* flag, uint32_t value, void* stream);
 int kvx_stream_wait(const void* flag, uint32_t value, void* stream);
+int kvx_stream_wait_eq(const void* flag, uint32_t value, void* stream);
 /* 1 if stream memory operations are usable on the current device. */
 int kvx_stream_memops_supported(int* supported);
 

@@ -33,11 +33,11 @@ SIGNATURES = {
     "kvx_device_count": [ctypes.POINTER(_I)],
     "kvx_quant_pack": [_P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _I64, _I, _I, _P],
     "kvx_quant_pack_signal": [_P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _I64,
-                              _I, _I, _P, _P, _I, _P],
+                              _I, _I, _P, _P, _I, _P, _P, _P],
     "kvx_dequant_scatter_paged": [_P, _P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _I64,
                                   _I, _I, _P],
     "kvx_pull_dequant_scatter_paged": [_P, _P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P,
-                                       _I64, _I, _I, _P, _U32, _I, _P, _P, _I, _P],
+                                       _I64, _I, _I, _P, _I, _P, _P, _P, _P],
     "kvx_pull_supported": [_I64, _I, _I, _I, _I],
     "kvx_quant_pack_kivi": [_P, _P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _I64, _P,
                             _I64, _P, _P],
@@ -56,6 +56,7 @@ SIGNATURES = {
     "kvx_ipc_close": [_P],
     "kvx_stream_signal": [_P, _U32, _P],
     "kvx_stream_wait": [_P, _U32, _P],
+    "kvx_stream_wait_eq": [_P, _U32, _P],
     "kvx_stream_memops_supported": [ctypes.POINTER(_I)],
 }
 

@@ -136,6 +136,8 @@ cudaError_t make_items(const kvx::Geo& g, kvx::ItemGeo& ig) {
 struct SignalReq {
   uint32_t* counters = nullptr;
   uint32_t* peer_flags = nullptr;
+  uint32_t* parity = nullptr;
+  const uint32_t* free_flag = nullptr;
   int layers_per_chunk = 1;
   int64_t n_layers = 0;
 };
@@ -150,6 +152,8 @@ cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero
   sig.counters = rq.counters;
   sig.peer_flags = rq.peer_flags;
   sig.items_per_chunk = 1;
+  sig.parity = rq.parity;
+  sig.free_flag = rq.free_flag;
   if (rq.peer_flags) {
     const int64_t per_layer = ig.n_items / (rq.n_layers > 0 ? rq.n_layers : 1);
     const int64_t ipc = per_layer * rq.layers_per_chunk;
@@ -157,8 +161,7 @@ cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero
     sig.items_per_chunk = uint32_t(ipc);
     const int64_t n_chunks = (ig.n_items + ipc - 1) / ipc;
     if (n_chunks > kvx::kMaxSignalChunks) return cudaErrorInvalidValue;
-    e = cudaMemsetAsync(rq.counters, 0, size_t(n_chunks) * 4, s);
-    if (e != cudaSuccess) return e;
+    // (the counters are zero between launches: each chunk's last arrival resets its own)
   }
   auto k = kvx::quant_pack_kernel<BITS, G>;
   k<<<grid_for(k, ig.n_items), kThreads, 0, s>>>(g, ig, static_cast<uint8_t*>(codes),
@@ -204,20 +207,19 @@ int64_t bulk_row_multiple(int64_t code_row_bytes, int64_t meta_row_bytes) {
 struct PullDone {  // optional in-kernel completion of a pull hand-off
   uint32_t* done_counter = nullptr;
   uint32_t* peer_free = nullptr;
-  int n_ready = 0;
+  uint32_t* parity = nullptr;
 };
 
 template <int BITS, int G>
 cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale, const void* zero,
-                        cudaStream_t s, bool* ok, const uint32_t* ready, uint32_t epoch,
+                        cudaStream_t s, bool* ok, const uint32_t* ready,
                         int layers_per_chunk, const PullDone& done = PullDone()) {
   *ok = false;
   kvx::BulkGeo bg;
   bg.ready = ready;
-  bg.epoch = epoch;
+  bg.parity = done.parity;
   bg.done_counter = done.done_counter;
   bg.peer_free = done.peer_free;
-  bg.n_ready = done.n_ready;
   bg.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
   bg.code_row_bytes = int(int64_t(g.row_elems) * BITS / 8);
   bg.meta_row_bytes = int(int64_t(g.row_elems) / G * 2);
@@ -274,11 +276,11 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
 template <int BITS>
 cudaError_t dispatch_pull(int group, const kvx::Geo& g, const void* c, const void* sc,
                           const void* z, cudaStream_t s, bool* ok, const uint32_t* ready,
-                          uint32_t epoch, int lpc, const PullDone& done) {
+                          int lpc, const PullDone& done) {
   switch (group) {
-    case 32: return launch_pull<BITS, 32>(g, c, sc, z, s, ok, ready, epoch, lpc, done);
-    case 64: return launch_pull<BITS, 64>(g, c, sc, z, s, ok, ready, epoch, lpc, done);
-    default: return launch_pull<BITS, 128>(g, c, sc, z, s, ok, ready, epoch, lpc, done);
+    case 32: return launch_pull<BITS, 32>(g, c, sc, z, s, ok, ready, lpc, done);
+    case 64: return launch_pull<BITS, 64>(g, c, sc, z, s, ok, ready, lpc, done);
+    default: return launch_pull<BITS, 128>(g, c, sc, z, s, ok, ready, lpc, done);
   }
 }
 
@@ -430,11 +432,13 @@ int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_laye
                           int n_heads, int head_dim, int group, int bits, void* codes,
                           void* scale, void* zero, int64_t payload_layer_stride,
                           int plane_heads, int head_offset, void* counters,
-                          void* peer_ready_flags, int layers_per_chunk, void* stream) {
+                          void* peer_ready_flags, int layers_per_chunk, const void* free_flag,
+                          void* parity_state, void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
   if (bits == 16 || !counters || !peer_ready_flags || layers_per_chunk < 1 ||
-      !aligned(counters, 4) || !aligned(peer_ready_flags, 4))
+      !aligned(counters, 4) || !aligned(peer_ready_flags, 4) || !aligned(free_flag, 4) ||
+      !aligned(parity_state, 4))
     return KVX_ERR_INVALID_ARG;
   kvx::Geo g;
   rc = make_geo(g, k_src, v_src, src_layer_stride, src_slots, n_layers, n_tokens, n_heads, head_dim,
@@ -448,6 +452,8 @@ int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_laye
   SignalReq rq;
   rq.counters = static_cast<uint32_t*>(counters);
   rq.peer_flags = static_cast<uint32_t*>(peer_ready_flags);
+  rq.parity = static_cast<uint32_t*>(parity_state);
+  rq.free_flag = static_cast<const uint32_t*>(free_flag);
   rq.layers_per_chunk = layers_per_chunk;
   rq.n_layers = n_layers;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -496,8 +502,8 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
                                    int64_t dst_layer_stride, int plane_heads, int head_offset,
-                                   const void* ready_flags, uint32_t epoch, int layers_per_chunk,
-                                   void* done_counter, void* peer_free_flag, int n_ready,
+                                   const void* ready_flags, int layers_per_chunk,
+                                   void* done_counter, void* peer_free_flag, void* parity_state,
                                    void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
@@ -508,13 +514,14 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
   if (g.n_token_rows == 0) return KVX_OK;
   if (ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) return KVX_ERR_INVALID_ARG;
   if ((done_counter != nullptr) != (peer_free_flag != nullptr) ||
-      (done_counter && (!ready_flags || n_ready < 0 || !aligned(done_counter, 4) ||
+      !aligned(parity_state, 4) || (parity_state && !done_counter) ||
+      (done_counter && (!ready_flags || !aligned(done_counter, 4) ||
                         !aligned(peer_free_flag, 4))))
     return KVX_ERR_INVALID_ARG;
   PullDone done;
   done.done_counter = static_cast<uint32_t*>(done_counter);
   done.peer_free = static_cast<uint32_t*>(peer_free_flag);
-  done.n_ready = n_ready;
+  done.parity = static_cast<uint32_t*>(parity_state);
   if (bits != 16 && codes && scale && zero && k_cache && aligned(k_cache, 32) &&
       aligned(v_cache, 32) && (dst_layer_stride * 2) % 32 == 0 && g.plane_row_b % 32 == 0 &&
       g.head_off_b % 32 == 0) {
@@ -523,9 +530,9 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
     bool ok = false;
     cudaError_t e;
     switch (bits) {
-      case 2: e = dispatch_pull<2>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk, done); break;
-      case 8: e = dispatch_pull<8>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk, done); break;
-      default: e = dispatch_pull<4>(group, g, codes, scale, zero, s, &ok, rf, epoch, layers_per_chunk, done); break;
+      case 2: e = dispatch_pull<2>(group, g, codes, scale, zero, s, &ok, rf, layers_per_chunk, done); break;
+      case 8: e = dispatch_pull<8>(group, g, codes, scale, zero, s, &ok, rf, layers_per_chunk, done); break;
+      default: e = dispatch_pull<4>(group, g, codes, scale, zero, s, &ok, rf, layers_per_chunk, done); break;
     }
     if (e != cudaSuccess) return e;
     if (ok) return KVX_OK;
@@ -752,6 +759,15 @@ int kvx_stream_wait(const void* flag, uint32_t value, void* stream) {
   if (!flag || !aligned(flag, 4)) return KVX_ERR_INVALID_ARG;
   CUresult r = g_wait32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
                         CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? KVX_OK : KVX_ERR_UNSUPPORTED;
+}
+
+int kvx_stream_wait_eq(const void* flag, uint32_t value, void* stream) {
+  resolve_driver();
+  if (g_drv_status) return g_drv_status;
+  if (!flag || !aligned(flag, 4)) return KVX_ERR_INVALID_ARG;
+  CUresult r = g_wait32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                        CU_STREAM_WAIT_VALUE_EQ);
   return r == CUDA_SUCCESS ? KVX_OK : KVX_ERR_UNSUPPORTED;
 }
 

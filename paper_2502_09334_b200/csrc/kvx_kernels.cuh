@@ -369,10 +369,31 @@ __device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)
 constexpr int kMaxSignalChunks = 64;  // = transport.PULL_MAX_CHUNKS
 
 struct SignalGeo {
-  uint32_t* counters;    // [n_chunks] arrivals (zeroed before the launch)
+  // [kMaxSignalChunks] chunk arrivals + [1] CTA exits; zero at launch, and
+  // reset in-kernel by the last arrival, so zero again after every launch
+  uint32_t* counters;
   uint32_t* peer_flags;  // [n_chunks] decode-side ready flags (IPC/peer mapped), or null
   uint32_t items_per_chunk;
+  // queue-half parity p (nullable = 0): doorbells are set to p ^ 1; the last
+  // CTA to exit flips *parity to p ^ 1 for the half's next use
+  uint32_t* parity;
+  // queue half free (nullable): every CTA waits *free_flag == p (written by
+  // the decode side over NVLink) before it stores into the half
+  const uint32_t* free_flag;
 };
+
+// Bounded spin until *flag == value (system-scope acquire: the flag is
+// written by the partner GPU over NVLink).  Traps after ~60 s so a lost
+// partner cannot hang the GPU forever.
+__device__ __forceinline__ void spin_until_eq(const uint32_t* flag, uint32_t value) {
+  uint32_t v;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v == value) break;
+    if (spin > (1u << 26)) __trap();
+    __nanosleep(spin < 64 ? 32 : 512);
+  }
+}
 
 // Warps w in [lo, hi) that own at least one item i in [a, b) (item i -> warp i % W).
 __device__ __forceinline__ uint32_t warps_owning(uint32_t a, uint32_t b, uint32_t W, uint32_t lo,
@@ -401,7 +422,8 @@ __device__ __forceinline__ uint32_t ctas_owning(uint32_t a, uint32_t b, uint32_t
 // one to the global chunk counter, the last CTA rings the peer's doorbell
 // (a same-address global atomic per warp would serialise for small hand-offs).
 __device__ __forceinline__ void chunk_arrive(const SignalGeo& sig, uint32_t* cta_cnt, uint32_t c,
-                                             uint32_t n_items, uint32_t n_warps, int lane) {
+                                             uint32_t n_items, uint32_t n_warps, int lane,
+                                             uint32_t ready_value) {
   __threadfence();  // this lane's payload stores, device-wide
   __syncwarp();
   if (lane == 0) {
@@ -412,8 +434,10 @@ __device__ __forceinline__ void chunk_arrive(const SignalGeo& sig, uint32_t* cta
     if (atomicAdd_block(cta_cnt + c, 1u) + 1 == mine) {
       __threadfence();
       if (atomicAdd(sig.counters + c, 1u) + 1 == ctas_owning(a, b, n_warps)) {
+        sig.counters[c] = 0u;  // every owner has arrived: ready for the next launch
         __threadfence_system();
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags + c), "r"(1u)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags + c),
+                     "r"(ready_value)
                      : "memory");
       }
     }
@@ -433,10 +457,17 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
   __shared__ uint32_t cta_cnt[kMaxSignalChunks];
+  __shared__ uint32_t s_parity;
   if (sig.peer_flags) {
     for (int i = threadIdx.x; i < kMaxSignalChunks; i += blockDim.x) cta_cnt[i] = 0u;
+    if (threadIdx.x == 0) {
+      const uint32_t p = sig.parity ? *sig.parity : 0u;
+      if (sig.free_flag) spin_until_eq(sig.free_flag, p);  // decode side done with the half
+      s_parity = p;
+    }
     __syncthreads();
   }
+  const uint32_t ready_value = sig.peer_flags ? (s_parity ^ 1u) : 0u;
   uint32_t w[NB][16];
   K1Item it[NB];
 #pragma unroll
@@ -454,7 +485,7 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
 #pragma unroll
     for (int st = 0; st < NB; ++st) {
       const uint32_t cur = base + st * n_warps;
-      if (cur >= ig.n_items) return;  // warp-uniform
+      if (cur >= ig.n_items) goto k1_done;  // warp-uniform
       const uint32_t pre = cur + (NB - 1) * n_warps;
       const int pb = (st + NB - 1) % NB;
       if (pre < ig.n_items) {
@@ -469,8 +500,17 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
         const uint32_t c = cur / sig.items_per_chunk;
         const uint32_t nxt = cur + n_warps;
         if (nxt >= ig.n_items || nxt / sig.items_per_chunk != c)
-          chunk_arrive(sig, cta_cnt, c, ig.n_items, n_warps, lane);
+          chunk_arrive(sig, cta_cnt, c, ig.n_items, n_warps, lane, ready_value);
       }
+    }
+  }
+k1_done:
+  if (sig.peer_flags && sig.parity) {
+    // every CTA has read the parity (at its start): the last one out flips it
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(sig.counters + kMaxSignalChunks, 1u) == gridDim.x - 1) {
+      sig.counters[kMaxSignalChunks] = 0u;
+      *sig.parity = s_parity ^ 1u;
     }
   }
 }
@@ -684,14 +724,14 @@ __global__ void __launch_bounds__(256) scatter16_kernel(Geo g, const uint8_t* __
 // cache; each warp releases the stage through an "empty" mbarrier.
 // ---------------------------------------------------------------------------
 struct BulkGeo {
-  const uint32_t* ready; // per-chunk doorbells (nullable): wait ready[c] >= epoch
-  uint32_t epoch;
-  // in-kernel completion (nullable): the last CTA to finish resets the n_ready
-  // doorbells to 0 and sets *peer_free = 1 on the prefill GPU (queue half
-  // consumed) -- no memset / stream-memop nodes after the kernel
+  // per-chunk doorbells (nullable): wait ready[c] == p ^ 1, p = *parity (or 0)
+  const uint32_t* ready;
+  uint32_t* parity;
+  // in-kernel completion (nullable): the last CTA to finish sets
+  // *peer_free = p ^ 1 on the prefill GPU (queue half consumed) and flips
+  // *parity -- no memset / stream-memop nodes after the kernel
   uint32_t* done_counter;
   uint32_t* peer_free;
-  int n_ready;
   int layers_per_chunk;
   int rows_per_span;     // R
   int spans_per_layer;   // ceil(2T / R)
@@ -726,19 +766,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Block (producer thread only) until the prefill side has published chunk c of
-// this epoch.  The doorbell lives in this GPU's memory and is written over
-// NVLink by the prefill GPU's stream (cuStreamWriteValue32, fenced); the
-// acquire + proxy fence order the following bulk reads of the peer payload.
-// Bounded: traps after ~60 s instead of hanging the GPU.
-__device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t epoch) {
-  uint32_t v;
-  for (uint32_t spin = 0;; ++spin) {
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    if (int32_t(v - epoch) >= 0) break;
-    if (spin > (1u << 26)) __trap();
-    __nanosleep(spin < 64 ? 32 : 512);
-  }
+// Block (producer thread only) until the prefill side has published chunk c
+// (doorbell == this hand-off's ready value).  The doorbell lives in this GPU's
+// memory and is written over NVLink by the prefill GPU (K1's last arriving
+// warp, or a stream memop); the acquire + proxy fence order the following
+// bulk reads of the peer payload.  Bounded (spin_until_eq).
+__device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t value) {
+  spin_until_eq(flag, value);
+  // the bulk copies that follow read through the async proxy
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
@@ -771,6 +806,7 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
   __syncthreads();
   const int64_t two_t = int64_t(g.planes) * g.n_tokens;  // payload rows per layer
 
+  const uint32_t par = bg.parity ? *bg.parity : 0u;  // read by every CTA before the flip
   if (warp == CONSUMERS) {  // ---- producer: one elected thread
     if (lane == 0) {
       uint32_t k = 0;
@@ -782,7 +818,7 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
         if (bg.ready) {
           const int c = int(layer) / bg.layers_per_chunk;
           if (c > ready_chunk) {
-            wait_ready(bg.ready + c, bg.epoch);
+            wait_ready(bg.ready + c, par ^ 1u);
             ready_chunk = c;
           }
         }
@@ -856,11 +892,11 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     if (threadIdx.x == 0) {
       __threadfence();
       if (atomicAdd(bg.done_counter, 1u) == gridDim.x - 1) {  // last CTA of the launch
-        uint32_t* rr = const_cast<uint32_t*>(bg.ready);
-        for (int c = 0; c < bg.n_ready; ++c) rr[c] = 0u;
         *bg.done_counter = 0u;
+        if (bg.parity) *bg.parity = par ^ 1u;
         __threadfence_system();
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(bg.peer_free), "r"(1u) : "memory");
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(bg.peer_free), "r"(par ^ 1u)
+                     : "memory");
       }
     }
   }

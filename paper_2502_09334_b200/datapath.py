@@ -294,10 +294,11 @@ def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
                            stream=None, bulk: bool = False, ready: tuple | None = None,
                            done: tuple | None = None) -> None:
     """K3 on layers [l0, l1).  ``bulk``: TMA bulk-staged variant (for payloads
-    read over NVLink).  ``ready=(flags_addr, epoch, layers_per_chunk)``: the
-    bulk kernel waits in-kernel for each chunk's doorbell (one launch per
-    hand-off).  ``done=(counter_addr, peer_free_addr, n_ready)``: in-kernel
-    completion (reset the doorbells, free the prefill-side queue half)."""
+    read over NVLink).  ``ready=(flags_addr, layers_per_chunk)``: the bulk
+    kernel waits in-kernel for each chunk's doorbell (one launch per
+    hand-off).  ``done=(counter_addr, peer_free_addr, parity_addr)``: in-kernel
+    completion (release the prefill-side queue half, flip the half's parity;
+    see kvx.h for the protocol)."""
     with nvtx_range(f"kvx.K3 layers[{l0},{l1})"):
         _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done)
 
@@ -309,10 +310,10 @@ def _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done) -> N
     args = (c, s, z, lay.layer_stride, dst.slots_ptr, l1 - l0, lay.n_tokens, lay.n_heads,
             lay.head_dim, lay.group, lay.bits, k, v, dst.layer_stride, *dst.window_args)
     if bulk or ready is not None:
-        rf, epoch, lpc = ready if ready is not None else (None, 0, 1)
-        dc, pf, nr = done if done is not None else (None, None, 0)
-        _lib.call("kvx_pull_dequant_scatter_paged", *args, rf, epoch & 0xFFFFFFFF, lpc, dc, pf,
-                  nr, _stream_ptr(stream))
+        rf, lpc = ready if ready is not None else (None, 1)
+        dc, pf, par = done if done is not None else (None, None, None)
+        _lib.call("kvx_pull_dequant_scatter_paged", *args, rf, lpc, dc, pf, par,
+                  _stream_ptr(stream))
     else:
         _lib.call("kvx_dequant_scatter_paged", *args, _stream_ptr(stream))
 

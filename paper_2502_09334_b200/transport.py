@@ -29,13 +29,14 @@ prefill replicas' GPU memory (``PAPER.md:859``).  Here:
   overlap.  In the default "pull" mode ONE K1 launch rings the doorbells from
   the device (fence + st.release.sys over NVLink, by the last warp to finish
   the chunk) and ONE K3-bulk launch waits for them in-kernel (bounded
-  ld.acquire polling by its producer warps); its last CTA resets the doorbells
-  and releases the queue half back to P.  P's queue is double-buffered
-  (hand-off e uses half e % 2).  The flags take constant values (0/1), so both
-  ends of a hand-off are captured once as CUDA graphs and replayed.  The other
-  modes use stream memory operations (cuStreamWriteValue32 /
-  cuStreamWaitValue32) for the same doorbells, in the GPU front-end.  No
-  host round trips per chunk.
+  ld.acquire polling by its producer warps); its last CTA releases the queue
+  half back to P, and K1's CTAs wait in-kernel for that release before they
+  reuse the half.  P's queue is double-buffered (hand-off e uses half e % 2).
+  The flags take constant values per (half, parity) and are never reset, so
+  both ends of a hand-off are single CUDA-graph launches with no memop or
+  memset nodes (see PairChannel._parity).  The non-fused paths use stream
+  memory operations (cuStreamWriteValue32 / cuStreamWaitValue32) on the same
+  doorbells, in the GPU front-end.  No host round trips per chunk.
 """
 from __future__ import annotations
 
@@ -205,6 +206,10 @@ def wait(flag_addr: int, value: int, stream) -> None:
     _lib.call("kvx_stream_wait", flag_addr, value & 0xFFFFFFFF, _stream_ptr(stream))
 
 
+def wait_eq(flag_addr: int, value: int, stream) -> None:
+    _lib.call("kvx_stream_wait_eq", flag_addr, value & 0xFFFFFFFF, _stream_ptr(stream))
+
+
 # ---------------------------------------------------------------------------
 # The channel
 # ---------------------------------------------------------------------------
@@ -258,17 +263,15 @@ class PairChannel:
         # local buffers: doorbells (written by the partner) + payload staging
         self.flags = IpcBuffer(FLAG_SLOTS * 4)
         self.graphs = bool(graphs) and mode in PULL_MODES
-        self.counters = torch.zeros(PULL_MAX_CHUNKS, dtype=torch.int32, device=self.device)
+        # K1's chunk arrival counters + CTA exit counter (zero between launches)
+        self.counters = torch.zeros(PULL_MAX_CHUNKS + 1, dtype=torch.int32, device=self.device)
         self.done_counter = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._graphs, self._seen = {}, set()
         if mode in PULL_MODES:
             if len(self.chunks) > PULL_MAX_CHUNKS:
                 raise ValueError(f"pull modes support at most {PULL_MAX_CHUNKS} chunks")
-            if self.role == "prefill":  # both queue halves start free
-                one = torch.ones(2, dtype=torch.int32, device=self.device)
-                _lib.call("kvx_copy_peer", self._pfree(self.flags.ptr, 0), self.device.index,
-                          one.data_ptr(), self.device.index, 8, None)
-                torch.cuda.synchronize(self.device)
+            # every flag starts at 0: both queue halves free for their first
+            # use (parity 0), no chunk published (see _parity)
         stage_here = (self.role == "prefill" and mode in ("pull", "pull_ldg", "copy", "nccl")) or (
             self.role == "decode" and mode in ("push", "copy", "nccl"))
         self.local_payload = None
@@ -305,15 +308,27 @@ class PairChannel:
         """Byte offset of the payload half used by hand-off ``e`` (pull modes)."""
         return (e & 1) * _round_up(self.spec.capacity_bytes)
 
-    # pull-mode doorbells use constant values (0/1) so a hand-off is
-    # graph-capturable: ready[h][c] lives on D (set to 1 by P after K1 of
-    # chunk c into half h, reset to 0 by D after consuming the half);
-    # free[h] lives on P (1 = D is done with half h; P clears it before reuse).
+    # pull-mode doorbells are never reset (no lost wake-ups): hand-off e uses
+    # half h = e & 1 for the u-th time, parity p = u & 1.
+    # ready[h][c] lives on D: P sets it to p ^ 1 once chunk c is in half h.
+    # free[h] lives on P: D sets it to p ^ 1 once it has consumed the half;
+    # P's next use of half h (parity p ^ 1) waits for free[h] == p ^ 1.
+    # Each side also keeps p in its own memory (state[h]); the fused kernels
+    # read it there and flip it, so their CUDA graphs do not depend on p.
+    # The stream-memop paths bake p in (their graphs are keyed by it) and flip
+    # state[h] with a memop.
+    @staticmethod
+    def _parity(e: int) -> int:
+        return ((e - 1) >> 1) & 1
+
     def _pready(self, base: int, h: int, c: int) -> int:
         return base + 4 * (h * PULL_MAX_CHUNKS + c)
 
     def _pfree(self, base: int, h: int) -> int:
         return base + 4 * (2 * PULL_MAX_CHUNKS + h)
+
+    def _pstate(self, h: int) -> int:
+        return self.flags.ptr + 4 * (2 * PULL_MAX_CHUNKS + 2 + h)
 
     def _fused(self, lay) -> bool:
         """One K1 launch ringing device-side doorbells -> one K3-bulk launch
@@ -336,29 +351,32 @@ class PairChannel:
                                self.spec.min_chunk_bytes)
 
     def _send_pull(self, src, lay, e, s, cur, timing, stage_in):
-        h = e & 1
+        h, p = e & 1, self._parity(e)
         chunks, lpc = self._pull_chunks(lay)
-        key = ("send", lay.n_tokens, h, src.k.data_ptr(), src.slots_ptr)
+        key = ("send", lay.n_tokens, h, p, src.k.data_ptr(), src.slots_ptr)
         if self._graph_ok(key, timing, stage_in):
             return self._replay(key, s, cur)
         payload = PackedKV(lay, self.k1_target + self._half(e), self.device)
 
         fused = self._fused(lay) and stage_in is None
+        # the fused graph reads the parity from device state: valid for both
+        keys = [key, key[:3] + (p ^ 1,) + key[4:]] if fused else [key]
 
         def body():
-            wait(self._pfree(self.flags.ptr, h), 1, s)        # D is done with this half
-            signal(self._pfree(self.flags.ptr, h), 0, s)      # claim it
             if fused:
+                # ONE launch: every CTA waits in-kernel for D to be done with
+                # this half, then quantises and rings the chunk doorbells
                 ev = _kernel_events(timing, s, "k1")
                 k, v = src.ptrs(0)
                 c0, sc0, z0 = payload.ptrs(0)
                 _lib.call("kvx_quant_pack_signal", k, v, src.layer_stride, src.slots_ptr,
                           lay.n_layers, lay.n_tokens, lay.n_heads, lay.head_dim, lay.group,
                           lay.bits, c0, sc0, z0, lay.layer_stride, *src.window_args,
-                          self.counters.data_ptr(),
-                          self._pready(self.peer_flags, h, 0), lpc, _stream_ptr(s))
+                          self.counters.data_ptr(), self._pready(self.peer_flags, h, 0), lpc,
+                          self._pfree(self.flags.ptr, h), self._pstate(h), _stream_ptr(s))
                 _kernel_events_end(ev, s)
                 return
+            wait_eq(self._pfree(self.flags.ptr, h), p, s)     # D is done with this half
             for c, (l0, l1) in enumerate(chunks):
                 if stage_in is not None:
                     host, devt = stage_in
@@ -372,9 +390,10 @@ class PairChannel:
                 _kernel_events_end(ev, s)
                 if stage_in is not None:
                     self.x_done[c].record(s)
-                signal(self._pready(self.peer_flags, h, c), 1, s)
+                signal(self._pready(self.peer_flags, h, c), p ^ 1, s)
+            signal(self._pstate(h), p ^ 1, s)
 
-        self._run_or_capture(key, body, s, cur, capturable=timing is None and stage_in is None)
+        self._run_or_capture(keys, body, s, cur, capturable=timing is None and stage_in is None)
         if stage_in is not None:
             cur.wait_stream(self.xfer)
 
@@ -390,13 +409,14 @@ class PairChannel:
         return SendSession(self, src, n_tokens)
 
     def _recv_pull(self, dst, lay, e, s, cur, timing, stage_out):
-        h = e & 1
+        h, p = e & 1, self._parity(e)
         chunks, lpc = self._pull_chunks(lay)
-        key = ("recv", lay.n_tokens, h, dst.slots_ptr, dst.k.data_ptr())
+        key = ("recv", lay.n_tokens, h, p, dst.slots_ptr, dst.k.data_ptr())
         if self._graph_ok(key, timing, stage_out):
             return self._replay(key, s, cur)
         payload = PackedKV(lay, self.k3_source + self._half(e), self.device)
         bulk = self.spec.mode == "pull" and pull_supported(lay)
+        keys = [key, key[:3] + (p ^ 1,) + key[4:]] if bulk else [key]
 
         def body():
             if stage_out is not None:
@@ -407,20 +427,19 @@ class PairChannel:
                 # threads wait in-kernel for each chunk's doorbell
                 ev = _kernel_events(timing, s, "k3")
                 dequant_scatter_layers(payload, dst, 0, lay.n_layers, s,
-                                       ready=(self._pready(self.flags.ptr, h, 0), 1, lpc),
+                                       ready=(self._pready(self.flags.ptr, h, 0), lpc),
                                        done=(self.done_counter.data_ptr(),
-                                             self._pfree(self.peer_flags, h), len(chunks)))
+                                             self._pfree(self.peer_flags, h), self._pstate(h)))
                 _kernel_events_end(ev, s)
             else:
                 for c, (l0, l1) in enumerate(chunks):
-                    wait(self._pready(self.flags.ptr, h, c), 1, s)
+                    wait_eq(self._pready(self.flags.ptr, h, c), p ^ 1, s)
                     ev = _kernel_events(timing, s, "k3")
                     dequant_scatter_layers(payload, dst, l0, l1, s)
                     _kernel_events_end(ev, s)
-            if not bulk:  # (the bulk kernel resets the doorbells and frees the half itself)
-                _lib.call("kvx_memset_async", self._pready(self.flags.ptr, h, 0), 0,
-                          4 * len(chunks), _stream_ptr(s))
-                signal(self._pfree(self.peer_flags, h), 1, s)  # half consumed
+            if not bulk:  # (the bulk kernel frees the half and flips the parity itself)
+                signal(self._pfree(self.peer_flags, h), p ^ 1, s)  # half consumed
+                signal(self._pstate(h), p ^ 1, s)
             if stage_out is not None:
                 (dk, dv), (hk, hv) = stage_out
                 self.x_ready[0].record(s)
@@ -431,7 +450,7 @@ class PairChannel:
                 for c in range(len(chunks)):
                     self.x_done[c].record(self.xfer)
 
-        self._run_or_capture(key, body, s, cur, capturable=timing is None and stage_out is None)
+        self._run_or_capture(keys, body, s, cur, capturable=timing is None and stage_out is None)
         if stage_out is not None:
             cur.wait_stream(self.xfer)
 
@@ -445,10 +464,10 @@ class PairChannel:
         gs, rt = kivi_groups(seqlens, lay.group)
         chunks, _ = pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
                                     self.spec.min_chunk_bytes)
-        return lay, gs, rt, chunks, e & 1
+        return lay, gs, rt, chunks, e & 1, self._parity(e)
 
     def _send_kivi(self, src, n_tokens, seqlens, e):
-        lay, gs, rt, chunks, h = self._kivi_common(n_tokens, seqlens, e)
+        lay, gs, rt, chunks, h, p = self._kivi_common(n_tokens, seqlens, e)
         s, cur = self.stream, torch.cuda.current_stream(self.device)
         s.wait_stream(cur)
         with torch.cuda.stream(s):
@@ -456,8 +475,7 @@ class PairChannel:
             rt_d = torch.from_numpy(rt).to(self.device, non_blocking=False)
         base = self.k1_target + self._half(e)
         offs = (ctypes.c_int64 * 7)(*lay.offsets)
-        wait(self._pfree(self.flags.ptr, h), 1, s)
-        signal(self._pfree(self.flags.ptr, h), 0, s)
+        wait_eq(self._pfree(self.flags.ptr, h), p, s)
         for c, (l0, l1) in enumerate(chunks):
             k, v = src.ptrs(l0)
             _lib.call("kvx_quant_pack_kivi", k, v, src.layer_stride, l1 - l0, n_tokens,
@@ -465,13 +483,14 @@ class PairChannel:
                       gs_d.data_ptr() if len(gs) else None, len(gs),
                       rt_d.data_ptr() if len(rt) else None, len(rt),
                       base + l0 * lay.layer_stride, lay.layer_stride, offs, _stream_ptr(s))
-            signal(self._pready(self.peer_flags, h, c), 1, s)
+            signal(self._pready(self.peer_flags, h, c), p ^ 1, s)
+        signal(self._pstate(h), p ^ 1, s)
         gs_d.record_stream(s)
         rt_d.record_stream(s)
         cur.wait_stream(s)
 
     def _recv_kivi(self, dst, n_tokens, seqlens, e):
-        lay, gs, rt, chunks, h = self._kivi_common(n_tokens, seqlens, e)
+        lay, gs, rt, chunks, h, p = self._kivi_common(n_tokens, seqlens, e)
         s, cur = self.stream, torch.cuda.current_stream(self.device)
         s.wait_stream(cur)
         with torch.cuda.stream(s):
@@ -480,7 +499,7 @@ class PairChannel:
         base = self.k3_source + self._half(e)
         offs = (ctypes.c_int64 * 7)(*lay.offsets)
         for c, (l0, l1) in enumerate(chunks):
-            wait(self._pready(self.flags.ptr, h, c), 1, s)
+            wait_eq(self._pready(self.flags.ptr, h, c), p ^ 1, s)
             k, v = dst.ptrs(l0)
             _lib.call("kvx_dequant_scatter_paged_kivi", base + l0 * lay.layer_stride,
                       lay.layer_stride, offs, dst.slots_ptr,
@@ -488,9 +507,8 @@ class PairChannel:
                       rdst.data_ptr() if rdst.numel() else None, rdst.numel(), l1 - l0,
                       n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
                       dst.layer_stride, _stream_ptr(s))
-        _lib.call("kvx_memset_async", self._pready(self.flags.ptr, h, 0), 0, 4 * len(chunks),
-                  _stream_ptr(s))
-        signal(self._pfree(self.peer_flags, h), 1, s)
+        signal(self._pfree(self.peer_flags, h), p ^ 1, s)
+        signal(self._pstate(h), p ^ 1, s)
         gs_d.record_stream(s)
         rdst.record_stream(s)
         cur.wait_stream(s)
@@ -502,9 +520,11 @@ class PairChannel:
     def _replay(self, key, s, cur):
         self._graphs[key].replay()  # graph launches are ordered on the current stream
 
-    def _run_or_capture(self, key, body, s, cur, capturable: bool):
+    def _run_or_capture(self, keys, body, s, cur, capturable: bool):
+        """Run ``body`` eagerly the first time, capture it the second time
+        (registered under every key in ``keys``), replay it afterwards."""
         s.wait_stream(cur)
-        if self.graphs and capturable and key in self._seen:
+        if self.graphs and capturable and any(k in self._seen for k in keys):
             g = torch.cuda.CUDAGraph()
             try:
                 with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
@@ -514,14 +534,15 @@ class PairChannel:
                 body()
                 cur.wait_stream(s)
                 return
-            self._graphs[key] = g
+            for k in keys:
+                self._graphs[k] = g
             cur.wait_stream(s)
             g.replay()
             return
         else:
             body()
             if capturable:
-                self._seen.add(key)  # eager once (attributes, caches), capture next time
+                self._seen.update(keys)  # eager once (attributes, caches), capture next time
         cur.wait_stream(s)
 
     # flags: slot c = "chunk c of epoch e ready" (written by P into D's flags);
@@ -547,10 +568,13 @@ class PairChannel:
         each layer chunk from pinned host memory first (the host-buffer e2e
         path; H2D of chunk c+1 overlaps K1 of chunk c)."""
         assert self.role == "prefill"
+        if n_tokens == 0:
+            return  # nothing to hand off (both ends skip it: no epoch consumed)
         if timing is None and stage_in is None and self._graphs:
             # fast path: a captured hand-off of this size/half/buffers is ONE
             # graph launch on the caller's stream (no extra stream syncs)
-            g = self._graphs.get(("send", n_tokens, (self.epoch + 1) & 1, src.k.data_ptr(),
+            e = self.epoch + 1
+            g = self._graphs.get(("send", n_tokens, e & 1, self._parity(e), src.k.data_ptr(),
                                   src.slots_ptr))
             if g is not None:
                 self.epoch += 1
@@ -624,8 +648,11 @@ class PairChannel:
         download each finished layer chunk of the cache to pinned host memory
         (D2H of chunk c overlaps K3 of chunk c+1)."""
         assert self.role == "decode"
+        if n_tokens == 0:
+            return
         if timing is None and stage_out is None and self._graphs:
-            g = self._graphs.get(("recv", n_tokens, (self.epoch + 1) & 1, dst.slots_ptr,
+            e = self.epoch + 1
+            g = self._graphs.get(("recv", n_tokens, e & 1, self._parity(e), dst.slots_ptr,
                                   dst.k.data_ptr()))
             if g is not None:
                 self.epoch += 1
@@ -731,14 +758,13 @@ class SendSession:
         self.ch, self.src = ch, src
         self.lay = ch.spec.layout(n_tokens)
         ch.epoch += 1
-        self.h = ch.epoch & 1
+        self.h, self.p = ch.epoch & 1, ch._parity(ch.epoch)
         self.chunks, _ = ch._pull_chunks(self.lay)
         self.payload = PackedKV(self.lay, ch.k1_target + ch._half(ch.epoch), ch.device)
         self.next = 0
         s = ch.stream
         s.wait_stream(torch.cuda.current_stream(ch.device))
-        wait(ch._pfree(ch.flags.ptr, self.h), 1, s)    # decode side done with this half
-        signal(ch._pfree(ch.flags.ptr, self.h), 0, s)  # claim it
+        wait_eq(ch._pfree(ch.flags.ptr, self.h), self.p, s)  # decode side done with this half
 
     def layers_ready(self, n_layers_done: int) -> None:
         ch, s = self.ch, self.ch.stream
@@ -746,11 +772,12 @@ class SendSession:
         while self.next < len(self.chunks) and self.chunks[self.next][1] <= n_layers_done:
             l0, l1 = self.chunks[self.next]
             quant_pack_layers(self.src, self.payload, l0, l1, s)
-            signal(ch._pready(ch.peer_flags, self.h, self.next), 1, s)
+            signal(ch._pready(ch.peer_flags, self.h, self.next), self.p ^ 1, s)
             self.next += 1
 
     def close(self) -> None:
         self.layers_ready(self.lay.n_layers)
+        signal(self.ch._pstate(self.h), self.p ^ 1, self.ch.stream)
         torch.cuda.current_stream(self.ch.device).wait_stream(self.ch.stream)
 
 

@@ -29,7 +29,10 @@ def main():
     # several hand-offs of varying length; repeated lengths exercise the CUDA
     # graph capture (2nd time) and replay (3rd time) of the pull modes, on
     # both halves of the double-buffered queue
-    seq = (Tmax, 77, Tmax, 77, Tmax, 77, 130, Tmax)
+    # (flags are per (queue half, parity): the same size recurs on the same
+    # (half, parity) every 4th hand-off -- eager, capture, replay -- and an
+    # empty hand-off in between must consume no epoch on either side)
+    seq = (Tmax, 77) * 3 + (0,) + (Tmax, 77) * 3 + (130, Tmax)
     for mode in modes:
         for bits in (4, 8, 16):
             # "pull_hostdb": pull with host-enqueued per-chunk doorbells instead
@@ -47,6 +50,12 @@ def main():
                 vc = torch.zeros_like(kc)
             for epoch, T in enumerate(seq):
                 seed = 1000 * ch.pair + 10 * epoch + bits
+                if T == 0:
+                    if ch.role == "prefill":
+                        ch.send(KVPlanes.dense(kv_cap), 0)
+                    else:
+                        ch.recv(KVPlanes.paged(kc, vc, slots_buf[:0]), 0)
+                    continue
                 if ch.role == "prefill":
                     kv_cap[:, :, :T].copy_(torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=seed)))
                     ch.send(KVPlanes.dense(kv_cap), T)

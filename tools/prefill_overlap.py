@@ -26,7 +26,7 @@ import torch.distributed as dist  # noqa: E402
 
 import bench as B  # noqa: E402
 from paper_2502_09334_b200.datapath import KVPlanes  # noqa: E402
-from paper_2502_09334_b200.transport import ChannelSpec, PairChannel, exchange, wait  # noqa: E402
+from paper_2502_09334_b200.transport import ChannelSpec, PairChannel, exchange, wait_eq  # noqa: E402
 
 
 def main():
@@ -76,10 +76,11 @@ def main():
                     sess.close()
                 else:
                     ch.send(planes, T)
-                # the decode side sets free[h] = 1 when its K3 has consumed the half
-                h = ch.epoch & 1
+                # the decode side sets free[h] = parity ^ 1 when its K3 has
+                # consumed the half
+                h, p = ch.epoch & 1, ch._parity(ch.epoch)
                 cur = torch.cuda.current_stream()
-                wait(ch._pfree(ch.flags.ptr, h), 1, cur)
+                wait_eq(ch._pfree(ch.flags.ptr, h), p ^ 1, cur)
                 e_done.record()
                 torch.cuda.synchronize()
                 if rep:
