@@ -114,3 +114,14 @@ def test_no_cpu_fallback(monkeypatch, tmp_path):
     for f in glob.glob(os.path.join(pkg, "*.py")):
         src = open(f).read()
         assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), f
+
+
+def test_integration_doc_bindings_match():
+    """The ctypes stub INTEGRATION.md shows a maintainer matches the real ABI."""
+    src = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    m = {"P": ctypes.c_void_p, "I": ctypes.c_int, "I64": ctypes.c_int64, "U32": ctypes.c_uint32}
+    found = re.findall(r"kvx\.(kvx_\w+)\.argtypes = \[([^\]]*)\]", src)
+    assert len(found) >= 4
+    for name, body in found:
+        got = [m[x.strip()] for x in body.replace("\n", " ").split(",")]
+        assert got == list(_lib.SIGNATURES[name]), name
