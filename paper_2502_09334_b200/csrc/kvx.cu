@@ -762,6 +762,20 @@ int kvx_stream_wait(const void* flag, uint32_t value, void* stream) {
   return r == CUDA_SUCCESS ? KVX_OK : KVX_ERR_UNSUPPORTED;
 }
 
+#ifdef KVX_TRACE
+// A/B trace builds only (not part of include/kvx.h): copy the timeline ring
+// of kernel kind 0 (K1-signal) or 1 (K3-bulk) to host memory.
+int kvx_trace_read(int kind, void* host_out, unsigned int* n_out) {
+  if (kind < 0 || kind > 1 || !host_out || !n_out) return KVX_ERR_INVALID_ARG;
+  unsigned int n[2];
+  cudaError_t e = cudaMemcpyFromSymbol(n, kvx::g_trace_n, sizeof(n));
+  if (e != cudaSuccess) return e;
+  *n_out = n[kind];
+  return cudaMemcpyFromSymbol(host_out, kvx::g_trace, sizeof(kvx::g_trace[0]),
+                              kind * sizeof(kvx::g_trace[0]));
+}
+#endif
+
 int kvx_stream_wait_eq(const void* flag, uint32_t value, void* stream) {
   resolve_driver();
   if (g_drv_status) return g_drv_status;

@@ -368,6 +368,24 @@ __device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)
 // decode side layer by layer, no per-chunk launches or host round trips.
 constexpr int kMaxSignalChunks = 64;  // = transport.PULL_MAX_CHUNKS
 
+// Hand-off timeline tracing (A/B builds only: -DKVX_TRACE, see
+// tools/handoff_trace.py).  Per launch of K1-signal (kind 0) and K3-bulk with
+// completion (kind 1): %globaltimer stamps of the key protocol events.
+#ifdef KVX_TRACE
+constexpr int kTraceLaunches = 4096;
+__device__ unsigned long long g_trace[2][kTraceLaunches][4];
+__device__ unsigned int g_trace_n[2];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define KVX_TRACE_STAMP(kind, launch, slot) \
+  (g_trace[kind][(launch) % kTraceLaunches][slot] = gtimer())
+#else
+#define KVX_TRACE_STAMP(kind, launch, slot) ((void)0)
+#endif
+
 struct SignalGeo {
   // [kMaxSignalChunks] chunk arrivals + [1] CTA exits; zero at launch, and
   // reset in-kernel by the last arrival, so zero again after every launch
@@ -435,10 +453,14 @@ __device__ __forceinline__ void chunk_arrive(const SignalGeo& sig, uint32_t* cta
       __threadfence();
       if (atomicAdd(sig.counters + c, 1u) + 1 == ctas_owning(a, b, n_warps)) {
         sig.counters[c] = 0u;  // every owner has arrived: ready for the next launch
-        __threadfence_system();
+        // st.release.sys is cumulative over the payload stores this thread has
+        // observed through the arrival atomics (it carries its own MEMBAR.SYS)
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags + c),
                      "r"(ready_value)
                      : "memory");
+#ifdef KVX_TRACE
+        if ((c + 1) * sig.items_per_chunk >= n_items) KVX_TRACE_STAMP(0, g_trace_n[0], 2);
+#endif
       }
     }
   }
@@ -458,12 +480,17 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
   const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
   __shared__ uint32_t cta_cnt[kMaxSignalChunks];
   __shared__ uint32_t s_parity;
+#ifdef KVX_TRACE
+  const uint32_t trace_id = g_trace_n[0];
+  if (sig.peer_flags && blockIdx.x == 0 && threadIdx.x == 0) KVX_TRACE_STAMP(0, trace_id, 0);
+#endif
   if (sig.peer_flags) {
     for (int i = threadIdx.x; i < kMaxSignalChunks; i += blockDim.x) cta_cnt[i] = 0u;
     if (threadIdx.x == 0) {
       const uint32_t p = sig.parity ? *sig.parity : 0u;
       if (sig.free_flag) spin_until_eq(sig.free_flag, p);  // decode side done with the half
       s_parity = p;
+      if (blockIdx.x == 0) KVX_TRACE_STAMP(0, trace_id, 1);
     }
     __syncthreads();
   }
@@ -511,6 +538,10 @@ k1_done:
     if (threadIdx.x == 0 && atomicAdd(sig.counters + kMaxSignalChunks, 1u) == gridDim.x - 1) {
       sig.counters[kMaxSignalChunks] = 0u;
       *sig.parity = s_parity ^ 1u;
+#ifdef KVX_TRACE
+      KVX_TRACE_STAMP(0, trace_id, 3);
+      g_trace_n[0] = trace_id + 1;
+#endif
     }
   }
 }
@@ -807,6 +838,10 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
   const int64_t two_t = int64_t(g.planes) * g.n_tokens;  // payload rows per layer
 
   const uint32_t par = bg.parity ? *bg.parity : 0u;  // read by every CTA before the flip
+#ifdef KVX_TRACE
+  const uint32_t trace_id = g_trace_n[1];
+  if (bg.done_counter && blockIdx.x == 0 && threadIdx.x == 0) KVX_TRACE_STAMP(1, trace_id, 0);
+#endif
   if (warp == CONSUMERS) {  // ---- producer: one elected thread
     if (lane == 0) {
       uint32_t k = 0;
@@ -820,6 +855,9 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
           if (c > ready_chunk) {
             wait_ready(bg.ready + c, par ^ 1u);
             ready_chunk = c;
+#ifdef KVX_TRACE
+            if (bg.done_counter && blockIdx.x == 0 && c == 0) KVX_TRACE_STAMP(1, trace_id, 1);
+#endif
           }
         }
         const int64_t r0 = int64_t(sp - layer * bg.spans_per_layer) * bg.rows_per_span;
@@ -888,15 +926,25 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
   }  // consumers
 
   if (bg.done_counter) {
+    // The free flag only has to say "every read of the peer half is
+    // complete": each bulk read completed (its mbarrier phase) before the
+    // consumers used the bytes, and every CTA counts itself done after that.
+    // The cache stores need no ordering against the flag (the prefill side
+    // never reads them), so neither a per-CTA fence nor a system-scope release
+    // is needed -- they cost ~1 us and ~3.5 us on the critical path of every
+    // hand-off (tools/handoff_trace.py).
     __syncthreads();  // this CTA has consumed every span it owned
     if (threadIdx.x == 0) {
-      __threadfence();
       if (atomicAdd(bg.done_counter, 1u) == gridDim.x - 1) {  // last CTA of the launch
         *bg.done_counter = 0u;
         if (bg.parity) *bg.parity = par ^ 1u;
-        __threadfence_system();
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(bg.peer_free), "r"(par ^ 1u)
+        KVX_TRACE_STAMP(1, trace_id, 2);
+        asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(bg.peer_free), "r"(par ^ 1u)
                      : "memory");
+#ifdef KVX_TRACE
+        KVX_TRACE_STAMP(1, trace_id, 3);
+        g_trace_n[1] = trace_id + 1;
+#endif
       }
     }
   }
