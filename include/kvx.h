@@ -195,6 +195,17 @@ int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_st
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
                                    int64_t dst_layer_stride, void* stream);
+/* Same contract, for a payload read over NVLink: the per-channel K groups and
+ * the per-token V rows are staged into shared memory with cp.async.bulk
+ * (TMA) before they are dequantised -- the kivi format's pull transport.
+ * Shapes that cannot be bulk-staged fall back to the per-lane kernels. */
+int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_stride,
+                                        const int64_t* seg_offsets, const int64_t* dst_slots,
+                                        const int64_t* group_starts, int64_t n_groups,
+                                        const int64_t* residual_dst_slots, int64_t n_residual,
+                                        int64_t n_layers, int64_t n_tokens, int n_heads,
+                                        int head_dim, int group, int bits, void* k_cache,
+                                        void* v_cache, int64_t dst_layer_stride, void* stream);
 
 /* Packed payload sizes in bytes for n_rows rows (codes, scale, zero). */
 int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t* codes_bytes,

@@ -357,6 +357,45 @@ cudaError_t launch_kchan_dequant(const kvx::KchanGeo& kg, const int64_t* slots, 
   return cudaGetLastError();
 }
 
+// Bulk-staged kchan dequant (payload read over NVLink).  *ok = false when the
+// shape cannot be staged (caller falls back to the per-lane kernel).
+template <int BITS, int G>
+cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, void* kc,
+                              int64_t dst_ls_b, cudaStream_t s, bool* ok) {
+  *ok = false;
+  constexpr int kStages = 4;
+  kvx::KchanBulk kb;
+  kb.slab = 16384 / (G * BITS / 8);  // 16 KB of codes per stage: 256..1024 channels
+  if (kg.row_elems % 32 || !aligned(kg.codes, 16) || !aligned(kg.scale, 16) ||
+      !aligned(kg.zero, 16) || kg.payload_ls % 16)
+    return cudaSuccess;
+  kb.slabs = (kg.row_elems + kb.slab - 1) / kb.slab;
+  kb.n_spans = kg.n_layers * kg.n_groups * kb.slabs;
+  kb.stage_bytes = G * kb.slab * BITS / 8 + 4 * kb.slab;
+  const int smem = kStages * kb.stage_bytes;
+  auto k = kvx::pull_kchan_kernel<BITS, G, kStages>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool attr_set[kMaxDev] = {false};
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  if (!attr_set[dev]) {
+    cudaError_t attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr != cudaSuccess) return attr;
+    attr_set[dev] = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBulkThreads, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  cudaGetLastError();
+  int64_t grid = int64_t(sm_count(dev)) * per_sm;
+  if (grid > kb.n_spans) grid = kb.n_spans;
+  if (grid < 1) return cudaSuccess;
+  *ok = true;
+  k<<<unsigned(grid), kBulkThreads, smem, s>>>(kg, kb, slots, static_cast<char*>(kc), dst_ls_b);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 extern "C" {
@@ -610,13 +649,13 @@ int kvx_quant_pack_kivi(const void* k_src, const void* v_src, int64_t src_layer_
   return e;
 }
 
-int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_stride,
-                                   const int64_t* seg_offsets, const int64_t* dst_slots,
-                                   const int64_t* group_starts, int64_t n_groups,
-                                   const int64_t* residual_dst_slots, int64_t n_residual,
-                                   int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
-                                   int group, int bits, void* k_cache, void* v_cache,
-                                   int64_t dst_layer_stride, void* stream) {
+static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
+                        const int64_t* seg_offsets, const int64_t* dst_slots,
+                        const int64_t* group_starts, int64_t n_groups,
+                        const int64_t* residual_dst_slots, int64_t n_residual, int64_t n_layers,
+                        int64_t n_tokens, int n_heads, int head_dim, int group, int bits,
+                        void* k_cache, void* v_cache, int64_t dst_layer_stride, void* stream,
+                        bool bulk) {
   int rc = kivi_check(head_dim, group, bits);
   if (rc) return rc;
   if (n_layers < 0 || n_tokens < 0 || n_heads <= 0 || n_groups < 0 || n_residual < 0 ||
@@ -645,13 +684,25 @@ int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_st
     kg.zero = const_cast<char*>(base + seg_offsets[2]);
     kg.payload_ls = payload_layer_stride;
     const int64_t dls = dst_layer_stride * 2;
-    if (bits == 4)
-      e = group == 32 ? launch_kchan_dequant<4, 32>(kg, dst_slots, k_cache, dls, s)
-                      : launch_kchan_dequant<4, 64>(kg, dst_slots, k_cache, dls, s);
-    else
-      e = group == 32 ? launch_kchan_dequant<8, 32>(kg, dst_slots, k_cache, dls, s)
-                      : launch_kchan_dequant<8, 64>(kg, dst_slots, k_cache, dls, s);
-    if (e != cudaSuccess) return e;
+    bool ok = false;
+    if (bulk) {
+      if (bits == 4)
+        e = group == 32 ? launch_kchan_pull<4, 32>(kg, dst_slots, k_cache, dls, s, &ok)
+                        : launch_kchan_pull<4, 64>(kg, dst_slots, k_cache, dls, s, &ok);
+      else
+        e = group == 32 ? launch_kchan_pull<8, 32>(kg, dst_slots, k_cache, dls, s, &ok)
+                        : launch_kchan_pull<8, 64>(kg, dst_slots, k_cache, dls, s, &ok);
+      if (e != cudaSuccess) return e;
+    }
+    if (!ok) {
+      if (bits == 4)
+        e = group == 32 ? launch_kchan_dequant<4, 32>(kg, dst_slots, k_cache, dls, s)
+                        : launch_kchan_dequant<4, 64>(kg, dst_slots, k_cache, dls, s);
+      else
+        e = group == 32 ? launch_kchan_dequant<8, 32>(kg, dst_slots, k_cache, dls, s)
+                        : launch_kchan_dequant<8, 64>(kg, dst_slots, k_cache, dls, s);
+      if (e != cudaSuccess) return e;
+    }
   }
   if (n_residual) {
     kvx::Geo g;
@@ -668,12 +719,42 @@ int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_st
     rc = make_geo(g, v_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
                   head_dim, group, bits, payload_layer_stride, 1, 1);
     if (rc) return rc;
-    e = bits == 4 ? dispatch_dequant<4>(group, g, base + seg_offsets[4], base + seg_offsets[5],
-                                        base + seg_offsets[6], s)
-                  : dispatch_dequant<8>(group, g, base + seg_offsets[4], base + seg_offsets[5],
-                                        base + seg_offsets[6], s);
+    const char *vc = base + seg_offsets[4], *vs = base + seg_offsets[5], *vz = base + seg_offsets[6];
+    bool ok = false;
+    if (bulk && aligned(v_cache, 32) && g.plane_row_b % 32 == 0) {
+      e = bits == 4 ? dispatch_pull<4>(group, g, vc, vs, vz, s, &ok, nullptr, 1, PullDone())
+                    : dispatch_pull<8>(group, g, vc, vs, vz, s, &ok, nullptr, 1, PullDone());
+      if (e != cudaSuccess) return e;
+    }
+    if (!ok)
+      e = bits == 4 ? dispatch_dequant<4>(group, g, vc, vs, vz, s)
+                    : dispatch_dequant<8>(group, g, vc, vs, vz, s);
   }
   return e;
+}
+
+int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_stride,
+                                   const int64_t* seg_offsets, const int64_t* dst_slots,
+                                   const int64_t* group_starts, int64_t n_groups,
+                                   const int64_t* residual_dst_slots, int64_t n_residual,
+                                   int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                                   int group, int bits, void* k_cache, void* v_cache,
+                                   int64_t dst_layer_stride, void* stream) {
+  return kivi_dequant(payload, payload_layer_stride, seg_offsets, dst_slots, group_starts,
+                      n_groups, residual_dst_slots, n_residual, n_layers, n_tokens, n_heads,
+                      head_dim, group, bits, k_cache, v_cache, dst_layer_stride, stream, false);
+}
+
+int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_stride,
+                                        const int64_t* seg_offsets, const int64_t* dst_slots,
+                                        const int64_t* group_starts, int64_t n_groups,
+                                        const int64_t* residual_dst_slots, int64_t n_residual,
+                                        int64_t n_layers, int64_t n_tokens, int n_heads,
+                                        int head_dim, int group, int bits, void* k_cache,
+                                        void* v_cache, int64_t dst_layer_stride, void* stream) {
+  return kivi_dequant(payload, payload_layer_stride, seg_offsets, dst_slots, group_starts,
+                      n_groups, residual_dst_slots, n_residual, n_layers, n_tokens, n_heads,
+                      head_dim, group, bits, k_cache, v_cache, dst_layer_stride, stream, true);
 }
 
 // ---- transport -------------------------------------------------------------

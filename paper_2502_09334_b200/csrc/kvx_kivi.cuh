@@ -243,4 +243,99 @@ __global__ void __launch_bounds__(256) dequant_kchan_kernel(KchanGeo g, const in
   }
 }
 
+// Bulk-staged variant of dequant_kchan_kernel for a payload read over NVLink
+// (the kivi format's pull transport).  Span = (layer, group k, slab of S
+// channels): one producer thread stages the group's G code-row slices
+// (S*BITS/8 bytes each) plus the slab's S scales and S zeros with
+// cp.async.bulk into a STAGES-deep shared-memory ring; 8 consumer warps
+// dequantise from shared memory (each thread keeps one 32-channel chunk's
+// scales/zeros in registers across the rows it walks) into the paged cache.
+struct KchanBulk {
+  int slab;          // S channels per span: 32 * 2^n, S/32 divides 256
+  int slabs;         // ceil(row_elems / S)
+  int64_t n_spans;   // n_layers * n_groups * slabs
+  int stage_bytes;   // G * S * BITS/8 + 4 * S
+};
+
+template <int BITS, int G, int STAGES>
+__global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBulk kb,
+                                                            const int64_t* __restrict__ dst_slots,
+                                                            char* k_cache, int64_t dst_ls_b) {
+  constexpr int CONSUMERS = 8;
+  constexpr int CB = 32 * BITS / 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int S = kb.slab;
+  const int code_slice = S * BITS / 8;  // bytes of one row's slab slice in smem
+  if (warp == CONSUMERS) {  // ---- producer: one elected thread
+    if (lane == 0) {
+      uint32_t k = 0;
+      for (int64_t sp = blockIdx.x; sp < kb.n_spans; sp += gridDim.x, ++k) {
+        const int st = k % STAGES;
+        if (k >= STAGES) mbar_wait(&empty[st], ((k / STAGES) & 1) ^ 1);
+        const int64_t lg = sp / kb.slabs;
+        const int c0 = int(sp - lg * kb.slabs) * S;
+        const int64_t layer = lg / g.n_groups, grp = lg - layer * g.n_groups;
+        const int ns = min(S, g.row_elems - c0);
+        const uint32_t rb = uint32_t(ns) * BITS / 8, mb = uint32_t(ns) * 2;
+        mbar_expect_tx(&full[st], G * rb + 2 * mb);
+        uint8_t* buf = smem + st * kb.stage_bytes;
+        const char* lc = g.codes + layer * g.payload_ls + int64_t(c0) * BITS / 8;
+        for (int j = 0; j < G; ++j)
+          bulk_g2s(buf + j * code_slice, lc + (grp * G + j) * int64_t(g.row_elems) * BITS / 8, rb,
+                   &full[st]);
+        const int64_t meta = (grp * g.row_elems + c0) * 2;
+        bulk_g2s(buf + G * code_slice, g.scale + layer * g.payload_ls + meta, mb, &full[st]);
+        bulk_g2s(buf + G * code_slice + 2 * S, g.zero + layer * g.payload_ls + meta, mb,
+                 &full[st]);
+      }
+    }
+  } else {  // ---- consumers
+    const int nck = S / 32;           // 32-channel chunks per full slab
+    const int c = threadIdx.x % nck;  // this thread's chunk (fixed across spans)
+    const int jstep = (CONSUMERS * 32) / nck;
+    uint32_t k = 0;
+    for (int64_t sp = blockIdx.x; sp < kb.n_spans; sp += gridDim.x, ++k) {
+      const int st = k % STAGES;
+      const int64_t lg = sp / kb.slabs;
+      const int c0 = int(sp - lg * kb.slabs) * S;
+      const int64_t layer = lg / g.n_groups, grp = lg - layer * g.n_groups;
+      const int ns = min(S, g.row_elems - c0);
+      const uint8_t* buf = smem + st * kb.stage_bytes;
+      mbar_wait(&full[st], (k / STAGES) & 1);
+      if (c * 32 < ns) {
+        const uint4* sv = reinterpret_cast<const uint4*>(buf + G * code_slice + c * 64);
+        const uint4* zv = reinterpret_cast<const uint4*>(buf + G * code_slice + 2 * S + c * 64);
+        uint32_t sw[16], zw[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 a = sv[i], b = zv[i];
+          sw[4 * i] = a.x; sw[4 * i + 1] = a.y; sw[4 * i + 2] = a.z; sw[4 * i + 3] = a.w;
+          zw[4 * i] = b.x; zw[4 * i + 1] = b.y; zw[4 * i + 2] = b.z; zw[4 * i + 3] = b.w;
+        }
+        const int64_t t0 = __ldg(g.group_starts + grp);
+        char* kplane = k_cache + layer * dst_ls_b + int64_t(c0 + c * 32) * 2;
+        for (int j = threadIdx.x / nck; j < G; j += jstep) {
+          const int64_t pos = __ldg(dst_slots + t0 + j);
+          if (pos < 0) continue;
+          uint32_t cw[BITS];
+          kchan_load_codes<BITS>(reinterpret_cast<const char*>(buf + j * code_slice + c * CB), cw);
+          kchan_dequant_store<BITS>(cw, sw, zw, kplane + pos * int64_t(g.row_elems) * 2);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+}
+
 }  // namespace kvx

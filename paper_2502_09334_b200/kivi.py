@@ -146,8 +146,10 @@ def compress_kivi(kv: torch.Tensor, prec=KvPrecision(4), group_size: int = 32, s
 
 
 def decompress_kivi_into_paged(packed: PackedKiviKV, k_cache: torch.Tensor, v_cache: torch.Tensor,
-                               slot_mapping: torch.Tensor, stream=None) -> None:
-    """Dequantise a kivi payload and scatter it into the paged cache."""
+                               slot_mapping: torch.Tensor, stream=None, bulk: bool = False) -> None:
+    """Dequantise a kivi payload and scatter it into the paged cache.
+    ``bulk``: stage the payload through shared memory with TMA bulk copies
+    (the variant for a payload read over NVLink)."""
     dst = KVPlanes.paged(k_cache, v_cache, slot_mapping)
     lay = packed.layout
     if slot_mapping.numel() != lay.n_tokens:
@@ -157,7 +159,8 @@ def decompress_kivi_into_paged(packed: PackedKiviKV, k_cache: torch.Tensor, v_ca
     gs = packed.group_starts.to(k_cache.device)
     rdst = dst.slots[packed.residual_tokens.to(k_cache.device)].contiguous()
     k, v = dst.ptrs(0)
-    _lib.call("kvx_dequant_scatter_paged_kivi", packed.base, lay.layer_stride, _offsets_arg(lay),
+    fn = "kvx_pull_dequant_scatter_paged_kivi" if bulk else "kvx_dequant_scatter_paged_kivi"
+    _lib.call(fn, packed.base, lay.layer_stride, _offsets_arg(lay),
               dst.slots_ptr, gs.data_ptr() if gs.numel() else None, gs.numel(),
               rdst.data_ptr() if rdst.numel() else None, rdst.numel(), lay.n_layers,
               lay.n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,

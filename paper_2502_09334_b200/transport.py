@@ -454,7 +454,7 @@ class PairChannel:
         if stage_out is not None:
             cur.wait_stream(self.xfer)
 
-    # ---- kivi format over the pull queue (per-chunk doorbells, LDG kernels) ---
+    # ---- kivi format over the pull queue (per-chunk doorbells) ----------------
     def _kivi_common(self, n_tokens, seqlens, e):
         from .kivi import kivi_groups
         seqlens = tuple(int(n) for n in (seqlens if seqlens is not None else (n_tokens,)))
@@ -498,10 +498,13 @@ class PairChannel:
             rdst = dst.slots[torch.from_numpy(rt).to(self.device)].contiguous()
         base = self.k3_source + self._half(e)
         offs = (ctypes.c_int64 * 7)(*lay.offsets)
+        # "pull": TMA bulk-staged kernels; "pull_ldg": per-lane peer loads
+        fn = ("kvx_pull_dequant_scatter_paged_kivi" if self.spec.mode == "pull"
+              else "kvx_dequant_scatter_paged_kivi")
         for c, (l0, l1) in enumerate(chunks):
             wait_eq(self._pready(self.flags.ptr, h, c), p ^ 1, s)
             k, v = dst.ptrs(l0)
-            _lib.call("kvx_dequant_scatter_paged_kivi", base + l0 * lay.layer_stride,
+            _lib.call(fn, base + l0 * lay.layer_stride,
                       lay.layer_stride, offs, dst.slots_ptr,
                       gs_d.data_ptr() if len(gs) else None, len(gs),
                       rdst.data_ptr() if rdst.numel() else None, rdst.numel(), l1 - l0,

@@ -24,7 +24,8 @@ CASES = [  # (L, H, D, seqlens)
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("bits", [4, 8])
 @pytest.mark.parametrize("group", [32, 64])
-def test_kivi_bit_exact(cuda, case, bits, group):
+@pytest.mark.parametrize("bulk", [False, True])  # per-lane kernels / TMA bulk-staged (pull)
+def test_kivi_bit_exact(cuda, case, bits, group, bulk):
     torch = cuda
     from paper_2502_09334_b200.kivi import compress_kivi, decompress_kivi_into_paged
     L, H, D, seq = case
@@ -46,9 +47,13 @@ def test_kivi_bit_exact(cuda, case, bits, group):
     slots = O.synthetic_slots(T, bs, nb, seed=T)
     kc = torch.full((L, nb, bs, H, D), -5.0, dtype=torch.float16, device="cuda")
     vc = torch.full_like(kc, -5.0)
-    decompress_kivi_into_paged(p, kc, vc, torch.from_numpy(slots).cuda())
+    sl = slots.copy()
+    sl[::7] = -1  # padding tokens are skipped by every kernel
+    decompress_kivi_into_paged(p, kc, vc, torch.from_numpy(sl).cuda(), bulk=bulk)
     torch.cuda.synchronize()
     K, V = O.unpack_dequant_kivi(want, bits, group, seq, H, D)
+    keep = sl >= 0
+    K, V, slots = K[:, keep], V[:, keep], slots[keep]
     okc = np.full((L, nb * bs, H, D), -5.0, np.float16); ovc = okc.copy()
     okc[:, slots] = K; ovc[:, slots] = V
     assert np.array_equal(h16(kc.cpu().numpy().reshape(okc.shape)), h16(okc))
