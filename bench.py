@@ -172,9 +172,11 @@ def cpu_reference(workload: str, bits: int, group: int, budget_s: float | None =
     vc = np.zeros_like(kc)
     layers = 0
     elapsed = 0.0
-    limit = max_layers or L
+    # cycle over the workload's layers until the time budget (a bounded sample
+    # of about 10-30 s of CPU work), or exactly max_layers layers
+    limit = max_layers or (L if budget_s is None else 1 << 30)
     while layers < limit:
-        kv = _cpu_layer(workload, layers, T, H, D)
+        kv = _cpu_layer(workload, layers % L, T, H, D)
         t0 = time.perf_counter()
         c, sc, z = C.quant_pack(kv.reshape(-1, D), bits, group)
         C.dequant_scatter_paged(c, sc, z, slots, 1, T, H, D, group, bits, kc, vc)
@@ -184,7 +186,8 @@ def cpu_reference(workload: str, bits: int, group: int, budget_s: float | None =
             break
     fp16_bytes = layers * 2 * T * H * D * 2
     return dict(value=fp16_bytes / elapsed / 1e9, unit=UNIT, cores=C.threads(), kind="port",
-                sample=f"{layers}/{L} layers of {workload} ({fp16_bytes / 1e9:.2f} GB fp16), "
+                sample=f"{layers} layers ({layers / L:.2f} passes over the {L}) of {workload} "
+                       f"({fp16_bytes / 1e9:.2f} GB fp16), "
                        f"oracle/kvq_oracle.c quant+pack+dequant+paged-scatter, "
                        f"{C.threads()} OpenMP threads, {elapsed:.2f} s")
 
