@@ -125,3 +125,29 @@ def test_integration_doc_bindings_match():
     for name, body in found:
         got = [m[x.strip()] for x in body.replace("\n", " ").split(",")]
         assert got == list(_lib.SIGNATURES[name]), name
+
+
+def test_fused_and_kivi_entry_points_validate(lib):
+    """The transport's fused kernels and the kivi pull variant reject bad
+    arguments before touching CUDA (no GPU here)."""
+    E = _lib.KVX_ERR_INVALID_ARG
+    # K1 with doorbells: 16-bit has no doorbell variant; misaligned counters
+    assert lib.kvx_quant_pack_signal(256, 256, 0, None, 1, 1, 1, 128, 128, 16, 256, 256, 256, 0,
+                                     0, 0, 256, 256, 1, None, None, None) == E
+    assert lib.kvx_quant_pack_signal(256, 256, 0, None, 1, 1, 1, 128, 128, 4, 256, 256, 256, 0,
+                                     0, 0, 258, 256, 1, None, None, None) == E
+    # K3-bulk: a parity state needs the in-kernel completion (done counter)
+    assert lib.kvx_pull_dequant_scatter_paged(256, 256, 256, 0, None, 1, 1, 1, 128, 128, 4, 256,
+                                              256, 0, 0, 0, 256, 1, None, None, 512,
+                                              None) == E
+    offs = (ctypes.c_int64 * 7)(*([0] * 7))
+    for fn in ("kvx_dequant_scatter_paged_kivi", "kvx_pull_dequant_scatter_paged_kivi"):
+        f = getattr(lib, fn)
+        # kivi: bits 2 and group 128 are not kivi formats
+        assert f(256, 256, offs, 256, None, 0, None, 0, 1, 1, 1, 128, 32, 2, 256, 256, 0,
+                 None) == E
+        assert f(256, 256, offs, 256, None, 0, None, 0, 1, 1, 1, 128, 128, 4, 256, 256, 0,
+                 None) == E
+        # group counts must add up to the token count
+        assert f(256, 256, offs, 256, 256, 1, None, 0, 1, 5, 1, 128, 32, 4, 256, 256, 0,
+                 None) == E
