@@ -350,15 +350,25 @@ class PairChannel:
         return pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
                                self.spec.min_chunk_bytes)
 
+    def _wait_half_free(self, h: int, p: int, stream) -> None:
+        """Hold the prefill side in the GPU front-end (a stream memop, no SMs
+        held) until the decode side has released queue half h.  The fused K1
+        re-checks in-kernel, but it must not sit spinning on every SM of a
+        prefill GPU that has compute to run while the decode side lags."""
+        wait_eq(self._pfree(self.flags.ptr, h), p, stream)
+
     def _send_pull(self, src, lay, e, s, cur, timing, stage_in):
         h, p = e & 1, self._parity(e)
         chunks, lpc = self._pull_chunks(lay)
         key = ("send", lay.n_tokens, h, p, src.k.data_ptr(), src.slots_ptr)
         if self._graph_ok(key, timing, stage_in):
+            self._wait_half_free(h, p, cur)
             return self._replay(key, s, cur)
         payload = PackedKV(lay, self.k1_target + self._half(e), self.device)
 
         fused = self._fused(lay) and stage_in is None
+        if fused:
+            self._wait_half_free(h, p, cur)  # outside the graph: it depends on p
         # the fused graph reads the parity from device state: valid for both
         keys = [key, key[:3] + (p ^ 1,) + key[4:]] if fused else [key]
 
@@ -577,10 +587,11 @@ class PairChannel:
             # fast path: a captured hand-off of this size/half/buffers is ONE
             # graph launch on the caller's stream (no extra stream syncs)
             e = self.epoch + 1
-            g = self._graphs.get(("send", n_tokens, e & 1, self._parity(e), src.k.data_ptr(),
-                                  src.slots_ptr))
+            h, p = e & 1, self._parity(e)
+            g = self._graphs.get(("send", n_tokens, h, p, src.k.data_ptr(), src.slots_ptr))
             if g is not None:
                 self.epoch += 1
+                self._wait_half_free(h, p, torch.cuda.current_stream(self.device))
                 g.replay()
                 return
         if self.spec.format == "kivi":
