@@ -400,7 +400,8 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
     mode = args.mode
     n_chunks = args.chunks or 8
     spec = ChannelSpec(L, T, H, D, args.bits, args.group, n_chunks, mode,
-                       format=getattr(args, "format", "default"))
+                       format=getattr(args, "format", "default"),
+                       queue_depth=getattr(args, "queue_depth", 2))
     ch = PairChannel(spec, rank, world, control_group=ctrl, graphs=not args.no_graphs)
     lay = spec.layout(T)
     # per step token counts (fixed workload, or the trace's batches)
@@ -462,9 +463,9 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                 else:
                     ch.recv(planes_b[i], next_t(), timing)
     # a fixed-size hand-off is captured as a CUDA graph on its 2nd use of each
-    # queue half: make sure that capture happens before the timed region even
+    # queue slot: make sure that capture happens before the timed region even
     # when the caller asks for fewer warm-up steps (untimed, like compilation)
-    prime = 0 if (trace is not None or kivi) else max(0, 4 - args.warmup)
+    prime = 0 if (trace is not None or kivi) else max(0, 2 * ch.Q - args.warmup)
     for _ in range(prime + args.warmup):
         step()
     torch.cuda.synchronize()
@@ -609,6 +610,7 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
             extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
                    "format": spec.format,
                    "cuda_graphs": bool(ch.graphs),
+                   "queue_depth": ch.Q,
                    "graph_priming_steps": prime,
                    **({"trace_batches_timed": tok[args.warmup:args.warmup + args.steps],
                        "trace": "lengths log-uniform [128, 8192], 1-16 req/batch, <=16384 "
@@ -645,6 +647,8 @@ def main():
                     help="reference arm: layers per step (default: ~1 GB of fp16 KV)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--queue-depth", type=int, default=2,
+                    help="pull: queue slots per pair in the prefill GPU's HBM")
     ap.add_argument("--no-graphs", action="store_true",
                     help="N>1: launch every hand-off eagerly instead of replaying a CUDA graph")
     args = ap.parse_args()

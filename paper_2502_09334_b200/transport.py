@@ -30,9 +30,10 @@ prefill replicas' GPU memory (``PAPER.md:859``).  Here:
   the device (fence + st.release.sys over NVLink, by the last warp to finish
   the chunk) and ONE K3-bulk launch waits for them in-kernel (bounded
   ld.acquire polling by its producer warps); its last CTA releases the queue
-  half back to P, and K1's CTAs wait in-kernel for that release before they
-  reuse the half.  P's queue is double-buffered (hand-off e uses half e % 2).
-  The flags take constant values per (half, parity) and are never reset, so
+  queue slot back to P; P waits for that release (in the GPU front-end, and
+  again in-kernel) before it reuses the slot.  P's queue holds
+  ``ChannelSpec.queue_depth`` slots (default 2; hand-off e uses slot e % Q).
+  The flags take constant values per (slot, parity) and are never reset, so
   both ends of a hand-off are single CUDA-graph launches with no memop or
   memset nodes (see PairChannel._parity).  The non-fused paths use stream
   memory operations (cuStreamWriteValue32 / cuStreamWaitValue32) on the same
@@ -54,8 +55,9 @@ from .datapath import (KVPlanes, PackedKV, PackedLayout, _round_up, _stream_ptr,
 
 MODES = ("pull", "pull_ldg", "push", "copy", "nccl")
 PULL_MODES = ("pull", "pull_ldg")
-FLAG_SLOTS = 256  # 32-bit doorbells per rank
+FLAG_SLOTS = 1024  # 32-bit doorbells per rank (a 4 KB page)
 PULL_MAX_CHUNKS = 64
+PULL_MAX_QUEUE = 8  # queue slots per pair in the prefill GPU's HBM
 PULL_CHUNK_TARGET = 128 << 20  # min fp16 bytes per pull chunk
 K1_WARPS_EST = 148 * 2 * 8     # resident K1 warps on a B200 (2 x 256-thread CTAs per SM)
 
@@ -98,13 +100,18 @@ class ChannelSpec:
     format: str = "default"  # "default" (per-token groups) or "kivi" (pull modes only)
     device_doorbells: bool = True  # "pull": K1 itself rings per-chunk doorbells (one launch)
     layerwise: bool = False  # pull: layer-granular chunks (<= 64) for open_send streaming
+    # pull: hand-offs the prefill side may queue in its HBM before the decode
+    # side has pulled them (PAPER.md:859's KV queues); 2 = double buffering
+    queue_depth: int = 2
 
     def __post_init__(self):
         if self.mode not in MODES:
             raise ValueError(f"mode must be one of {MODES}")
         KvPrecision(self.bits)
-        if self.n_chunks < 1 or self.n_chunks > FLAG_SLOTS:
+        if self.n_chunks < 1 or self.n_chunks > FLAG_SLOTS // 4:
             raise ValueError("n_chunks out of range")
+        if not 1 <= self.queue_depth <= PULL_MAX_QUEUE:
+            raise ValueError(f"queue_depth must be in [1, {PULL_MAX_QUEUE}]")
         if self.format not in ("default", "kivi"):
             raise ValueError("format must be 'default' or 'kivi'")
         if self.format == "kivi" and self.mode not in PULL_MODES:
@@ -248,6 +255,7 @@ class PairChannel:
         self.cstream = torch.cuda.Stream(self.device)   # copy engine / NCCL
         self.data_group = data_group
         self.epoch = 0
+        self.Q = spec.queue_depth if spec.mode in PULL_MODES else 1
         self._prev_ranges = None
         self.chunks = spec.chunks()
         self.lpc = layers_per_chunk(spec.n_layers, spec.n_chunks)
@@ -270,7 +278,7 @@ class PairChannel:
         if mode in PULL_MODES:
             if len(self.chunks) > PULL_MAX_CHUNKS:
                 raise ValueError(f"pull modes support at most {PULL_MAX_CHUNKS} chunks")
-            # every flag starts at 0: both queue halves free for their first
+            # every flag starts at 0: every queue slot free for its first
             # use (parity 0), no chunk published (see _parity)
         stage_here = (self.role == "prefill" and mode in ("pull", "pull_ldg", "copy", "nccl")) or (
             self.role == "decode" and mode in ("push", "copy", "nccl"))
@@ -280,10 +288,10 @@ class PairChannel:
                 t = torch.empty(spec.capacity_bytes, dtype=torch.uint8, device=self.device)
                 self.local_payload = (t, _round_up(t.data_ptr()))
             else:
-                # pull modes double-buffer the prefill-side queue: hand-off e
-                # fills half e % 2 while the decode side may still read e - 1
-                halves = 2 if mode in PULL_MODES else 1
-                b = IpcBuffer(_round_up(spec.capacity_bytes) * halves)
+                # pull modes keep a queue of Q slots on the prefill side:
+                # hand-off e fills slot e % Q while the decode side may still
+                # be pulling the previous Q - 1
+                b = IpcBuffer(_round_up(spec.capacity_bytes) * self.Q)
                 self.local_payload = (b, _round_up(b.ptr))
         mine = {"flags": self.flags.handle()}
         if self.local_payload is not None and mode != "nccl":
@@ -304,31 +312,34 @@ class PairChannel:
             self.k3_source = (self.peer_payload if mode in ("pull", "pull_ldg")
                               else self.local_payload[1])
 
+    def _slot(self, e: int) -> int:
+        """Queue slot used by hand-off ``e`` (pull modes)."""
+        return e % self.Q
+
     def _half(self, e: int) -> int:
-        """Byte offset of the payload half used by hand-off ``e`` (pull modes)."""
-        return (e & 1) * _round_up(self.spec.capacity_bytes)
+        """Byte offset of the payload slot used by hand-off ``e`` (pull modes)."""
+        return (e % self.Q) * _round_up(self.spec.capacity_bytes)
 
     # pull-mode doorbells are never reset (no lost wake-ups): hand-off e uses
-    # half h = e & 1 for the u-th time, parity p = u & 1.
-    # ready[h][c] lives on D: P sets it to p ^ 1 once chunk c is in half h.
-    # free[h] lives on P: D sets it to p ^ 1 once it has consumed the half;
-    # P's next use of half h (parity p ^ 1) waits for free[h] == p ^ 1.
+    # queue slot h = e % Q for the u-th time, u = (e - 1) // Q, parity p = u & 1.
+    # ready[h][c] lives on D: P sets it to p ^ 1 once chunk c is in slot h.
+    # free[h] lives on P: D sets it to p ^ 1 once it has consumed the slot;
+    # P's next use of slot h (parity p ^ 1) waits for free[h] == p ^ 1.
     # Each side also keeps p in its own memory (state[h]); the fused kernels
     # read it there and flip it, so their CUDA graphs do not depend on p.
     # The stream-memop paths bake p in (their graphs are keyed by it) and flip
     # state[h] with a memop.
-    @staticmethod
-    def _parity(e: int) -> int:
-        return ((e - 1) >> 1) & 1
+    def _parity(self, e: int) -> int:
+        return ((e - 1) // self.Q) & 1
 
     def _pready(self, base: int, h: int, c: int) -> int:
         return base + 4 * (h * PULL_MAX_CHUNKS + c)
 
     def _pfree(self, base: int, h: int) -> int:
-        return base + 4 * (2 * PULL_MAX_CHUNKS + h)
+        return base + 4 * (PULL_MAX_QUEUE * PULL_MAX_CHUNKS + h)
 
     def _pstate(self, h: int) -> int:
-        return self.flags.ptr + 4 * (2 * PULL_MAX_CHUNKS + 2 + h)
+        return self.flags.ptr + 4 * (PULL_MAX_QUEUE * PULL_MAX_CHUNKS + PULL_MAX_QUEUE + h)
 
     def _fused(self, lay) -> bool:
         """One K1 launch ringing device-side doorbells -> one K3-bulk launch
@@ -358,7 +369,7 @@ class PairChannel:
         wait_eq(self._pfree(self.flags.ptr, h), p, stream)
 
     def _send_pull(self, src, lay, e, s, cur, timing, stage_in):
-        h, p = e & 1, self._parity(e)
+        h, p = self._slot(e), self._parity(e)
         chunks, lpc = self._pull_chunks(lay)
         key = ("send", lay.n_tokens, h, p, src.k.data_ptr(), src.slots_ptr)
         if self._graph_ok(key, timing, stage_in):
@@ -419,7 +430,7 @@ class PairChannel:
         return SendSession(self, src, n_tokens)
 
     def _recv_pull(self, dst, lay, e, s, cur, timing, stage_out):
-        h, p = e & 1, self._parity(e)
+        h, p = self._slot(e), self._parity(e)
         chunks, lpc = self._pull_chunks(lay)
         key = ("recv", lay.n_tokens, h, p, dst.slots_ptr, dst.k.data_ptr())
         if self._graph_ok(key, timing, stage_out):
@@ -474,7 +485,7 @@ class PairChannel:
         gs, rt = kivi_groups(seqlens, lay.group)
         chunks, _ = pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
                                     self.spec.min_chunk_bytes)
-        return lay, gs, rt, chunks, e & 1, self._parity(e)
+        return lay, gs, rt, chunks, self._slot(e), self._parity(e)
 
     def _send_kivi(self, src, n_tokens, seqlens, e):
         lay, gs, rt, chunks, h, p = self._kivi_common(n_tokens, seqlens, e)
@@ -587,7 +598,7 @@ class PairChannel:
             # fast path: a captured hand-off of this size/half/buffers is ONE
             # graph launch on the caller's stream (no extra stream syncs)
             e = self.epoch + 1
-            h, p = e & 1, self._parity(e)
+            h, p = self._slot(e), self._parity(e)
             g = self._graphs.get(("send", n_tokens, h, p, src.k.data_ptr(), src.slots_ptr))
             if g is not None:
                 self.epoch += 1
@@ -666,7 +677,7 @@ class PairChannel:
             return
         if timing is None and stage_out is None and self._graphs:
             e = self.epoch + 1
-            g = self._graphs.get(("recv", n_tokens, e & 1, self._parity(e), dst.slots_ptr,
+            g = self._graphs.get(("recv", n_tokens, self._slot(e), self._parity(e), dst.slots_ptr,
                                   dst.k.data_ptr()))
             if g is not None:
                 self.epoch += 1
@@ -772,7 +783,7 @@ class SendSession:
         self.ch, self.src = ch, src
         self.lay = ch.spec.layout(n_tokens)
         ch.epoch += 1
-        self.h, self.p = ch.epoch & 1, ch._parity(ch.epoch)
+        self.h, self.p = ch._slot(ch.epoch), ch._parity(ch.epoch)
         self.chunks, _ = ch._pull_chunks(self.lay)
         self.payload = PackedKV(self.lay, ch.k1_target + ch._half(ch.epoch), ch.device)
         self.next = 0

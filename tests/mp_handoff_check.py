@@ -242,6 +242,41 @@ def main():
         print(f"mixed paths: graphs={ch.graphs} captured={len(ch._graphs)}", flush=True)
     dist.barrier()
     ch.close()
+
+    # a deeper queue: with queue_depth=3 the prefill side completes 3 hand-offs
+    # before the decode side pulls any of them (with 2 slots the 3rd would wait)
+    Q = 3
+    spec = ChannelSpec(L, Tmax, H, D, 4, 128, 3, "pull", queue_depth=Q)
+    ch = PairChannel(spec, rank, world, control_group=ctrl)
+    for rnd in range(3):
+        Ts = [Tmax, 77, 130]
+        seeds = [5000 + 100 * rnd + 10 * i + ch.pair for i in range(Q)]
+        if ch.role == "prefill":
+            kvs = [torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=sd)).to(dev)
+                   for T, sd in zip(Ts, seeds)]
+            for kv_i, T in zip(kvs, Ts):
+                ch.send(KVPlanes.dense(kv_i), T)
+            torch.cuda.synchronize()  # all Q hand-offs queued in P's HBM
+            dist.barrier(ctrl)
+        else:
+            dist.barrier(ctrl)  # the decode side starts only after P finished
+            for T, sd in zip(Ts, seeds):
+                slots_np = O.synthetic_slots(T, bs, nb, seed=sd)
+                kc.zero_(); vc.zero_()
+                ch.recv(KVPlanes.paged(kc, vc, torch.from_numpy(slots_np).to(dev)), T)
+                torch.cuda.synchronize()
+                okc = np.zeros((L, nb, bs, H, D), np.float16); ovc = okc.copy()
+                c, s_, z = O.quant_pack(O.synthetic_kv(L, T, H, D, seed=sd).reshape(-1, D), 4, 128)
+                O.scatter_paged(O.unpack_dequant(c, s_, z, 4, 128, D).reshape(L, 2, T, H, D),
+                                slots_np, okc, ovc)
+                if not (np.array_equal(kc.cpu().numpy().view(np.uint16), okc.view(np.uint16)) and
+                        np.array_equal(vc.cpu().numpy().view(np.uint16), ovc.view(np.uint16))):
+                    failures += 1
+                    print(f"MISMATCH queue rank={rank} round={rnd} T={T}", flush=True)
+    if rank == 0:
+        print(f"queue_depth={Q}: prefill ran {Q} hand-offs ahead", flush=True)
+    dist.barrier()
+    ch.close()
     f = torch.tensor([failures], device=dev)
     dist.all_reduce(f)
     if rank == 0:

@@ -128,47 +128,52 @@ def test_kivi_capacity_covers_every_split():
         ChannelSpec(5, 300, 4, 128, 4, 32, 3, "push", format="kivi")
 
 
-def _simulate_protocol(schedule, n_handoffs):
+def _simulate_protocol(schedule, n_handoffs, Q=2):
     """Discrete model of the pull doorbells (PairChannel._parity, kvx.h).
 
-    P (prefill) and D (decode) each process hand-offs 1..n in order.  Flags:
-    ready[h] on D, free[h] on P, and each side's parity state[h]; nothing is
-    ever reset.  ``schedule`` picks which side tries to move next.  Returns the
-    order in which hand-offs were produced / consumed and checks the safety
-    properties at every step."""
+    P (prefill) and D (decode) each process hand-offs 1..n in order over Q
+    queue slots.  Flags: ready[h] on D, free[h] on P, and each side's parity
+    state[h]; nothing is ever reset.  ``schedule`` picks which side tries to
+    move next.  Returns the order in which hand-offs were produced / consumed
+    and checks the safety properties at every step."""
     from paper_2502_09334_b200.transport import PairChannel
-    par = PairChannel._parity
-    ready = [0, 0]; free = [0, 0]; p_state = [0, 0]; d_state = [0, 0]
+    ch = PairChannel.__new__(PairChannel)  # only the slot/parity arithmetic
+    ch.Q = Q
+    ready = [0] * Q; free = [0] * Q; p_state = [0] * Q; d_state = [0] * Q
     produced = []; consumed = []
     p_next = d_next = 1
     for who in schedule:
         if who == "P" and p_next <= n_handoffs:
-            e = p_next; h = e & 1; p = p_state[h]
-            assert p == par(e)  # the device state matches the host's epoch parity
+            e = p_next; h = ch._slot(e); p = p_state[h]
+            assert p == ch._parity(e)  # the device state matches the host's epoch parity
             if free[h] != p:
-                continue  # K1 waits in-kernel: D has not consumed the half's last use
-            # safe to overwrite half h: its previous use (if any) is consumed
-            assert e <= 2 or (e - 2) in consumed
+                continue  # P waits: D has not consumed the slot's last use
+            # safe to overwrite slot h: its previous use (if any) is consumed
+            assert e <= Q or (e - Q) in consumed
             produced.append(e); ready[h] = p ^ 1; p_state[h] = p ^ 1; p_next += 1
         elif who == "D" and d_next <= n_handoffs:
-            e = d_next; h = e & 1; p = d_state[h]
-            assert p == par(e)
+            e = d_next; h = ch._slot(e); p = d_state[h]
+            assert p == ch._parity(e)
             if ready[h] != p ^ 1:
                 continue  # K3 waits in-kernel for the doorbell
-            assert e in produced  # never reads a half before it is written
+            assert e in produced  # never reads a slot before it is written
             consumed.append(e); free[h] = p ^ 1; d_state[h] = p ^ 1; d_next += 1
-        # P never runs more than one use ahead per half
-        assert p_next - d_next <= 2
+        # P never runs more than Q hand-offs ahead
+        assert p_next - d_next <= Q
     return produced, consumed
 
 
-def test_parity_doorbells_are_safe_and_live():
-    """Every interleaving: no half is overwritten before it is consumed, none
-    is consumed before it is produced, and progress never stalls."""
+@pytest.mark.parametrize("Q", [1, 2, 3, 8])
+def test_parity_doorbells_are_safe_and_live(Q):
+    """Every interleaving: no slot is overwritten before it is consumed, none
+    is consumed before it is produced, progress never stalls, and P can run a
+    full queue (Q hand-offs) ahead of D."""
     import random
-    rng = random.Random(0)
+    rng = random.Random(Q)
     for trial in range(300):
-        n = rng.randint(1, 12)
+        n = rng.randint(1, 4 * Q + 4)
         sched = [rng.choice("PPD" if trial % 2 else "PDD") for _ in range(400)]
-        produced, consumed = _simulate_protocol(sched + list("PD") * 2 * n, n)
+        produced, consumed = _simulate_protocol(sched + list("PD") * 2 * n, n, Q)
         assert produced == list(range(1, n + 1)) and consumed == produced
+    produced, _ = _simulate_protocol("P" * (Q + 3), Q + 3, Q)
+    assert produced == list(range(1, Q + 1))  # a full queue, then P waits

@@ -78,7 +78,7 @@ def main():
                     ch.send(planes, T)
                 # the decode side sets free[h] = parity ^ 1 when its K3 has
                 # consumed the half
-                h, p = ch.epoch & 1, ch._parity(ch.epoch)
+                h, p = ch._slot(ch.epoch), ch._parity(ch.epoch)
                 cur = torch.cuda.current_stream()
                 wait_eq(ch._pfree(ch.flags.ptr, h), p ^ 1, cur)
                 e_done.record()
