@@ -271,9 +271,13 @@ class PairChannel:
         # local buffers: doorbells (written by the partner) + payload staging
         self.flags = IpcBuffer(FLAG_SLOTS * 4)
         self.graphs = bool(graphs) and mode in PULL_MODES
-        # K1's chunk arrival counters + CTA exit counter (zero between launches)
-        self.counters = torch.zeros(PULL_MAX_CHUNKS + 1, dtype=torch.int32, device=self.device)
-        self.done_counter = torch.zeros(1, dtype=torch.int32, device=self.device)
+        # per queue slot: K1's chunk arrival counters + CTA exit counter, and
+        # K3-bulk's done counter (zero between launches) -- per slot, so
+        # hand-offs on different slots never share scratch even if the caller
+        # issues them from different streams
+        self.counters = torch.zeros((self.Q, PULL_MAX_CHUNKS + 1), dtype=torch.int32,
+                                    device=self.device)
+        self.done_counter = torch.zeros(self.Q, dtype=torch.int32, device=self.device)
         self._graphs, self._seen = {}, set()
         if mode in PULL_MODES:
             if len(self.chunks) > PULL_MAX_CHUNKS:
@@ -393,7 +397,7 @@ class PairChannel:
                 _lib.call("kvx_quant_pack_signal", k, v, src.layer_stride, src.slots_ptr,
                           lay.n_layers, lay.n_tokens, lay.n_heads, lay.head_dim, lay.group,
                           lay.bits, c0, sc0, z0, lay.layer_stride, *src.window_args,
-                          self.counters.data_ptr(), self._pready(self.peer_flags, h, 0), lpc,
+                          self.counters[h].data_ptr(), self._pready(self.peer_flags, h, 0), lpc,
                           self._pfree(self.flags.ptr, h), self._pstate(h), _stream_ptr(s))
                 _kernel_events_end(ev, s)
                 return
@@ -449,7 +453,7 @@ class PairChannel:
                 ev = _kernel_events(timing, s, "k3")
                 dequant_scatter_layers(payload, dst, 0, lay.n_layers, s,
                                        ready=(self._pready(self.flags.ptr, h, 0), lpc),
-                                       done=(self.done_counter.data_ptr(),
+                                       done=(self.done_counter[h].data_ptr(),
                                              self._pfree(self.peer_flags, h), self._pstate(h)))
                 _kernel_events_end(ev, s)
             else:

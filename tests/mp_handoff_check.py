@@ -34,10 +34,11 @@ def main():
     # empty hand-off in between must consume no epoch on either side)
     seq = (Tmax, 77) * 3 + (0,) + (Tmax, 77) * 3 + (130, Tmax)
     for mode in modes:
-        for bits in (4, 8, 16):
+        for bits in ((2, 4, 8, 16) if mode == "pull" else (4, 8, 16)):
             # "pull_hostdb": pull with host-enqueued per-chunk doorbells instead
             # of the fused K1 ringing them from the device
-            spec = ChannelSpec(L, Tmax, H, D, bits, 64 if bits != 16 else 128, 3,
+            grp = {2: 32, 4: 64, 8: 64, 16: 128}[bits]
+            spec = ChannelSpec(L, Tmax, H, D, bits, grp, 3,
                                "pull" if mode == "pull_hostdb" else mode,
                                min_chunk_bytes=0,  # always 3 chunks: exercise the pipeline
                                device_doorbells=(mode != "pull_hostdb"))
