@@ -78,7 +78,11 @@ def peaks():
         return 6650.0, "fallback"
 
 
-NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+# NVLink roofline per direction: the fastest peer copy measured on this pool's
+# B200s -- a TMA bulk pull into shared memory (tools/nvlink_bench.cu,
+# profiles/r01_nvlink/nvlink_bench.jsonl: 782-783 GB/s; copy engines 777,
+# B200_PROFILING.md's peer copy 770; 900 nominal)
+NVLINK_GBS = 783.0
 
 
 # ---------------------------------------------------------------------------
@@ -598,7 +602,8 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
             roofline={"bound": "nvlink", "kernel": "pull_dequant_scatter_paged (TMA bulk pull "
                       "over NVLink)" if mode == "pull" else f"hand-off ({mode})",
                       "achieved": round(link_gbs, 1), "peak": B.NVLINK_GBS,
-                      "peak_kind": "measured peer copy, B200_PROFILING.md (900 nominal)",
+                      "peak_kind": "measured TMA bulk-pull peer copy, tools/nvlink_bench.cu "
+                                   "(770 in B200_PROFILING.md, 900 nominal)",
                       "unit": "GB/s", "frac": round(link_gbs / B.NVLINK_GBS, 4), "traffic": None,
                       "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
                       "k3_link_gbs": round(k3_link, 1) if k3_link else None,

@@ -192,6 +192,10 @@ cudaError_t launch_dequant(const kvx::Geo& g, const void* codes, const void* sca
 constexpr int kBulkStages = KVX_BULK_STAGES;
 constexpr int kBulkThreads = 288;
 constexpr int kBulkStageTarget = KVX_BULK_STAGE_BYTES;  // code bytes per stage
+#ifndef KVX_PULL_PER_SM
+#define KVX_PULL_PER_SM 1
+#endif
+constexpr int kPullCtasPerSm = KVX_PULL_PER_SM;  // bulk-pull CTAs per SM (A/B: -DKVX_PULL_PER_SM)
 
 // Smallest row count whose code and metadata bytes are both 16-byte multiples.
 int64_t bulk_row_multiple(int64_t code_row_bytes, int64_t meta_row_bytes) {
@@ -264,7 +268,17 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   cudaGetLastError();
   int dev = 0;
   cudaGetDevice(&dev);
+  // ONE CTA per SM (4 stages x ~16 KB in flight each, 9.5 MB device-wide):
+  // enough to saturate the link, and measured faster than filling every SM
+  // with as many CTAs as fit (cfg3 pair 2,948 vs 2,798 GB/s fp16-eq), while
+  // leaving room on each SM for the decode GPU's own kernels
+  // (tools/decode_interference.py: a concurrent HBM-bound round slows 1.96x
+  // instead of 2.2x).
+  per_sm = per_sm < kPullCtasPerSm ? per_sm : kPullCtasPerSm;
   int64_t grid = int64_t(sm_count(dev)) * per_sm;
+#ifdef KVX_PULL_MAX_CTAS
+  if (grid > KVX_PULL_MAX_CTAS) grid = KVX_PULL_MAX_CTAS;
+#endif
   if (grid > n_spans) grid = n_spans;
   *ok = true;
   k<<<unsigned(grid), kBulkThreads, smem, s>>>(g, bg, static_cast<const uint8_t*>(codes),
@@ -388,6 +402,7 @@ cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, voi
       per_sm < 1)
     per_sm = 1;
   cudaGetLastError();
+  per_sm = per_sm < kPullCtasPerSm ? per_sm : kPullCtasPerSm;  // as launch_pull
   int64_t grid = int64_t(sm_count(dev)) * per_sm;
   if (grid > kb.n_spans) grid = kb.n_spans;
   if (grid < 1) return cudaSuccess;
