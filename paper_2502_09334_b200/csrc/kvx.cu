@@ -187,11 +187,14 @@ cudaError_t launch_dequant(const kvx::Geo& g, const void* codes, const void* sca
 #define KVX_BULK_STAGES 4
 #endif
 #ifndef KVX_BULK_STAGE_BYTES
-#define KVX_BULK_STAGE_BYTES 16384
+#define KVX_BULK_STAGE_BYTES 12288
 #endif
 constexpr int kBulkStages = KVX_BULK_STAGES;
 constexpr int kBulkThreads = 288;
-constexpr int kBulkStageTarget = KVX_BULK_STAGE_BYTES;  // code bytes per stage
+// code bytes per stage: 4 x 12 KB in flight per SM.  A/B at one CTA per SM
+// (N=2, GB/s fp16-eq, cfg3 / cfg4 pair): 8 KB 2,833 / 2,867; 12 KB 2,945 /
+// 2,903; 16 KB 2,947 / 2,865; 32 KB 2,758 / 2,629; 6 x 16 KB 2,707 / 2,604.
+constexpr int kBulkStageTarget = KVX_BULK_STAGE_BYTES;
 #ifndef KVX_PULL_PER_SM
 #define KVX_PULL_PER_SM 1
 #endif
