@@ -374,6 +374,11 @@ cudaError_t launch_kchan_dequant(const kvx::KchanGeo& kg, const int64_t* slots, 
   return cudaGetLastError();
 }
 
+#ifndef KVX_KCHAN_STAGE_CODES
+#define KVX_KCHAN_STAGE_CODES 16384
+#endif
+constexpr int kKchanStageCodes = KVX_KCHAN_STAGE_CODES;  // code bytes per kchan span
+
 // Bulk-staged kchan dequant (payload read over NVLink).  *ok = false when the
 // shape cannot be staged (caller falls back to the per-lane kernel).
 template <int BITS, int G>
@@ -382,7 +387,7 @@ cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, voi
   *ok = false;
   constexpr int kStages = 4;
   kvx::KchanBulk kb;
-  kb.slab = 16384 / (G * BITS / 8);  // 16 KB of codes per stage: 256..1024 channels
+  kb.slab = kKchanStageCodes / (G * BITS / 8);  // channels per span (S/32 divides 256)
   if (kg.row_elems % 32 || !aligned(kg.codes, 16) || !aligned(kg.scale, 16) ||
       !aligned(kg.zero, 16) || kg.payload_ls % 16)
     return cudaSuccess;
