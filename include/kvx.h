@@ -198,14 +198,22 @@ int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_st
 /* Same contract, for a payload read over NVLink: the per-channel K groups and
  * the per-token V rows are staged into shared memory with cp.async.bulk
  * (TMA) before they are dequantised -- the kivi format's pull transport.
- * Shapes that cannot be bulk-staged fall back to the per-lane kernels. */
+ * Shapes that cannot be bulk-staged fall back to the per-lane kernels.
+ * ready_flags (nullable, this GPU's memory): the kernels wait in-kernel, per
+ * chunk of layers_per_chunk layers, until ready_flags[chunk] == p ^ 1 (p =
+ * *parity_state, read only; or 0), so ONE call consumes a whole hand-off
+ * while the prefill side is still publishing it; the caller releases the
+ * queue slot after the call (stream order).  With flags, shapes that cannot
+ * be bulk-staged return KVX_ERR_UNSUPPORTED. */
 int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_stride,
                                         const int64_t* seg_offsets, const int64_t* dst_slots,
                                         const int64_t* group_starts, int64_t n_groups,
                                         const int64_t* residual_dst_slots, int64_t n_residual,
                                         int64_t n_layers, int64_t n_tokens, int n_heads,
                                         int head_dim, int group, int bits, void* k_cache,
-                                        void* v_cache, int64_t dst_layer_stride, void* stream);
+                                        void* v_cache, int64_t dst_layer_stride,
+                                        const void* ready_flags, int layers_per_chunk,
+                                        const void* parity_state, void* stream);
 
 /* Packed payload sizes in bytes for n_rows rows (codes, scale, zero). */
 int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t* codes_bytes,

@@ -383,10 +383,15 @@ constexpr int kKchanStageCodes = KVX_KCHAN_STAGE_CODES;  // code bytes per kchan
 // shape cannot be staged (caller falls back to the per-lane kernel).
 template <int BITS, int G>
 cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, void* kc,
-                              int64_t dst_ls_b, cudaStream_t s, bool* ok) {
+                              int64_t dst_ls_b, cudaStream_t s, bool* ok,
+                              const uint32_t* ready = nullptr, int layers_per_chunk = 1,
+                              const uint32_t* parity = nullptr) {
   *ok = false;
   constexpr int kStages = 4;
   kvx::KchanBulk kb;
+  kb.ready = ready;
+  kb.parity = parity;
+  kb.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
   kb.slab = kKchanStageCodes / (G * BITS / 8);  // channels per span (S/32 divides 256)
   if (kg.row_elems % 32 || !aligned(kg.codes, 16) || !aligned(kg.scale, 16) ||
       !aligned(kg.zero, 16) || kg.payload_ls % 16)
@@ -678,7 +683,8 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
                         const int64_t* residual_dst_slots, int64_t n_residual, int64_t n_layers,
                         int64_t n_tokens, int n_heads, int head_dim, int group, int bits,
                         void* k_cache, void* v_cache, int64_t dst_layer_stride, void* stream,
-                        bool bulk) {
+                        bool bulk, const uint32_t* ready = nullptr, int layers_per_chunk = 1,
+                        const uint32_t* parity = nullptr) {
   int rc = kivi_check(head_dim, group, bits);
   if (rc) return rc;
   if (n_layers < 0 || n_tokens < 0 || n_heads <= 0 || n_groups < 0 || n_residual < 0 ||
@@ -709,13 +715,17 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
     const int64_t dls = dst_layer_stride * 2;
     bool ok = false;
     if (bulk) {
+      const int lpc = layers_per_chunk;
       if (bits == 4)
-        e = group == 32 ? launch_kchan_pull<4, 32>(kg, dst_slots, k_cache, dls, s, &ok)
-                        : launch_kchan_pull<4, 64>(kg, dst_slots, k_cache, dls, s, &ok);
+        e = group == 32
+                ? launch_kchan_pull<4, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, lpc, parity)
+                : launch_kchan_pull<4, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, lpc, parity);
       else
-        e = group == 32 ? launch_kchan_pull<8, 32>(kg, dst_slots, k_cache, dls, s, &ok)
-                        : launch_kchan_pull<8, 64>(kg, dst_slots, k_cache, dls, s, &ok);
+        e = group == 32
+                ? launch_kchan_pull<8, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, lpc, parity)
+                : launch_kchan_pull<8, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, lpc, parity);
       if (e != cudaSuccess) return e;
+      if (!ok && ready) return KVX_ERR_UNSUPPORTED;  // per-lane kernels cannot wait in-kernel
     }
     if (!ok) {
       if (bits == 4)
@@ -727,6 +737,29 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
       if (e != cudaSuccess) return e;
     }
   }
+  {
+    kvx::Geo g;
+    rc = make_geo(g, v_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
+                  head_dim, group, bits, payload_layer_stride, 1, 1);
+    if (rc) return rc;
+    const char *vc = base + seg_offsets[4], *vs = base + seg_offsets[5], *vz = base + seg_offsets[6];
+    bool ok = false;
+    if (bulk && aligned(v_cache, 32) && g.plane_row_b % 32 == 0) {
+      PullDone pd;  // parity read-only: the caller releases the slot after this call
+      pd.parity = const_cast<uint32_t*>(parity);
+      e = bits == 4 ? dispatch_pull<4>(group, g, vc, vs, vz, s, &ok, ready, layers_per_chunk, pd)
+                    : dispatch_pull<8>(group, g, vc, vs, vz, s, &ok, ready, layers_per_chunk, pd);
+      if (e != cudaSuccess) return e;
+    }
+    if (!ok && ready) return KVX_ERR_UNSUPPORTED;  // per-lane kernels cannot wait in-kernel
+    if (!ok)
+      e = bits == 4 ? dispatch_dequant<4>(group, g, vc, vs, vz, s)
+                    : dispatch_dequant<8>(group, g, vc, vs, vz, s);
+  }
+  if (e != cudaSuccess) return e;
+  // residual fp16 rows last: once the V kernel has seen every chunk's
+  // doorbell, the whole payload is published, so these per-lane reads need
+  // no wait of their own
   if (n_residual) {
     kvx::Geo g;
     rc = make_geo(g, k_cache, k_cache, dst_layer_stride, residual_dst_slots, n_layers, n_residual,
@@ -736,22 +769,6 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
     k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(
         g, reinterpret_cast<const uint8_t*>(base + seg_offsets[3]));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  {
-    kvx::Geo g;
-    rc = make_geo(g, v_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
-                  head_dim, group, bits, payload_layer_stride, 1, 1);
-    if (rc) return rc;
-    const char *vc = base + seg_offsets[4], *vs = base + seg_offsets[5], *vz = base + seg_offsets[6];
-    bool ok = false;
-    if (bulk && aligned(v_cache, 32) && g.plane_row_b % 32 == 0) {
-      e = bits == 4 ? dispatch_pull<4>(group, g, vc, vs, vz, s, &ok, nullptr, 1, PullDone())
-                    : dispatch_pull<8>(group, g, vc, vs, vz, s, &ok, nullptr, 1, PullDone());
-      if (e != cudaSuccess) return e;
-    }
-    if (!ok)
-      e = bits == 4 ? dispatch_dequant<4>(group, g, vc, vs, vz, s)
-                    : dispatch_dequant<8>(group, g, vc, vs, vz, s);
   }
   return e;
 }
@@ -774,10 +791,17 @@ int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_lay
                                         const int64_t* residual_dst_slots, int64_t n_residual,
                                         int64_t n_layers, int64_t n_tokens, int n_heads,
                                         int head_dim, int group, int bits, void* k_cache,
-                                        void* v_cache, int64_t dst_layer_stride, void* stream) {
+                                        void* v_cache, int64_t dst_layer_stride,
+                                        const void* ready_flags, int layers_per_chunk,
+                                        const void* parity_state, void* stream) {
+  if ((ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) ||
+      !aligned(parity_state, 4))
+    return KVX_ERR_INVALID_ARG;
   return kivi_dequant(payload, payload_layer_stride, seg_offsets, dst_slots, group_starts,
                       n_groups, residual_dst_slots, n_residual, n_layers, n_tokens, n_heads,
-                      head_dim, group, bits, k_cache, v_cache, dst_layer_stride, stream, true);
+                      head_dim, group, bits, k_cache, v_cache, dst_layer_stride, stream, true,
+                      static_cast<const uint32_t*>(ready_flags), layers_per_chunk,
+                      static_cast<const uint32_t*>(parity_state));
 }
 
 // ---- transport -------------------------------------------------------------

@@ -255,6 +255,12 @@ struct KchanBulk {
   int slabs;         // ceil(row_elems / S)
   int64_t n_spans;   // n_layers * n_groups * slabs
   int stage_bytes;   // G * S * BITS/8 + 4 * S
+  // per-chunk doorbells (nullable): wait ready[layer / layers_per_chunk] ==
+  // p ^ 1 before a span's bulk reads, p = *parity (or 0) -- one launch
+  // consumes a whole hand-off while the prefill side is still producing it
+  const uint32_t* ready;
+  const uint32_t* parity;
+  int layers_per_chunk;
 };
 
 template <int BITS, int G, int STAGES>
@@ -278,6 +284,8 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
   const int code_slice = S * BITS / 8;  // bytes of one row's slab slice in smem
   if (warp == CONSUMERS) {  // ---- producer: one elected thread
     if (lane == 0) {
+      const uint32_t want = (kb.parity ? *kb.parity : 0u) ^ 1u;
+      int64_t ready_chunk = -1;
       uint32_t k = 0;
       for (int64_t sp = blockIdx.x; sp < kb.n_spans; sp += gridDim.x, ++k) {
         const int st = k % STAGES;
@@ -285,6 +293,13 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
         const int64_t lg = sp / kb.slabs;
         const int c0 = int(sp - lg * kb.slabs) * S;
         const int64_t layer = lg / g.n_groups, grp = lg - layer * g.n_groups;
+        if (kb.ready) {
+          const int64_t c = layer / kb.layers_per_chunk;
+          if (c > ready_chunk) {
+            wait_ready(kb.ready + c, want);
+            ready_chunk = c;
+          }
+        }
         const int ns = min(S, g.row_elems - c0);
         const uint32_t rb = uint32_t(ns) * BITS / 8, mb = uint32_t(ns) * 2;
         mbar_expect_tx(&full[st], G * rb + 2 * mb);

@@ -159,12 +159,16 @@ def decompress_kivi_into_paged(packed: PackedKiviKV, k_cache: torch.Tensor, v_ca
     gs = packed.group_starts.to(k_cache.device)
     rdst = dst.slots[packed.residual_tokens.to(k_cache.device)].contiguous()
     k, v = dst.ptrs(0)
-    fn = "kvx_pull_dequant_scatter_paged_kivi" if bulk else "kvx_dequant_scatter_paged_kivi"
-    _lib.call(fn, packed.base, lay.layer_stride, _offsets_arg(lay),
-              dst.slots_ptr, gs.data_ptr() if gs.numel() else None, gs.numel(),
-              rdst.data_ptr() if rdst.numel() else None, rdst.numel(), lay.n_layers,
-              lay.n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
-              dst.layer_stride, _stream_ptr(stream))
+    args = (packed.base, lay.layer_stride, _offsets_arg(lay),
+            dst.slots_ptr, gs.data_ptr() if gs.numel() else None, gs.numel(),
+            rdst.data_ptr() if rdst.numel() else None, rdst.numel(), lay.n_layers,
+            lay.n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
+            dst.layer_stride)
+    if bulk:
+        _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args, None, 1, None,
+                  _stream_ptr(stream))
+    else:
+        _lib.call("kvx_dequant_scatter_paged_kivi", *args, _stream_ptr(stream))
     if stream is not None:  # temporaries were allocated on the current stream
         gs.record_stream(stream)
         rdst.record_stream(stream)

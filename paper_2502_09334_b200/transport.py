@@ -487,8 +487,9 @@ class PairChannel:
         if lay.n_tokens != n_tokens:
             raise ValueError("seqlens must sum to n_tokens")
         gs, rt = kivi_groups(seqlens, lay.group)
-        chunks, _ = pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
-                                    self.spec.min_chunk_bytes)
+        chunks, lpc = pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
+                                      self.spec.min_chunk_bytes)
+        self._kivi_lpc = lpc
         return lay, gs, rt, chunks, self._slot(e), self._parity(e)
 
     def _send_kivi(self, src, n_tokens, seqlens, e):
@@ -523,18 +524,25 @@ class PairChannel:
             rdst = dst.slots[torch.from_numpy(rt).to(self.device)].contiguous()
         base = self.k3_source + self._half(e)
         offs = (ctypes.c_int64 * 7)(*lay.offsets)
-        # "pull": TMA bulk-staged kernels; "pull_ldg": per-lane peer loads
-        fn = ("kvx_pull_dequant_scatter_paged_kivi" if self.spec.mode == "pull"
-              else "kvx_dequant_scatter_paged_kivi")
-        for c, (l0, l1) in enumerate(chunks):
-            wait_eq(self._pready(self.flags.ptr, h, c), p ^ 1, s)
+
+        def args(l0, l1):
             k, v = dst.ptrs(l0)
-            _lib.call(fn, base + l0 * lay.layer_stride,
-                      lay.layer_stride, offs, dst.slots_ptr,
-                      gs_d.data_ptr() if len(gs) else None, len(gs),
-                      rdst.data_ptr() if rdst.numel() else None, rdst.numel(), l1 - l0,
-                      n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
-                      dst.layer_stride, _stream_ptr(s))
+            return (base + l0 * lay.layer_stride, lay.layer_stride, offs, dst.slots_ptr,
+                    gs_d.data_ptr() if len(gs) else None, len(gs),
+                    rdst.data_ptr() if rdst.numel() else None, rdst.numel(), l1 - l0,
+                    n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
+                    dst.layer_stride)
+
+        if self.spec.mode == "pull":
+            # TMA bulk-staged kernels over the whole hand-off, waiting in-kernel
+            # for each chunk's doorbell (a handful of launches per hand-off)
+            _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args(0, lay.n_layers),
+                      self._pready(self.flags.ptr, h, 0), self._kivi_lpc, self._pstate(h),
+                      _stream_ptr(s))
+        else:  # "pull_ldg": per-chunk stream waits, per-lane peer loads
+            for c, (l0, l1) in enumerate(chunks):
+                wait_eq(self._pready(self.flags.ptr, h, c), p ^ 1, s)
+                _lib.call("kvx_dequant_scatter_paged_kivi", *args(l0, l1), _stream_ptr(s))
         signal(self._pfree(self.peer_flags, h), p ^ 1, s)
         signal(self._pstate(h), p ^ 1, s)
         gs_d.record_stream(s)

@@ -143,11 +143,16 @@ def test_fused_and_kivi_entry_points_validate(lib):
     offs = (ctypes.c_int64 * 7)(*([0] * 7))
     for fn in ("kvx_dequant_scatter_paged_kivi", "kvx_pull_dequant_scatter_paged_kivi"):
         f = getattr(lib, fn)
+        tail = (None,) if fn.startswith("kvx_dequant") else (None, 1, None, None)
         # kivi: bits 2 and group 128 are not kivi formats
         assert f(256, 256, offs, 256, None, 0, None, 0, 1, 1, 1, 128, 32, 2, 256, 256, 0,
-                 None) == E
+                 *tail) == E
         assert f(256, 256, offs, 256, None, 0, None, 0, 1, 1, 1, 128, 128, 4, 256, 256, 0,
-                 None) == E
+                 *tail) == E
         # group counts must add up to the token count
         assert f(256, 256, offs, 256, 256, 1, None, 0, 1, 5, 1, 128, 32, 4, 256, 256, 0,
-                 None) == E
+                 *tail) == E
+    # the pull variant's doorbells must be aligned
+    assert lib.kvx_pull_dequant_scatter_paged_kivi(256, 256, offs, 256, None, 0, None, 0, 1, 32,
+                                                   1, 128, 32, 4, 256, 256, 0, 258, 1, None,
+                                                   None) == E
