@@ -356,6 +356,19 @@ def ncu_traffic(workload, args, kernel):
         return None
 
 
+def ncu_link_traffic(workload, args):
+    """NVLink bytes per K3-bulk launch of this configuration from the committed
+    ncu capture (nvlrx user bytes = the payload exactly when nothing is
+    re-read; raw bytes include the link protocol), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            doc = json.load(f)
+        key = f"{workload}/bits{args.bits}/g{args.group}/nvlink_pull"
+        return dict(doc["configs"][key]["pull_dequant_scatter_paged"], source=doc["source_" + key])
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def plan_chunks(args, L):
     from paper_2502_09334_b200.datapath import layer_chunks
     return layer_chunks(L, args.chunks)
@@ -604,7 +617,9 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                       "achieved": round(link_gbs, 1), "peak": B.NVLINK_GBS,
                       "peak_kind": "measured TMA bulk-pull peer copy, tools/nvlink_bench.cu "
                                    "(770 in B200_PROFILING.md, 900 nominal)",
-                      "unit": "GB/s", "frac": round(link_gbs / B.NVLINK_GBS, 4), "traffic": None,
+                      "unit": "GB/s", "frac": round(link_gbs / B.NVLINK_GBS, 4),
+                      "traffic": None,  # DRAM traffic is not the bound here; see link_traffic
+                      "link_traffic": B.ncu_link_traffic(wl, args),
                       "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
                       "k3_link_gbs": round(k3_link, 1) if k3_link else None,
                       "frac_of_nominal_900": round(link_gbs / 900.0, 4),
