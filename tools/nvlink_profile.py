@@ -5,7 +5,7 @@ interest per run; no in-kernel cross-GPU waits, so ncu replay is safe):
   pull_ldg  per-lane K3 on GPU 1 reading GPU 0's payload (LDG.128)
   push      K1 on GPU 0 storing the payload into GPU 1 (STG over NVLink)
 
-  python tools/nvlink_profile.py pull      (config 4 pair: 70B GQA, 8192 tokens)
+  python tools/nvlink_profile.py pull [workload]   (default: config 4 pair, 70B GQA)
 """
 import os
 import sys
@@ -22,7 +22,8 @@ from paper_2502_09334_b200.datapath import HandoffPlan, KVPlanes  # noqa: E402
 
 def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "pull"
-    L, H, D, b, s = B.WORKLOADS["cfg4_70b_gqa_pair"]
+    wl = sys.argv[2] if len(sys.argv) > 2 else "cfg4_70b_gqa_pair"
+    L, H, D, b, s = B.WORKLOADS[wl]
     T = b * s
     p, d = torch.device("cuda", 0), torch.device("cuda", 1)
     kv = B.synthetic_kv_device(torch, L, T, H, D, p)
