@@ -43,9 +43,15 @@ def main():
                  (2, ["--workload", "trace_7b", "--no-e2e"]),
                  (2, ["--workload", "small_70b_gqa_128x1", "--no-e2e"]),
                  (2, ["--format", "kivi", "--group", "32", "--no-e2e"]),
-                 (2, ["--mode", "copy", "--no-e2e"]), (2, ["--mode", "nccl", "--no-e2e"])]
+                 (2, ["--format", "kivi", "--group", "32", "--workload", "cfg4_70b_gqa_pair",
+                      "--no-e2e"]),
+                 (2, ["--mode", "pull_ldg", "--no-e2e"]), (2, ["--mode", "push", "--no-e2e"]),
+                 (2, ["--mode", "copy", "--no-e2e"]), (2, ["--mode", "nccl", "--no-e2e"]),
+                 (2, ["--bits", "8", "--group", "64", "--no-e2e"]),
+                 (2, ["--bits", "16", "--no-e2e"])]
     if a.gpus >= 4:
-        plan += [(4, []), (4, ["--workload", "trace_70b_gqa", "--no-e2e"])]
+        plan += [(4, []), (4, ["--workload", "trace_70b_gqa", "--no-e2e"]),
+                 (4, ["--workload", "trace_7b", "--no-e2e"])]
     if a.gpus >= 8:
         plan += [(8, []), (8, ["--workload", "trace_70b_gqa", "--no-e2e"])]
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
