@@ -231,6 +231,11 @@ int kvx_copy_peer(void* dst, int dst_dev, const void* src, int src_dev, size_t n
 
 /* ---- transport: NVLink P2P across processes (one process per GPU) ------- */
 
+/* cudaMemcpyAsync with cudaMemcpyDefault (unified addressing): any mix of
+ * host-pinned, local, peer and IPC-mapped addresses (doorbell polling,
+ * staging). */
+int kvx_memcpy_async(void* dst, const void* src, size_t n_bytes, void* stream);
+
 /* IPC-exportable device allocation (setup only, never on the hot path). */
 int kvx_malloc(void** ptr, size_t n_bytes);
 int kvx_free(void* ptr);

@@ -58,6 +58,7 @@ SIGNATURES = {
     "kvx_ipc_close": [_P],
     "kvx_stream_signal": [_P, _U32, _P],
     "kvx_stream_wait": [_P, _U32, _P],
+    "kvx_memcpy_async": [_P, _P, _SZ, _P],
     "kvx_stream_wait_eq": [_P, _U32, _P],
     "kvx_stream_memops_supported": [ctypes.POINTER(_I)],
 }

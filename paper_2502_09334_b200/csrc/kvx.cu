@@ -835,6 +835,12 @@ int kvx_copy_peer(void* dst, int dst_dev, const void* src, int src_dev, size_t n
   return cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, n, static_cast<cudaStream_t>(stream));
 }
 
+int kvx_memcpy_async(void* dst, const void* src, size_t n, void* stream) {
+  if (n == 0) return KVX_OK;
+  if (!dst || !src) return KVX_ERR_INVALID_ARG;
+  return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+}
+
 int kvx_malloc(void** ptr, size_t n) {
   if (!ptr) return KVX_ERR_INVALID_ARG;
   return cudaMalloc(ptr, n ? n : 256);

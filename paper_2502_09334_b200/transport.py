@@ -679,6 +679,23 @@ class PairChannel:
         if stage_in is not None:
             cur.wait_stream(self.xfer)
 
+    def poll(self) -> bool:
+        """Decode end, pull modes: has the prefill side started publishing the
+        next hand-off (its first chunk's doorbell rang)?  A host-side check
+        (a 4-byte device-to-host read of this GPU's doorbell page) for a
+        serving loop that pulls queued KV between decode rounds without
+        launching a pull that would wait for an idle prefill side."""
+        assert self.role == "decode" and self.spec.mode in PULL_MODES
+        e = self.epoch + 1
+        h, p = self._slot(e), self._parity(e)
+        if getattr(self, "_poll_buf", None) is None:
+            self._poll_buf = torch.empty(1, dtype=torch.int32, pin_memory=True)
+            self._poll_stream = torch.cuda.Stream(self.device)
+        _lib.call("kvx_memcpy_async", self._poll_buf.data_ptr(), self._pready(self.flags.ptr, h, 0),
+                  4, _stream_ptr(self._poll_stream))
+        self._poll_stream.synchronize()
+        return int(self._poll_buf[0]) == (p ^ 1)
+
     def recv(self, dst: KVPlanes, n_tokens: int, timing: list | None = None,
              stage_out: tuple | None = None, seqlens=None) -> None:
         """Receive into ``dst``.  ``stage_out=((dev_k, dev_v), (host_k, host_v))``:

@@ -252,6 +252,10 @@ def main():
     for rnd in range(3):
         Ts = [Tmax, 77, 130]
         seeds = [5000 + 100 * rnd + 10 * i + ch.pair for i in range(Q)]
+        if ch.role == "decode" and ch.poll():  # nothing sent yet this round
+            failures += 1
+            print(f"POLL rank={rank} round={rnd}: saw a hand-off before it was sent", flush=True)
+        dist.barrier(ctrl)
         if ch.role == "prefill":
             kvs = [torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=sd)).to(dev)
                    for T, sd in zip(Ts, seeds)]
@@ -261,6 +265,9 @@ def main():
             dist.barrier(ctrl)
         else:
             dist.barrier(ctrl)  # the decode side starts only after P finished
+            if not ch.poll():
+                failures += 1
+                print(f"POLL rank={rank} round={rnd}: queued hand-off not visible", flush=True)
             for T, sd in zip(Ts, seeds):
                 slots_np = O.synthetic_slots(T, bs, nb, seed=sd)
                 kc.zero_(); vc.zero_()
