@@ -627,7 +627,10 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
             calibration=_calibration(spec, T, ms_max, float(g[:, 7].max()),
                                      host_us=float(g[:, 8].max())) if (
                 trace is None and not kivi) else None,
-            extra={"mode": mode, "n_chunks": len(spec.chunks()), "pairs": pairs,
+            extra={"mode": mode,
+                   "n_chunks": (len(ch._pull_chunks(lay)[0]) if mode in ("pull", "pull_ldg")
+                                and not kivi else len(spec.chunks())),
+                   "pairs": pairs,
                    "format": spec.format,
                    "cuda_graphs": bool(ch.graphs),
                    "queue_depth": ch.Q,
