@@ -393,6 +393,9 @@ cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, voi
   kb.parity = parity;
   kb.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
   kb.slab = kKchanStageCodes / (G * BITS / 8);  // channels per span (S/32 divides 256)
+  // rows that fit one span whole: the group's code rows are then a single
+  // contiguous range, one bulk copy instead of G (when S/32 still divides 256)
+  if (kg.row_elems <= kb.slab && 256 % (kg.row_elems / 32) == 0) kb.slab = kg.row_elems;
   if (kg.row_elems % 32 || !aligned(kg.codes, 16) || !aligned(kg.scale, 16) ||
       !aligned(kg.zero, 16) || kg.payload_ls % 16)
     return cudaSuccess;
@@ -406,7 +409,11 @@ cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, voi
   static bool attr_set[kMaxDev] = {false};
   if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
   if (!attr_set[dev]) {
-    cudaError_t attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    // the largest span of this instantiation (the slab shrinks for short rows)
+    const int s_max = kKchanStageCodes / (G * BITS / 8);
+    const int smem_max = kStages * (G * s_max * BITS / 8 + 4 * s_max);
+    cudaError_t attr =
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
     if (attr != cudaSuccess) return attr;
     attr_set[dev] = true;
   }

@@ -305,9 +305,14 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
         mbar_expect_tx(&full[st], G * rb + 2 * mb);
         uint8_t* buf = smem + st * kb.stage_bytes;
         const char* lc = g.codes + layer * g.payload_ls + int64_t(c0) * BITS / 8;
-        for (int j = 0; j < G; ++j)
-          bulk_g2s(buf + j * code_slice, lc + (grp * G + j) * int64_t(g.row_elems) * BITS / 8, rb,
-                   &full[st]);
+        if (ns == g.row_elems && code_slice == int(rb)) {
+          // the slab is whole rows: the group's G code rows are one range
+          bulk_g2s(buf, lc + grp * G * int64_t(g.row_elems) * BITS / 8, G * rb, &full[st]);
+        } else {
+          for (int j = 0; j < G; ++j)
+            bulk_g2s(buf + j * code_slice, lc + (grp * G + j) * int64_t(g.row_elems) * BITS / 8,
+                     rb, &full[st]);
+        }
         const int64_t meta = (grp * g.row_elems + c0) * 2;
         bulk_g2s(buf + G * code_slice, g.scale + layer * g.payload_ls + meta, mb, &full[st]);
         bulk_g2s(buf + G * code_slice + 2 * S, g.zero + layer * g.payload_ls + meta, mb,
