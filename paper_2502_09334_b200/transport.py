@@ -43,6 +43,8 @@ from __future__ import annotations
 
 import ctypes
 import os
+
+import numpy as np
 from dataclasses import dataclass
 
 import torch
@@ -492,13 +494,29 @@ class PairChannel:
         self._kivi_lpc = lpc
         return lay, gs, rt, chunks, self._slot(e), self._parity(e)
 
+    def _kivi_index(self, gs, rt, stream):
+        """Device copies of a batch's group starts / residual tokens, cached per
+        batch shape.  A synchronous upload from pageable memory would make the
+        host wait for the channel stream to drain, so a hand-off could never
+        be enqueued while the previous one runs."""
+        key = (gs.tobytes(), rt.tobytes())
+        cache = self.__dict__.setdefault("_kivi_idx", {})
+        hit = cache.get(key)
+        if hit is None:
+            if len(cache) >= 64:
+                cache.pop(next(iter(cache)))
+            host = torch.from_numpy(np.concatenate([gs, rt]).astype(np.int64)).pin_memory()
+            with torch.cuda.stream(stream):
+                dev = host.to(self.device, non_blocking=True)
+            dev.record_stream(stream)
+            hit = cache[key] = (dev[:len(gs)], dev[len(gs):], host)
+        return hit[0], hit[1]
+
     def _send_kivi(self, src, n_tokens, seqlens, e):
         lay, gs, rt, chunks, h, p = self._kivi_common(n_tokens, seqlens, e)
         s, cur = self.stream, torch.cuda.current_stream(self.device)
         s.wait_stream(cur)
-        with torch.cuda.stream(s):
-            gs_d = torch.from_numpy(gs).to(self.device, non_blocking=False)
-            rt_d = torch.from_numpy(rt).to(self.device, non_blocking=False)
+        gs_d, rt_d = self._kivi_index(gs, rt, s)
         base = self.k1_target + self._half(e)
         offs = (ctypes.c_int64 * 7)(*lay.offsets)
         wait_eq(self._pfree(self.flags.ptr, h), p, s)
@@ -511,17 +529,15 @@ class PairChannel:
                       base + l0 * lay.layer_stride, lay.layer_stride, offs, _stream_ptr(s))
             signal(self._pready(self.peer_flags, h, c), p ^ 1, s)
         signal(self._pstate(h), p ^ 1, s)
-        gs_d.record_stream(s)
-        rt_d.record_stream(s)
         cur.wait_stream(s)
 
     def _recv_kivi(self, dst, n_tokens, seqlens, e):
         lay, gs, rt, chunks, h, p = self._kivi_common(n_tokens, seqlens, e)
         s, cur = self.stream, torch.cuda.current_stream(self.device)
         s.wait_stream(cur)
+        gs_d, rt_d = self._kivi_index(gs, rt, s)
         with torch.cuda.stream(s):
-            gs_d = torch.from_numpy(gs).to(self.device)
-            rdst = dst.slots[torch.from_numpy(rt).to(self.device)].contiguous()
+            rdst = dst.slots[rt_d].contiguous()
         base = self.k3_source + self._half(e)
         offs = (ctypes.c_int64 * 7)(*lay.offsets)
 
@@ -545,7 +561,6 @@ class PairChannel:
                 _lib.call("kvx_dequant_scatter_paged_kivi", *args(l0, l1), _stream_ptr(s))
         signal(self._pfree(self.peer_flags, h), p ^ 1, s)
         signal(self._pstate(h), p ^ 1, s)
-        gs_d.record_stream(s)
         rdst.record_stream(s)
         cur.wait_stream(s)
 
