@@ -786,6 +786,7 @@ class PairChannel:
         if self.role is None:
             return
         torch.cuda.synchronize(self.device)
+        self._graphs, self._seen = {}, set()  # their kernels point at the buffers freed below
         if self.peer_flags:
             _lib.call("kvx_ipc_close", self.peer_flags)
             self.peer_flags = 0
