@@ -886,7 +886,16 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     const __half* sbuf = reinterpret_cast<const __half*>(buf + bg.rows_per_span * bg.code_row_bytes);
     const __half* zbuf = sbuf + bg.rows_per_span * bg.meta_row_bytes / 2;
     mbar_wait(&full[st], (k / STAGES) & 1);
-    for (int r = warp; r < rows; r += CONSUMERS) {
+    // short rows (fewer than 32 chunks, e.g. a TP shard's few KV heads): a
+    // warp covers 32 / cpr rows per pass so every lane has a chunk
+    const int cpr = bg.cpr;
+    const int rpw = (cpr < 32 && (32 % cpr) == 0) ? 32 / cpr : 1;
+    const int sub = rpw > 1 ? lane / cpr : 0;
+    const int cl = rpw > 1 ? lane % cpr : lane;
+    const int gpr = bg.meta_row_bytes / 2;
+    for (int rb = warp * rpw; rb < rows; rb += CONSUMERS * rpw) {
+      const int r = rb + sub;
+      if (r >= rows) continue;
       const int64_t lrow = r0 + r;
       const int p = lrow >= g.n_tokens;
       const int kv = g.plane0 + p;
@@ -895,8 +904,7 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
       if (pos < 0) continue;  // padding token
       char* dst = const_cast<char*>(row_ptr(g, plane_ptr(g, kv, layer), pos));
       const uint8_t* crow = buf + r * bg.code_row_bytes;
-      const int gpr = bg.meta_row_bytes / 2;
-      for (int c = lane; c < bg.cpr; c += 32) {
+      for (int c = cl; c < cpr; c += 32) {
         K3Data<BITS> d;
         if constexpr (BITS == 2) {
           const uint2 v = *reinterpret_cast<const uint2*>(crow + c * CB);
