@@ -124,7 +124,22 @@ kvx::FastDiv make_fastdiv(uint32_t d) {
 cudaError_t make_items(const kvx::Geo& g, kvx::ItemGeo& ig) {
   ig.cpr = g.row_elems / 32;
   const uint32_t ipr = uint32_t((ig.cpr + 31) / 32);
-  const int64_t n_items = g.n_token_rows * ipr;
+  int64_t n_items = g.n_token_rows * ipr;
+  ig.rpi_shift = 0;
+  ig.cpr_shift = 0;
+  ig.pt = 0;
+  ig.ipl = make_fastdiv(1);
+  if (ig.cpr > 0 && ig.cpr < 32 && (32 % ig.cpr) == 0 && g.n_tokens > 0) {
+    // short rows: pack 32 / cpr rows of one layer into each item
+    while ((1 << ig.cpr_shift) < ig.cpr) ++ig.cpr_shift;
+    ig.rpi_shift = 5 - ig.cpr_shift;
+    const int64_t pt = int64_t(g.planes) * g.n_tokens;
+    const int64_t ipl = (pt + (int64_t(1) << ig.rpi_shift) - 1) >> ig.rpi_shift;
+    if (pt >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    ig.pt = uint32_t(pt);
+    ig.ipl = make_fastdiv(uint32_t(ipl));
+    n_items = (g.n_token_rows / pt) * ipl;
+  }
   if (n_items >= (int64_t(1) << 31) || g.n_tokens >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   ig.ipr = make_fastdiv(ipr);
   ig.tokens = make_fastdiv(uint32_t(g.n_tokens));
@@ -176,7 +191,8 @@ cudaError_t launch_dequant(const kvx::Geo& g, const void* codes, const void* sca
   kvx::ItemGeo ig;
   cudaError_t e = make_items(g, ig);
   if (e != cudaSuccess) return e;
-  auto k = kvx::dequant_scatter_kernel<BITS, G>;
+  auto k = ig.rpi_shift ? kvx::dequant_scatter_kernel<BITS, G, true>
+                        : kvx::dequant_scatter_kernel<BITS, G, false>;
   k<<<grid_for(k, ig.n_items), kThreads, 0, s>>>(g, ig, static_cast<const uint8_t*>(codes),
                                                  static_cast<const __half*>(scale),
                                                  static_cast<const __half*>(zero));

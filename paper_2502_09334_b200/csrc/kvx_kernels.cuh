@@ -184,7 +184,32 @@ struct ItemGeo {
   FastDiv tokens;   // n_tokens
   int cpr;          // 32-element chunks per token row
   uint32_t n_items;
+  // short rows (cpr < 32, a power of two -- e.g. a TP shard's few KV heads):
+  // one item packs 2^rpi_shift consecutive rows of one layer so every lane
+  // has a chunk; rpi_shift == 0 is the one-row-per-item geometry
+  int rpi_shift;
+  int cpr_shift;    // log2(cpr) when rows are packed
+  FastDiv ipl;      // items per layer when rows are packed
+  uint32_t pt;      // token rows per layer (planes * n_tokens)
 };
+
+// (token row, chunk) of this lane's share of ``item``; false = no work
+// (beyond the row's chunks or the layer's rows; tr stays a valid row).
+template <bool PACKED = true>
+__device__ __forceinline__ bool item_row_chunk(const ItemGeo& ig, uint32_t item, int lane,
+                                               uint32_t& tr, int& c) {
+  if (!PACKED || ig.rpi_shift == 0) {
+    tr = fdiv(item, ig.ipr);
+    c = int(item - tr * ig.ipr.d) * 32 + lane;
+    return c < ig.cpr;
+  }
+  const uint32_t layer = fdiv(item, ig.ipl);
+  const uint32_t r = ((item - layer * ig.ipl.d) << ig.rpi_shift) + (uint32_t(lane) >> ig.cpr_shift);
+  c = lane & (ig.cpr - 1);
+  const bool ok = r < ig.pt;
+  tr = layer * ig.pt + (ok ? r : 0u);
+  return ok;
+}
 
 __device__ __forceinline__ void ld256(const void* p, uint32_t (&r)[8]) {
   asm volatile(
@@ -283,8 +308,9 @@ __device__ __forceinline__ K1Item k1_item(const Geo& g, const ItemGeo& ig, uint3
                                           uint8_t* codes, __half* scale, __half* zero) {
   constexpr int CB = 32 * BITS / 8;  // code bytes per chunk
   K1Item it;
-  const uint32_t tr = fdiv(item, ig.ipr);
-  const int c = int(item - tr * ig.ipr.d) * 32 + lane;  // chunk inside the token row
+  uint32_t tr;
+  int c;  // chunk inside the token row
+  const bool ok = item_row_chunk(ig, item, lane, tr, c);
   const uint32_t lk = fdiv(tr, ig.tokens);
   const uint32_t t = tr - lk * ig.tokens.d;
   const uint32_t layer = lk >> (g.planes - 1);
@@ -292,7 +318,7 @@ __device__ __forceinline__ K1Item k1_item(const Geo& g, const ItemGeo& ig, uint3
   const uint32_t lrow = tr - layer * g.planes * ig.tokens.d;
   const int64_t pos = pos_of(g, t);
   const char* plane = plane_ptr(g, kv, layer);
-  it.active = c < ig.cpr;
+  it.active = ok;
   it.src = row_ptr(g, plane, pos) + int64_t(c) * 64;
   it.codes = reinterpret_cast<char*>(codes) + int64_t(layer) * g.codes_ls +
              (int64_t(lrow) * ig.cpr + c) * CB;
@@ -592,14 +618,15 @@ struct K3Item {
   bool active;
 };
 
-template <int BITS, int G>
+template <int BITS, int G, bool PACKED>
 __device__ __forceinline__ K3Item k3_item(const Geo& g, const ItemGeo& ig, uint32_t item, int lane,
                                           const uint8_t* codes, const __half* scale,
                                           const __half* zero) {
   constexpr int CB = 32 * BITS / 8;
   K3Item it;
-  const uint32_t tr = fdiv(item, ig.ipr);
-  const int c = int(item - tr * ig.ipr.d) * 32 + lane;
+  uint32_t tr;
+  int c;
+  const bool ok = item_row_chunk<PACKED>(ig, item, lane, tr, c);
   const uint32_t lk = fdiv(tr, ig.tokens);
   const uint32_t t = tr - lk * ig.tokens.d;
   const uint32_t layer = lk >> (g.planes - 1);
@@ -607,7 +634,7 @@ __device__ __forceinline__ K3Item k3_item(const Geo& g, const ItemGeo& ig, uint3
   const uint32_t lrow = tr - layer * g.planes * ig.tokens.d;
   const int64_t pos = pos_of(g, t);
   char* plane = const_cast<char*>(plane_ptr(g, kv, layer));
-  it.active = (c < ig.cpr) && (pos >= 0);  // pos < 0: padding token, skipped
+  it.active = ok && (pos >= 0);  // pos < 0: padding token, skipped
   it.dst = const_cast<char*>(row_ptr(g, plane, pos)) + int64_t(c) * 64;
   it.codes = reinterpret_cast<const char*>(codes) + int64_t(layer) * g.codes_ls +
              (int64_t(lrow) * ig.cpr + c) * CB;
@@ -675,7 +702,9 @@ __device__ __forceinline__ void k3_process(const K3Item& it, const K3Data<BITS>&
 #ifndef KVX_K3_PF
 #define KVX_K3_PF 2  // items prefetched ahead per warp (A/B: profiles/r01_summary.md)
 #endif
-template <int BITS, int G>
+// PACKED: the short-row item geometry (ItemGeo::rpi_shift > 0), a separate
+// instantiation so the common one keeps its register budget (48 vs 58).
+template <int BITS, int G, bool PACKED = false>
 __global__ void __launch_bounds__(256) dequant_scatter_kernel(Geo g, ItemGeo ig,
                                                               const uint8_t* __restrict__ codes,
                                                               const __half* __restrict__ scale,
@@ -690,7 +719,7 @@ __global__ void __launch_bounds__(256) dequant_scatter_kernel(Geo g, ItemGeo ig,
   for (int i = 0; i < NB - 1; ++i) {
     const uint32_t itm = warp + i * n_warps;
     if (itm < ig.n_items) {
-      it[i] = k3_item<BITS, G>(g, ig, itm, lane, codes, scale, zero);
+      it[i] = k3_item<BITS, G, PACKED>(g, ig, itm, lane, codes, scale, zero);
       k3_load<BITS>(it[i], d[i]);
     }
   }
@@ -702,7 +731,7 @@ __global__ void __launch_bounds__(256) dequant_scatter_kernel(Geo g, ItemGeo ig,
       const uint32_t pre = cur + (NB - 1) * n_warps;
       const int pb = (st + NB - 1) % NB;
       if (pre < ig.n_items) {
-        it[pb] = k3_item<BITS, G>(g, ig, pre, lane, codes, scale, zero);
+        it[pb] = k3_item<BITS, G, PACKED>(g, ig, pre, lane, codes, scale, zero);
         k3_load<BITS>(it[pb], d[pb]);
       }
       k3_process<BITS>(it[st], d[st]);

@@ -231,25 +231,6 @@ class KVPlanes:
     def window_args(self):
         return (self.plane_heads or self.n_heads, self.head_offset)
 
-    def k1_rows(self, n_tokens: int):
-        """(tokens, heads, plane_heads, head_offset) to hand K1 for n_tokens.
-
-        K1 gives each warp item up to 32 chunks of 32 elements of ONE token
-        row, so a row shorter than 1024 elements (a TP shard's few KV heads)
-        leaves lanes idle.  A dense, unwindowed source stores consecutive
-        token rows back to back, and the payload lays out rows, groups and
-        codes in the same linear order, so k short rows can be packed as one
-        row of k times the heads with byte-identical results."""
-        row = self.n_heads * self.head_dim
-        cpr = row // 32
-        if (self.slots is None and self.head_offset == 0 and
-                (self.plane_heads or self.n_heads) == self.n_heads and
-                row % 32 == 0 and 0 < cpr < 32 and 32 % cpr == 0):
-            k = 32 // cpr
-            if n_tokens % k == 0:
-                return n_tokens // k, self.n_heads * k, 0, 0
-        return (n_tokens, self.n_heads, *self.window_args)
-
     @staticmethod
     def dense(kv: torch.Tensor) -> "KVPlanes":
         """kv: fp16 [L, 2, T, H, D] contiguous."""
@@ -304,10 +285,9 @@ def _quant_pack_layers(src: KVPlanes, packed: PackedKV, l0: int, l1: int, stream
     lay = packed.layout
     k, v = src.ptrs(l0)
     c, s, z = packed.ptrs(l0)
-    t, h, ph, ho = src.k1_rows(lay.n_tokens)
-    _lib.call("kvx_quant_pack", k, v, src.layer_stride, src.slots_ptr, l1 - l0, t, h,
-              lay.head_dim, lay.group, lay.bits, c, s, z, lay.layer_stride, ph, ho,
-              _stream_ptr(stream))
+    _lib.call("kvx_quant_pack", k, v, src.layer_stride, src.slots_ptr, l1 - l0, lay.n_tokens,
+              lay.n_heads, lay.head_dim, lay.group, lay.bits, c, s, z, lay.layer_stride,
+              *src.window_args, _stream_ptr(stream))
 
 
 def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,

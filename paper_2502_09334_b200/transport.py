@@ -396,10 +396,9 @@ class PairChannel:
                 ev = _kernel_events(timing, s, "k1")
                 k, v = src.ptrs(0)
                 c0, sc0, z0 = payload.ptrs(0)
-                t, hh, ph, ho = src.k1_rows(lay.n_tokens)
                 _lib.call("kvx_quant_pack_signal", k, v, src.layer_stride, src.slots_ptr,
-                          lay.n_layers, t, hh, lay.head_dim, lay.group,
-                          lay.bits, c0, sc0, z0, lay.layer_stride, ph, ho,
+                          lay.n_layers, lay.n_tokens, lay.n_heads, lay.head_dim, lay.group,
+                          lay.bits, c0, sc0, z0, lay.layer_stride, *src.window_args,
                           self.counters[h].data_ptr(), self._pready(self.peer_flags, h, 0), lpc,
                           self._pfree(self.flags.ptr, h), self._pstate(h), _stream_ptr(s))
                 _kernel_events_end(ev, s)
