@@ -167,6 +167,7 @@ cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero
   sig.counters = rq.counters;
   sig.peer_flags = rq.peer_flags;
   sig.items_per_chunk = 1;
+  sig.ipc = make_fastdiv(1);
   sig.parity = rq.parity;
   sig.free_flag = rq.free_flag;
   if (rq.peer_flags) {
@@ -174,6 +175,7 @@ cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero
     const int64_t ipc = per_layer * rq.layers_per_chunk;
     if (ipc <= 0 || ipc >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     sig.items_per_chunk = uint32_t(ipc);
+    sig.ipc = make_fastdiv(uint32_t(ipc));
     const int64_t n_chunks = (ig.n_items + ipc - 1) / ipc;
     if (n_chunks > kvx::kMaxSignalChunks) return cudaErrorInvalidValue;
     // (the counters are zero between launches: each chunk's last arrival resets its own)

@@ -418,6 +418,7 @@ struct SignalGeo {
   uint32_t* counters;
   uint32_t* peer_flags;  // [n_chunks] decode-side ready flags (IPC/peer mapped), or null
   uint32_t items_per_chunk;
+  FastDiv ipc;           // items_per_chunk as a multiply-shift (per-item chunk test)
   // queue-half parity p (nullable = 0): doorbells are set to p ^ 1; the last
   // CTA to exit flips *parity to p ^ 1 for the half's next use
   uint32_t* parity;
@@ -550,9 +551,9 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
       }
       k1_process<BITS, G>(it[st], w[st], lane);
       if (sig.peer_flags) {
-        const uint32_t c = cur / sig.items_per_chunk;
+        const uint32_t c = fdiv(cur, sig.ipc);
         const uint32_t nxt = cur + n_warps;
-        if (nxt >= ig.n_items || nxt / sig.items_per_chunk != c)
+        if (nxt >= ig.n_items || fdiv(nxt, sig.ipc) != c)
           chunk_arrive(sig, cta_cnt, c, ig.n_items, n_warps, lane, ready_value);
       }
     }
