@@ -9,6 +9,8 @@ share a GPU's link between edges.
 
 Prints one JSON line per scenario: GB/s of fp16-equivalent KV handed off
 (the whole replica's KV per step), max over ranks of CUDA-event time.
+--paged-src: the prefill ranks hand off from their own paged caches (a slot
+mapping per token) instead of dense KV.
 """
 import json
 import os
@@ -26,6 +28,7 @@ from paper_2502_09334_b200.transport import TPHandoff  # noqa: E402
 
 
 def main():
+    paged_src = "--paged-src" in sys.argv
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
@@ -39,8 +42,13 @@ def main():
         tp = TPHandoff(L, T, H, D, pr, dr, rank, world, ctrl)
         if rank in pr:
             hp = H // len(pr)
-            kv = B.synthetic_kv_device(torch, L, T, hp, D, dev, seed=rank)
-            step = lambda: tp.send(KVPlanes.dense(kv), T)  # noqa: E731
+            if paged_src:
+                sl, nbp = B.paged_slots(torch, T, dev, seed=rank)
+                pk = torch.randn((L, nbp, B.BLOCK, hp, D), device=dev).half()
+                src = KVPlanes.paged(pk, torch.randn_like(pk), sl)
+            else:
+                src = KVPlanes.dense(B.synthetic_kv_device(torch, L, T, hp, D, dev, seed=rank))
+            step = lambda: tp.send(src, T)  # noqa: E731
         elif rank in dr:
             hd = H // len(dr)
             slots, nb = B.paged_slots(torch, T, dev)
@@ -66,7 +74,8 @@ def main():
         dist.barrier()
         if rank == 0:
             fp16 = L * 2 * T * H * D * 2
-            print(json.dumps({"scenario": name, "prefill_ranks": pr, "decode_ranks": dr,
+            print(json.dumps({"scenario": name, "prefill_source": "paged" if paged_src else "dense",
+                              "prefill_ranks": pr, "decode_ranks": dr,
                               "edges": len(tp.edges) if rank in pr or rank in dr else None,
                               "ms_per_step": round(float(ms), 4),
                               "GBps_fp16_eq": round(fp16 / (float(ms) * 1e-3) / 1e9, 1)}),
