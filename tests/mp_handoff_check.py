@@ -188,61 +188,62 @@ def main():
     # fused graph-replayed hand-off, the staged host-buffer path (per-chunk K1
     # + memops on P), layer-wise streaming, and empty hand-offs -- all share
     # the queue halves and the parity doorbells
-    spec = ChannelSpec(L, Tmax, H, D, 4, 128, 3, "pull")
-    ch = PairChannel(spec, rank, world, control_group=ctrl)
-    rng = np.random.default_rng(123)
-    nb = Tmax // bs + 4
-    kv_cap = torch.zeros((L, 2, Tmax, H, D), dtype=torch.float16, device=dev)
-    slots_buf = torch.zeros(Tmax, dtype=torch.int64, device=dev)
-    kc = torch.zeros((L, nb, bs, H, D), dtype=torch.float16, device=dev)
-    vc = torch.zeros_like(kc)
-    for epoch in range(40):
-        path = rng.choice(["fused", "fused", "fused", "staged", "layerwise", "empty"])
-        T = 0 if path == "empty" else int(rng.choice([Tmax, 77, 130]))
-        seed = 9000 + 1000 * ch.pair + epoch
-        if ch.role == "prefill":
-            if T:
-                kv_cap[:, :, :T].copy_(torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=seed)))
-            src = KVPlanes.dense(kv_cap)
-            if path == "staged":
-                host = kv_cap.cpu().pin_memory()
-                ch.send(src, T, stage_in=(host, kv_cap))
-            elif path == "layerwise":
-                sess = ch.open_send(src, T)
-                for l in range(1, L + 1):
-                    sess.layers_ready(l)
-                sess.close()
+    for Q in (2, 1, 3):  # queue depths (1: no run-ahead at all)
+        spec = ChannelSpec(L, Tmax, H, D, 4, 128, 3, "pull", queue_depth=Q)
+        ch = PairChannel(spec, rank, world, control_group=ctrl)
+        rng = np.random.default_rng(123 + Q)
+        nb = Tmax // bs + 4
+        kv_cap = torch.zeros((L, 2, Tmax, H, D), dtype=torch.float16, device=dev)
+        slots_buf = torch.zeros(Tmax, dtype=torch.int64, device=dev)
+        kc = torch.zeros((L, nb, bs, H, D), dtype=torch.float16, device=dev)
+        vc = torch.zeros_like(kc)
+        for epoch in range(40 if Q == 2 else 24):
+            path = rng.choice(["fused", "fused", "fused", "staged", "layerwise", "empty"])
+            T = 0 if path == "empty" else int(rng.choice([Tmax, 77, 130]))
+            seed = 9000 + 1000 * ch.pair + epoch
+            if ch.role == "prefill":
+                if T:
+                    kv_cap[:, :, :T].copy_(torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=seed)))
+                src = KVPlanes.dense(kv_cap)
+                if path == "staged":
+                    host = kv_cap.cpu().pin_memory()
+                    ch.send(src, T, stage_in=(host, kv_cap))
+                elif path == "layerwise":
+                    sess = ch.open_send(src, T)
+                    for l in range(1, L + 1):
+                        sess.layers_ready(l)
+                    sess.close()
+                else:
+                    ch.send(src, T)
+                torch.cuda.synchronize()
             else:
-                ch.send(src, T)
-            torch.cuda.synchronize()
-        else:
-            slots_np = O.synthetic_slots(T, bs, nb, seed=seed) if T else np.zeros(0, np.int64)
-            slots_buf[:T].copy_(torch.from_numpy(slots_np))
-            kc.zero_(); vc.zero_()
-            dst = KVPlanes.paged(kc, vc, slots_buf[:T])
-            if path == "staged":
-                hk = torch.zeros_like(kc, device="cpu").pin_memory()
-                hv = torch.zeros_like(vc, device="cpu").pin_memory()
-                ch.recv(dst, T, stage_out=((kc, vc), (hk, hv)))
-            else:
-                ch.recv(dst, T)
-            torch.cuda.synchronize()
-            if T:
-                okc = np.zeros((L, nb, bs, H, D), np.float16); ovc = okc.copy()
-                c, s_, z = O.quant_pack(O.synthetic_kv(L, T, H, D, seed=seed).reshape(-1, D), 4, 128)
-                O.scatter_paged(O.unpack_dequant(c, s_, z, 4, 128, D).reshape(L, 2, T, H, D),
-                                slots_np, okc, ovc)
-                gk, gv = (hk.numpy(), hv.numpy()) if path == "staged" else (kc.cpu().numpy(),
-                                                                             vc.cpu().numpy())
-                if not (np.array_equal(gk.view(np.uint16), okc.view(np.uint16)) and
-                        np.array_equal(gv.view(np.uint16), ovc.view(np.uint16))):
-                    failures += 1
-                    print(f"MISMATCH mixed rank={rank} epoch={epoch} path={path} T={T}",
-                          flush=True)
-    if rank == 0:
-        print(f"mixed paths: graphs={ch.graphs} captured={len(ch._graphs)}", flush=True)
-    dist.barrier()
-    ch.close()
+                slots_np = O.synthetic_slots(T, bs, nb, seed=seed) if T else np.zeros(0, np.int64)
+                slots_buf[:T].copy_(torch.from_numpy(slots_np))
+                kc.zero_(); vc.zero_()
+                dst = KVPlanes.paged(kc, vc, slots_buf[:T])
+                if path == "staged":
+                    hk = torch.zeros_like(kc, device="cpu").pin_memory()
+                    hv = torch.zeros_like(vc, device="cpu").pin_memory()
+                    ch.recv(dst, T, stage_out=((kc, vc), (hk, hv)))
+                else:
+                    ch.recv(dst, T)
+                torch.cuda.synchronize()
+                if T:
+                    okc = np.zeros((L, nb, bs, H, D), np.float16); ovc = okc.copy()
+                    c, s_, z = O.quant_pack(O.synthetic_kv(L, T, H, D, seed=seed).reshape(-1, D), 4, 128)
+                    O.scatter_paged(O.unpack_dequant(c, s_, z, 4, 128, D).reshape(L, 2, T, H, D),
+                                    slots_np, okc, ovc)
+                    gk, gv = (hk.numpy(), hv.numpy()) if path == "staged" else (kc.cpu().numpy(),
+                                                                                 vc.cpu().numpy())
+                    if not (np.array_equal(gk.view(np.uint16), okc.view(np.uint16)) and
+                            np.array_equal(gv.view(np.uint16), ovc.view(np.uint16))):
+                        failures += 1
+                        print(f"MISMATCH mixed Q={Q} rank={rank} epoch={epoch} path={path} T={T}",
+                              flush=True)
+        if rank == 0:
+            print(f"mixed paths Q={Q}: graphs={ch.graphs} captured={len(ch._graphs)}", flush=True)
+        dist.barrier()
+        ch.close()
 
     # a deeper queue: with queue_depth=3 the prefill side completes 3 hand-offs
     # before the decode side pulls any of them (with 2 slots the 3rd would wait)
