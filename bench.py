@@ -83,6 +83,7 @@ def peaks():
 # profiles/r01_nvlink/nvlink_bench.jsonl: 782-783 GB/s; copy engines 777,
 # B200_PROFILING.md's peer copy 770; 900 nominal)
 NVLINK_GBS = 783.0
+L2_BYTES = 126 * 2**20  # B200 L2
 
 
 # ---------------------------------------------------------------------------
@@ -702,12 +703,15 @@ def emit(args, r, world):
     out = {
         "metric": METRIC, "value": round(r["value"], 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms"], 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16->u4",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp16" if args.bits == 16 else f"fp16->u{args.bits}",
         "data": "synthetic",
         "config": {"workload": r["workload"], "bits": args.bits, "group": args.group,
                    "block_size": BLOCK, "fp16_bytes_per_step": r["fp16_bytes"],
                    "wire_bytes_per_step": r["wire_bytes"],
-                   "l2": "inputs larger than L2 (no flush)", **r.get("extra", {})},
+                   "l2": ("inputs larger than L2 (no flush)" if r["fp16_bytes"] > L2_BYTES else
+                          "inputs fit in L2 (126 MB): a latency-bound workload, no bandwidth "
+                          "claim"), **r.get("extra", {})},
         "roofline": r["roofline"],
         "cpu_baseline": r["cpu"],
         "e2e": r["e2e"],
