@@ -659,7 +659,8 @@ def main():
                     help="payload format: per-token groups, or KIVI per-channel K + residual")
     ap.add_argument("--group", type=int, default=128)
     ap.add_argument("--chunks", type=int, default=None,
-                    help="layer chunks per hand-off (default: 1 at N=1, 8 per pair at N>1)")
+                    help="layer chunks per hand-off (default: 1 at N=1; 8 per pair at N>1 for "
+                    "the non-fused paths -- the fused pull picks layer-granular chunks itself)")
     ap.add_argument("--mode", default="pull", choices=["pull", "pull_ldg", "push", "copy", "nccl"])
     ap.add_argument("--k3", default="ldg", choices=["ldg", "bulk"],
                     help="N=1: K3 variant (per-lane loads or TMA bulk staging)")
