@@ -389,7 +389,8 @@ def _calibration(spec, T, ms_large, ms_small, t_small=16, host_us=None):
     return {"alpha_us": round(alpha * 1e6, 2), "beta_GBps_of_modelled_volume": round(beta / 1e9, 1),
             "small_handoff_us": round(ms_small * 1e3, 2), "small_tokens": t_small,
             "host_enqueue_us_per_handoff": round(host_us, 2) if host_us is not None else None,
-            "note": "t = alpha + (2*b*s*h*bits/8*L)/beta, per pair, CUDA-graph replayed"}
+            "note": "t = alpha + (2*b*s*h*bits/8*L)/beta, per pair, back-to-back native "
+                    "launches on the caller's stream"}
 
 
 def run_pairs(args, torch, rank: int, world: int) -> None:
@@ -419,8 +420,9 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
     n_chunks = args.chunks or 8
     spec = ChannelSpec(L, T, H, D, args.bits, args.group, n_chunks, mode,
                        format=getattr(args, "format", "default"),
-                       queue_depth=getattr(args, "queue_depth", 2))
-    ch = PairChannel(spec, rank, world, control_group=ctrl, graphs=not args.no_graphs)
+                       queue_depth=getattr(args, "queue_depth", 2),
+                       pdl=not args.no_pdl, gate_recv=args.gate_recv)
+    ch = PairChannel(spec, rank, world, control_group=ctrl)
     lay = spec.layout(T)
     # per step token counts (fixed workload, or the trace's batches)
     tok = [T] * (args.warmup + args.steps + 2) if trace is None else [sum(x) for x in trace]
@@ -480,11 +482,7 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                     ch.recv(planes_b[i], next_t(), seqlens=seqs[i])
                 else:
                     ch.recv(planes_b[i], next_t(), timing)
-    # a fixed-size hand-off is captured as a CUDA graph on its 2nd use of each
-    # queue slot: make sure that capture happens before the timed region even
-    # when the caller asks for fewer warm-up steps (untimed, like compilation)
-    prime = 0 if (trace is not None or kivi) else max(0, 2 * ch.Q - args.warmup)
-    for _ in range(prime + args.warmup):
+    for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     dist.barrier()
@@ -493,14 +491,14 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
     with B.ClockSampler(local) as clk:
         t0.record()
         for _ in range(args.steps):
-            step()  # CUDA-graph replay per hand-off once warmed up (pull modes)
+            step()  # one native kernel launch per end and hand-off (fused pull)
         t1.record()
         torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
     # per-kernel durations: a separate eager pass with CUDA events on the
-    # launching streams (events cannot sit inside the captured graph)
+    # launching streams (events between launches break the PDL chaining)
     timing = []
     n_kt = max(1, min(args.steps, 5))
     for _ in range(n_kt):
@@ -511,7 +509,7 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
     for name, a, b_ in timing:
         kern[name] = kern.get(name, 0.0) + a.elapsed_time(b_) / n_kt
     launches = len(timing) / n_kt * args.steps
-    # alpha-beta calibration of this very channel (graph-replayed pull): a
+    # alpha-beta calibration of this very channel (native pull): a
     # 16-token hand-off against the main one -> kv_comm_cost's (alpha, beta)
     # for the reference's volume at this bit-width
     cal_small_ms, host_us = 0.0, 0.0
@@ -633,9 +631,9 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                                 and not kivi else len(spec.chunks())),
                    "pairs": pairs,
                    "format": spec.format,
-                   "cuda_graphs": bool(ch.graphs),
+                   "native_pair": ch._pair is not None,
+                   "pdl": spec.pdl, "gate_recv": spec.gate_recv,
                    "queue_depth": ch.Q,
-                   "graph_priming_steps": prime,
                    **({"trace_batches_timed": tok[args.warmup:args.warmup + args.steps],
                        "trace": "lengths log-uniform [128, 8192], 1-16 req/batch, <=16384 "
                                 "tokens/batch, rng(0)"} if trace is not None else {}),
@@ -674,8 +672,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--queue-depth", type=int, default=2,
                     help="pull: queue slots per pair in the prefill GPU's HBM")
-    ap.add_argument("--no-graphs", action="store_true",
-                    help="N>1: launch every hand-off eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--no-pdl", action="store_true",
+                    help="N>1: no programmatic dependent launch between consecutive pulls")
+    ap.add_argument("--gate-recv", action="store_true",
+                    help="N>1: hold each pull in the GPU front-end until chunk 0 is published")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps

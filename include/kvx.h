@@ -22,7 +22,8 @@
  *  - Every compute/transfer call is stream-ordered and asynchronous; `stream`
  *    is a cudaStream_t passed as void* (NULL = legacy default stream).
  *  - Return 0 on success, else a kvx/cuda error code; kvx_strerror() names it.
- *    No exceptions cross the ABI.  Re-entrant across host threads.
+ *    No exceptions cross the ABI.  Re-entrant across host threads (the
+ *    per-device launch caches are atomics / mutex-guarded).
  *  - Device pointers may be local, peer-mapped (kvx_enable_peer) or
  *    IPC-mapped (kvx_ipc_open): a quantise kernel writing into a peer buffer
  *    is the fused quantise+NVLink-push path, a dequantise kernel reading from
@@ -41,7 +42,8 @@
  *      scale  fp16  [2*T*H][head_dim/group]
  *      zero   fp16  [2*T*H][head_dim/group]
  *    payload_layer_stride == 0: three dense arrays, layers back to back in
- *    each.  payload_layer_stride > 0 (bytes, multiple of 16): one segment per
+ *    each.  payload_layer_stride > 0 (bytes, multiple of 16; of 32 at 8 bits,
+ *    whose codes move as 32-byte vectors): one segment per
  *    layer, codes/scale/zero of layer l at codes/scale/zero + l*stride -- a
  *    range of layers is then ONE contiguous byte range (one NVLink copy or
  *    one doorbell per layer chunk).
@@ -98,29 +100,30 @@ int kvx_quant_pack(const void* k_src, const void* v_src, int64_t src_layer_strid
  * K1 with device-side doorbells (fused quantise -> NVLink pull pipeline):
  * same contract as kvx_quant_pack (bits 2/4/8), plus for every chunk of
  * layers_per_chunk layers the kernel itself sets peer_ready_flags[chunk] =
- * p ^ 1 (a peer/IPC-mapped address on the decode GPU; fence.sys +
- * st.release.sys) as soon as the chunk's payload is complete, while it keeps
- * quantising later layers.
- * counters: 65 u32 of scratch on this GPU, zero before the first call (the
+ * ready_value (a peer/IPC-mapped address on the decode GPU; st.release.sys)
+ * as soon as the chunk's payload is complete, while it keeps quantising
+ * later layers.
+ * counters: 64 u32 of scratch on this GPU, zero before the first call (the
  * kernel leaves them zero again).
- * parity_state (nullable = parity 0, never flipped): a u32 on this GPU
- * holding the queue half's parity p; the last CTA to exit flips it.
  * free_flag (nullable, this GPU's memory): before storing anything, every
- * CTA waits (bounded, in-kernel) until *free_flag == p -- the decode side's
- * "queue half consumed" flag -- so a hand-off needs no stream-memop nodes.
- * Transport protocol (every flag value is read from device state, so a
- * captured CUDA graph replays unchanged; no flag is ever reset, so there is
- * no lost wake-up): the u-th use of a queue half has p = u & 1, rings
- * ready = p ^ 1 and, once the decode side has consumed it, finds
- * free = p ^ 1 -- which is what the half's next use (parity p ^ 1) waits for.
+ * CTA waits (in-kernel, bounded, abortable through ctl) until
+ * *free_flag >= free_value -- the decode side's "queue slot consumed"
+ * sequence number.
+ * Sequence protocol (replaces round 1's parity flags): hand-off e uses
+ * queue slot h = e % Q for the v-th time, v = (e - 1) / Q + 1; the prefill
+ * side waits free[h] >= v - 1 and rings ready[h][c] = v, the decode side
+ * waits ready[h][c] >= v and sets free[h] = v.  Values only grow, every wait
+ * is the wrap-safe (int32)(flag - value) >= 0, so a doorbell left by an
+ * earlier (longer) use of the slot can never satisfy a later wait.
+ * ctl (nullable): a kvx_ctl_alloc'd control block; see below.
  */
 int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_layer_stride,
                           const int64_t* src_slots, int64_t n_layers, int64_t n_tokens,
                           int n_heads, int head_dim, int group, int bits, void* codes,
                           void* scale, void* zero, int64_t payload_layer_stride,
                           int plane_heads, int head_offset, void* counters,
-                          void* peer_ready_flags, int layers_per_chunk, const void* free_flag,
-                          void* parity_state, void* stream);
+                          void* peer_ready_flags, int layers_per_chunk, uint32_t ready_value,
+                          const void* free_flag, uint32_t free_value, void* ctl, void* stream);
 
 /*
  * K3: unpack + dequantise + scatter into the decode side's paged KV cache.
@@ -145,26 +148,31 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
  * per span of token rows) -- the fused NVLink-pull variant for a payload that
  * lives in the prefill GPU's HBM.
  * ready_flags (nullable, this GPU's memory): the kernel itself waits, per
- * chunk of layers_per_chunk layers, until ready_flags[chunk] == p ^ 1 (p =
- * *parity_state, or 0 without one), so ONE launch consumes a whole hand-off
- * while the prefill GPU is still producing it (kvx_quant_pack_signal, or
- * kvx_stream_signal after each chunk's K1).  Without flags, shapes whose rows
- * are not 16-byte multiples fall back to the per-lane kernel; with flags they
- * return KVX_ERR_UNSUPPORTED (see kvx_pull_supported).
+ * chunk of layers_per_chunk layers, until ready_flags[chunk] >= ready_value,
+ * so ONE launch consumes a whole hand-off while the prefill GPU is still
+ * producing it (kvx_quant_pack_signal, or kvx_stream_signal after each
+ * chunk's K1).  Without flags, shapes whose rows are not 16-byte multiples
+ * fall back to the per-lane kernel; with flags they return
+ * KVX_ERR_UNSUPPORTED (see kvx_pull_supported).
  * done_counter / peer_free_flag (nullable, together): in-kernel completion --
- * the last CTA zeroes *done_counter (a u32 on this GPU, 0 before the first
- * call), sets *peer_free_flag = p ^ 1 (a peer/IPC-mapped u32 on the prefill
- * GPU: "queue half consumed") and flips *parity_state (this GPU's parity of
- * the half; requires done_counter).
+ * done_counter is a u32 on this GPU (0 before the first call, left 0); the
+ * last CTA sets *peer_free_flag = ready_value (a peer/IPC-mapped u32 on the
+ * prefill GPU: "queue slot consumed") unless the wait was aborted.
+ * flags: KVX_PULL_PDL launches with programmatic stream serialization -- the
+ * kernel's producer may start pulling this hand-off's slot while the
+ * stream's previous kernel (typically the previous hand-off's pull) is still
+ * running; everything that touches stream-ordered memory (the slot mapping,
+ * the cache, done_counter) waits for it (griddepcontrol.wait).
  */
+#define KVX_PULL_PDL 1
 int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
                                    int64_t payload_layer_stride, const int64_t* dst_slots,
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
                                    int64_t dst_layer_stride, int plane_heads, int head_offset,
-                                   const void* ready_flags, int layers_per_chunk,
-                                   void* done_counter, void* peer_free_flag, void* parity_state,
-                                   void* stream);
+                                   const void* ready_flags, uint32_t ready_value,
+                                   int layers_per_chunk, void* done_counter, void* peer_free_flag,
+                                   void* ctl, int flags, void* stream);
 
 /* 1 if kvx_pull_dequant_scatter_paged can bulk-stage this shape. */
 int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, int bits);
@@ -200,11 +208,13 @@ int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_st
  * (TMA) before they are dequantised -- the kivi format's pull transport.
  * Shapes that cannot be bulk-staged fall back to the per-lane kernels.
  * ready_flags (nullable, this GPU's memory): the kernels wait in-kernel, per
- * chunk of layers_per_chunk layers, until ready_flags[chunk] == p ^ 1 (p =
- * *parity_state, read only; or 0), so ONE call consumes a whole hand-off
- * while the prefill side is still publishing it; the caller releases the
- * queue slot after the call (stream order).  With flags, shapes that cannot
- * be bulk-staged return KVX_ERR_UNSUPPORTED. */
+ * chunk of layers_per_chunk layers, until ready_flags[chunk] >= ready_value,
+ * so ONE call consumes a whole hand-off while the prefill side is still
+ * publishing it; the caller releases the queue slot after the call (stream
+ * order).  With flags, shapes that cannot be bulk-staged return
+ * KVX_ERR_UNSUPPORTED.  ctl as for kvx_quant_pack_signal.
+ * 8-bit: seg_offsets[4] (V codes) and payload_layer_stride must be 32-byte
+ * multiples (32-byte vector accesses). */
 int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_stride,
                                         const int64_t* seg_offsets, const int64_t* dst_slots,
                                         const int64_t* group_starts, int64_t n_groups,
@@ -212,8 +222,8 @@ int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_lay
                                         int64_t n_layers, int64_t n_tokens, int n_heads,
                                         int head_dim, int group, int bits, void* k_cache,
                                         void* v_cache, int64_t dst_layer_stride,
-                                        const void* ready_flags, int layers_per_chunk,
-                                        const void* parity_state, void* stream);
+                                        const void* ready_flags, uint32_t ready_value,
+                                        int layers_per_chunk, void* ctl, void* stream);
 
 /* Packed payload sizes in bytes for n_rows rows (codes, scale, zero). */
 int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t* codes_bytes,
@@ -260,6 +270,74 @@ int kvx_stream_wait(const void* flag, uint32_t value, void* stream);
 int kvx_stream_wait_eq(const void* flag, uint32_t value, void* stream);
 /* 1 if stream memory operations are usable on the current device. */
 int kvx_stream_memops_supported(int* supported);
+
+/* ---- control block: abort and timeout of the in-kernel waits ------------- */
+
+/* A channel's control block, in host memory mapped into every GPU (UVA: the
+ * kernels use the host address).  The host sets `abort` to make every
+ * kernel spinning on one of the channel's doorbells wind down; a kernel whose
+ * wait is aborted or outlives `timeout_ns` (0 = 60 s) records
+ * KVX_STATUS_ABORTED / KVX_STATUS_TIMEOUT in `status` and exits cleanly
+ * instead of trapping -- the CUDA context and the decode GPU's cache survive
+ * a lost partner; the Python layer raises PartnerLost (a NoPath). */
+typedef struct kvx_ctl {
+  uint32_t abort;      /* host -> device: nonzero = give up waiting      */
+  uint32_t status;     /* device -> host: 0 ok, KVX_STATUS_*              */
+  uint64_t timeout_ns; /* bound of every in-kernel wait (0 = 60 s)        */
+} kvx_ctl;
+#define KVX_STATUS_OK 0
+#define KVX_STATUS_ABORTED 1
+#define KVX_STATUS_TIMEOUT 2
+int kvx_ctl_alloc(void** ctl_out); /* zeroed, cudaHostAlloc(Mapped|Portable) */
+int kvx_ctl_free(void* ctl);
+
+/* ---- the pair channel: one end of a prefill -> decode pair ---------------- */
+
+/* Layer chunks of one pull hand-off of n_tokens tokens (identical on both
+ * ends): layer-granular doorbells (<= 64 chunks) with at least 4 K1 items per
+ * resident K1 warp in each, or every layer its own chunk (<= 64) when
+ * `layerwise` (streaming during prefill). */
+int kvx_handoff_chunk_plan(int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                           int layerwise, int* layers_per_chunk, int* n_chunks);
+
+/* One end of a prefill -> decode pair over the sequence protocol above,
+ * mirroring the paper's pre-built P2P group pool with KV queues in prefill
+ * GPU memory.  The caller maps the memory (CUDA IPC or peer
+ * access) and owns it:
+ *   local_flags / peer_flags: this GPU's and the partner's 4 KB doorbell
+ *     pages (u32 ready[8][64] at 0, free[8] at 512);
+ *   payload: the prefill GPU's queue, queue_depth slots of slot_bytes
+ *     (256-B aligned, each >= n_layers * the 256-B aligned per-layer segment
+ *     of max_tokens tokens); local on the prefill end, mapped on the decode
+ *     end;  ctl: nullable control block.
+ * The pair allocates Q x 65 u32 of device scratch at creation; send/recv
+ * never allocate.  Hand-off e (1, 2, ... in the same order on both ends) is
+ * ONE kernel launch per end:
+ *   kvx_pair_send: K1 with device doorbells into slot e % Q (KVX_PAIR_GATE:
+ *     first a stream memop holding the launch in the GPU front-end until the
+ *     decode side has freed the slot -- a lagging partner holds no SMs);
+ *   kvx_pair_recv: K3-bulk pulling the slot over NVLink as chunks are
+ *     published, freeing it in-kernel (KVX_PAIR_GATE: launch once chunk 0 is
+ *     published; KVX_PAIR_PDL: programmatic dependent launch, so a pull
+ *     streams its slot while the previous hand-off's pull drains).
+ * Validation: n_tokens <= max_tokens, the head window inside the planes, the
+ * current device == the creating device.  Replaces the kv_delay the
+ * reference charges per request (simulate.py:221-235). */
+#define KVX_ROLE_PREFILL 0
+#define KVX_ROLE_DECODE 1
+#define KVX_PAIR_GATE 1
+#define KVX_PAIR_PDL 2
+int kvx_pair_create(int role, int64_t n_layers, int64_t max_tokens, int n_heads, int head_dim,
+                    int bits, int group, int queue_depth, int layerwise, void* local_flags,
+                    void* peer_flags, void* payload, int64_t slot_bytes, void* ctl,
+                    void** pair_out);
+int kvx_pair_send(void* pair, uint64_t epoch, const void* k_src, const void* v_src,
+                  int64_t src_layer_stride, const int64_t* src_slots, int64_t n_tokens,
+                  int plane_heads, int head_offset, int flags, void* stream);
+int kvx_pair_recv(void* pair, uint64_t epoch, void* k_cache, void* v_cache,
+                  int64_t dst_layer_stride, const int64_t* dst_slots, int64_t n_tokens,
+                  int plane_heads, int head_offset, int flags, void* stream);
+int kvx_pair_destroy(void* pair);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,7 @@ _I = ctypes.c_int
 _I64 = ctypes.c_int64
 _U32 = ctypes.c_uint32
 _SZ = ctypes.c_size_t
+_U64 = ctypes.c_uint64
 
 # name -> argtypes (restype is int for every entry point except kvx_strerror)
 SIGNATURES = {
@@ -33,18 +34,18 @@ SIGNATURES = {
     "kvx_device_count": [ctypes.POINTER(_I)],
     "kvx_quant_pack": [_P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _I64, _I, _I, _P],
     "kvx_quant_pack_signal": [_P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _I64,
-                              _I, _I, _P, _P, _I, _P, _P, _P],
+                              _I, _I, _P, _P, _I, _U32, _P, _U32, _P, _P],
     "kvx_dequant_scatter_paged": [_P, _P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P, _I64,
                                   _I, _I, _P],
     "kvx_pull_dequant_scatter_paged": [_P, _P, _P, _I64, _P, _I64, _I64, _I, _I, _I, _I, _P, _P,
-                                       _I64, _I, _I, _P, _I, _P, _P, _P, _P],
+                                       _I64, _I, _I, _P, _U32, _I, _P, _P, _P, _I, _P],
     "kvx_pull_supported": [_I64, _I, _I, _I, _I],
     "kvx_quant_pack_kivi": [_P, _P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _I64, _P,
                             _I64, _P, _P],
     "kvx_dequant_scatter_paged_kivi": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _I, _I,
                                        _I, _I, _P, _P, _I64, _P],
     "kvx_pull_dequant_scatter_paged_kivi": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _I,
-                                            _I, _I, _I, _P, _P, _I64, _P, _I, _P, _P],
+                                            _I, _I, _I, _P, _P, _I64, _P, _U32, _I, _P, _P],
     "kvx_packed_sizes": [_I64, _I, _I, _I, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                          ctypes.POINTER(_I64)],
     "kvx_enable_peer": [_I, _I],
@@ -61,7 +62,21 @@ SIGNATURES = {
     "kvx_memcpy_async": [_P, _P, _SZ, _P],
     "kvx_stream_wait_eq": [_P, _U32, _P],
     "kvx_stream_memops_supported": [ctypes.POINTER(_I)],
+    "kvx_ctl_alloc": [ctypes.POINTER(_P)],
+    "kvx_ctl_free": [_P],
+    "kvx_handoff_chunk_plan": [_I64, _I64, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)],
+    "kvx_pair_create": [_I, _I64, _I64, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I64, _P,
+                        ctypes.POINTER(_P)],
+    "kvx_pair_send": [_P, _U64, _P, _P, _I64, _P, _I64, _I, _I, _I, _P],
+    "kvx_pair_recv": [_P, _U64, _P, _P, _I64, _P, _I64, _I, _I, _I, _P],
+    "kvx_pair_destroy": [_P],
 }
+
+# constants of include/kvx.h
+KVX_PULL_PDL = 1
+KVX_ROLE_PREFILL, KVX_ROLE_DECODE = 0, 1
+KVX_PAIR_GATE, KVX_PAIR_PDL = 1, 2
+KVX_STATUS_OK, KVX_STATUS_ABORTED, KVX_STATUS_TIMEOUT = 0, 1, 2
 
 _lib = None
 _lock = threading.Lock()

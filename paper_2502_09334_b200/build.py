@@ -13,6 +13,7 @@ SO_PATH = os.path.join(HERE, "_kvx.so")
 SOURCES = [os.path.join(HERE, "csrc", "kvx.cu")]
 DEPS = SOURCES + [
     os.path.join(HERE, "csrc", "kvx_kernels.cuh"),
+    os.path.join(HERE, "csrc", "kvx_kivi.cuh"),
     os.path.join(os.path.dirname(HERE), "include", "kvx.h"),
 ]
 NVCC_FLAGS = [

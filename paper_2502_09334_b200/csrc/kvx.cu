@@ -6,7 +6,12 @@
 #include <cuda.h>  // driver API types only; entry points resolved at run time
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstring>
+#include <new>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "../../include/kvx.h"
 #include "kvx_kernels.cuh"
@@ -18,33 +23,69 @@ constexpr int kThreads = 256;
 constexpr int kWarpsPerBlock = kThreads / 32;
 constexpr int kMaxDev = 64;
 
+// Per-device / per-kernel launch facts, queried once and shared by every host
+// thread (kvx.h promises re-entrancy): atomics for the SM counts, a mutex for
+// the occupancy and shared-memory-attribute caches.
 int sm_count(int dev) {
-  static int cache[kMaxDev] = {0};
+  static std::atomic<int> cache[kMaxDev];
   if (dev < 0 || dev >= kMaxDev) return 148;
-  if (!cache[dev]) {
-    int n = 0;
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (!n) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
       n = 148;
-    cache[dev] = n;
+    }
+    cache[dev].store(n, std::memory_order_relaxed);
   }
-  return cache[dev];
+  return n;
+}
+
+std::mutex g_cache_mu;
+std::map<std::tuple<int, const void*, int, int>, int> g_occupancy;  // (dev, fn, threads, smem)
+std::map<std::pair<int, const void*>, int> g_smem_attr;            // (dev, fn) -> bytes set
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
 }
 
 template <typename K>
-int blocks_per_sm(K kernel) {
+int blocks_per_sm(K kernel, int threads = kThreads, int smem = 0) {
+  const auto key = std::make_tuple(current_device(), reinterpret_cast<const void*>(kernel), threads, smem);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_occupancy.find(key);
+    if (it != g_occupancy.end()) return it->second;
+  }
   int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b <= 0)
-    b = 4;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem) != cudaSuccess || b <= 0) {
+    cudaGetLastError();
+    b = 1;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_occupancy[key] = b;
   return b;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel)
+// -- not a stream op, so it never lands inside a graph capture.
+template <typename K>
+cudaError_t ensure_smem_attr(K kernel, int bytes) {
+  const auto key = std::make_pair(current_device(), reinterpret_cast<const void*>(kernel));
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_smem_attr.find(key);
+  if (it != g_smem_attr.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) g_smem_attr[key] = bytes;
+  return e;
 }
 
 // Persistent-style grid: enough warps to cover every token row once, capped at
 // the number of CTAs the SMs hold concurrently (a multiple of the SM count).
 template <typename K>
 dim3 grid_for(K kernel, int64_t n_token_rows) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int64_t full = int64_t(sm_count(dev)) * blocks_per_sm(kernel);
+  const int64_t full = int64_t(sm_count(current_device())) * blocks_per_sm(kernel);
   const int64_t need = (n_token_rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
   int64_t g = need < full ? need : full;
   if (g < 1) g = 1;
@@ -100,7 +141,9 @@ int make_geo(kvx::Geo& g, const void* k, const void* v, int64_t layer_stride, co
     g.codes_ls = rows_per_layer * head_dim * bits / 8;
     g.meta_ls = rows_per_layer * ng * 2;
   } else {
-    if (payload_layer_stride % 16) return KVX_ERR_INVALID_ARG;
+    // 8-bit codes move as 32-byte vectors (st/ld.global.v8.b32): the layer
+    // stride must keep every layer's codes 32-byte aligned
+    if (payload_layer_stride % (bits == 8 ? 32 : 16)) return KVX_ERR_INVALID_ARG;
     g.codes_ls = payload_layer_stride;
     g.meta_ls = payload_layer_stride;
   }
@@ -151,8 +194,10 @@ cudaError_t make_items(const kvx::Geo& g, kvx::ItemGeo& ig) {
 struct SignalReq {
   uint32_t* counters = nullptr;
   uint32_t* peer_flags = nullptr;
-  uint32_t* parity = nullptr;
+  uint32_t ready_value = 0;
   const uint32_t* free_flag = nullptr;
+  uint32_t free_value = 0;
+  kvx::Ctl* ctl = nullptr;
   int layers_per_chunk = 1;
   int64_t n_layers = 0;
 };
@@ -168,8 +213,10 @@ cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero
   sig.peer_flags = rq.peer_flags;
   sig.items_per_chunk = 1;
   sig.ipc = make_fastdiv(1);
-  sig.parity = rq.parity;
+  sig.ready_value = rq.ready_value;
   sig.free_flag = rq.free_flag;
+  sig.free_value = rq.free_value;
+  sig.ctl = rq.ctl;
   if (rq.peer_flags) {
     const int64_t per_layer = ig.n_items / (rq.n_layers > 0 ? rq.n_layers : 1);
     const int64_t ipc = per_layer * rq.layers_per_chunk;
@@ -232,19 +279,20 @@ int64_t bulk_row_multiple(int64_t code_row_bytes, int64_t meta_row_bytes) {
 struct PullDone {  // optional in-kernel completion of a pull hand-off
   uint32_t* done_counter = nullptr;
   uint32_t* peer_free = nullptr;
-  uint32_t* parity = nullptr;
 };
 
 template <int BITS, int G>
 cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale, const void* zero,
-                        cudaStream_t s, bool* ok, const uint32_t* ready,
-                        int layers_per_chunk, const PullDone& done = PullDone()) {
+                        cudaStream_t s, bool* ok, const uint32_t* ready, uint32_t ready_value,
+                        int layers_per_chunk, const PullDone& done = PullDone(),
+                        kvx::Ctl* ctl = nullptr, bool pdl = false) {
   *ok = false;
   kvx::BulkGeo bg;
   bg.ready = ready;
-  bg.parity = done.parity;
+  bg.ready_value = ready_value;
   bg.done_counter = done.done_counter;
   bg.peer_free = done.peer_free;
+  bg.ctl = ctl;
   bg.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
   bg.code_row_bytes = int(int64_t(g.row_elems) * BITS / 8);
   bg.meta_row_bytes = int(int64_t(g.row_elems) / G * 2);
@@ -271,51 +319,45 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   if (n_spans >= (int64_t(1) << 31)) return cudaSuccess;
   bg.n_spans = uint32_t(n_spans);
   auto k = kvx::pull_dequant_scatter_kernel<BITS, G, kBulkStages>;
-  // once per device and instantiation (not a stream op; keeps capture clean)
-  int cur_dev = 0;
-  cudaGetDevice(&cur_dev);
-  static bool attr_set[kMaxDev] = {false};
-  if (cur_dev < 0 || cur_dev >= kMaxDev) return cudaErrorInvalidDevice;
-  if (!attr_set[cur_dev]) {
-    cudaError_t attr =
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (attr != cudaSuccess) return attr;
-    attr_set[cur_dev] = true;
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBulkThreads, smem) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  cudaGetLastError();
-  int dev = 0;
-  cudaGetDevice(&dev);
-  // ONE CTA per SM (4 stages x ~16 KB in flight each, 9.5 MB device-wide):
+  cudaError_t attr = ensure_smem_attr(k, 200 * 1024);
+  if (attr != cudaSuccess) return attr;
+  int per_sm = blocks_per_sm(k, kBulkThreads, smem);
+  // ONE CTA per SM (4 stages x ~12 KB in flight each, ~7 MB device-wide):
   // enough to saturate the link, and measured faster than filling every SM
   // with as many CTAs as fit (cfg3 pair 2,948 vs 2,798 GB/s fp16-eq), while
-  // leaving room on each SM for the decode GPU's own kernels
+  // leaving room on each SM for the decode GPU's own kernels -- and for the
+  // next hand-off's pull, which PDL schedules next to this one
   // (tools/decode_interference.py: a concurrent HBM-bound round slows 1.96x
   // instead of 2.2x).
   per_sm = per_sm < kPullCtasPerSm ? per_sm : kPullCtasPerSm;
-  int64_t grid = int64_t(sm_count(dev)) * per_sm;
+  int64_t grid = int64_t(sm_count(current_device())) * per_sm;
 #ifdef KVX_PULL_MAX_CTAS
   if (grid > KVX_PULL_MAX_CTAS) grid = KVX_PULL_MAX_CTAS;
 #endif
   if (grid > n_spans) grid = n_spans;
   *ok = true;
-  k<<<unsigned(grid), kBulkThreads, smem, s>>>(g, bg, static_cast<const uint8_t*>(codes),
-                                                static_cast<const __half*>(scale),
-                                                static_cast<const __half*>(zero));
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kBulkThreads);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, g, bg, static_cast<const uint8_t*>(codes),
+                            static_cast<const __half*>(scale), static_cast<const __half*>(zero));
 }
 
 template <int BITS>
 cudaError_t dispatch_pull(int group, const kvx::Geo& g, const void* c, const void* sc,
                           const void* z, cudaStream_t s, bool* ok, const uint32_t* ready,
-                          int lpc, const PullDone& done) {
+                          uint32_t rv, int lpc, const PullDone& done, kvx::Ctl* ctl, bool pdl) {
   switch (group) {
-    case 32: return launch_pull<BITS, 32>(g, c, sc, z, s, ok, ready, lpc, done);
-    case 64: return launch_pull<BITS, 64>(g, c, sc, z, s, ok, ready, lpc, done);
-    default: return launch_pull<BITS, 128>(g, c, sc, z, s, ok, ready, lpc, done);
+    case 32: return launch_pull<BITS, 32>(g, c, sc, z, s, ok, ready, rv, lpc, done, ctl, pdl);
+    case 64: return launch_pull<BITS, 64>(g, c, sc, z, s, ok, ready, rv, lpc, done, ctl, pdl);
+    default: return launch_pull<BITS, 128>(g, c, sc, z, s, ok, ready, rv, lpc, done, ctl, pdl);
   }
 }
 
@@ -362,6 +404,15 @@ void resolve_driver() {
   });
 }
 
+// Sub-array offsets of a kivi payload segment: 16-byte aligned, and the V
+// codes (8-bit: 32-byte vector accesses) 32-byte aligned in every layer.
+bool kivi_offsets_bad(const int64_t* seg_offsets, int64_t payload_layer_stride, int bits) {
+  for (int i = 0; i < 7; ++i)
+    if (seg_offsets[i] < 0 || seg_offsets[i] % 16) return true;
+  if (bits == 8 && (seg_offsets[4] % 32 || payload_layer_stride % 32)) return true;
+  return false;
+}
+
 int kivi_check(int head_dim, int group, int bits) {
   if (bits != 4 && bits != 8) return KVX_ERR_INVALID_ARG;
   if (group != 32 && group != 64) return KVX_ERR_INVALID_ARG;
@@ -374,9 +425,7 @@ cudaError_t launch_kchan_quant(const kvx::KchanGeo& kg, cudaStream_t s) {
   constexpr int cta_ch = 4 * (32 / (G / 16)) * 8;  // matches quant_pack_kchan_kernel
   const int cblocks = (kg.row_elems + cta_ch - 1) / cta_ch;
   const int64_t items = kg.n_layers * kg.n_groups * cblocks;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int64_t grid = int64_t(sm_count(dev)) * 8;
+  int64_t grid = int64_t(sm_count(current_device())) * 8;
   if (grid > items) grid = items;
   kvx::quant_pack_kchan_kernel<BITS, G><<<unsigned(grid), 128, 0, s>>>(kg);
   return cudaGetLastError();
@@ -402,13 +451,14 @@ constexpr int kKchanStageCodes = KVX_KCHAN_STAGE_CODES;  // code bytes per kchan
 template <int BITS, int G>
 cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, void* kc,
                               int64_t dst_ls_b, cudaStream_t s, bool* ok,
-                              const uint32_t* ready = nullptr, int layers_per_chunk = 1,
-                              const uint32_t* parity = nullptr) {
+                              const uint32_t* ready = nullptr, uint32_t ready_value = 0,
+                              int layers_per_chunk = 1, kvx::Ctl* ctl = nullptr) {
   *ok = false;
   constexpr int kStages = 4;
   kvx::KchanBulk kb;
   kb.ready = ready;
-  kb.parity = parity;
+  kb.ready_value = ready_value;
+  kb.ctl = ctl;
   kb.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
   kb.slab = kKchanStageCodes / (G * BITS / 8);  // channels per span (S/32 divides 256)
   // rows that fit one span whole: the group's code rows are then a single
@@ -422,26 +472,16 @@ cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, voi
   kb.stage_bytes = G * kb.slab * BITS / 8 + 4 * kb.slab;
   const int smem = kStages * kb.stage_bytes;
   auto k = kvx::pull_kchan_kernel<BITS, G, kStages>;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  static bool attr_set[kMaxDev] = {false};
-  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
-  if (!attr_set[dev]) {
+  {
     // the largest span of this instantiation (the slab shrinks for short rows)
     const int s_max = kKchanStageCodes / (G * BITS / 8);
     const int smem_max = kStages * (G * s_max * BITS / 8 + 4 * s_max);
-    cudaError_t attr =
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    cudaError_t attr = ensure_smem_attr(k, smem_max);
     if (attr != cudaSuccess) return attr;
-    attr_set[dev] = true;
   }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBulkThreads, smem) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  cudaGetLastError();
+  int per_sm = blocks_per_sm(k, kBulkThreads, smem);
   per_sm = per_sm < kPullCtasPerSm ? per_sm : kPullCtasPerSm;  // as launch_pull
-  int64_t grid = int64_t(sm_count(dev)) * per_sm;
+  int64_t grid = int64_t(sm_count(current_device())) * per_sm;
   if (grid > kb.n_spans) grid = kb.n_spans;
   if (grid < 1) return cudaSuccess;
   *ok = true;
@@ -453,7 +493,7 @@ cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, voi
 
 extern "C" {
 
-int kvx_version(void) { return 100; }
+int kvx_version(void) { return 20000; }
 
 const char* kvx_strerror(int code) {
   switch (code) {
@@ -524,13 +564,13 @@ int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_laye
                           int n_heads, int head_dim, int group, int bits, void* codes,
                           void* scale, void* zero, int64_t payload_layer_stride,
                           int plane_heads, int head_offset, void* counters,
-                          void* peer_ready_flags, int layers_per_chunk, const void* free_flag,
-                          void* parity_state, void* stream) {
+                          void* peer_ready_flags, int layers_per_chunk, uint32_t ready_value,
+                          const void* free_flag, uint32_t free_value, void* ctl, void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
   if (bits == 16 || !counters || !peer_ready_flags || layers_per_chunk < 1 ||
       !aligned(counters, 4) || !aligned(peer_ready_flags, 4) || !aligned(free_flag, 4) ||
-      !aligned(parity_state, 4))
+      !aligned(ctl, 8))
     return KVX_ERR_INVALID_ARG;
   kvx::Geo g;
   rc = make_geo(g, k_src, v_src, src_layer_stride, src_slots, n_layers, n_tokens, n_heads, head_dim,
@@ -544,8 +584,10 @@ int kvx_quant_pack_signal(const void* k_src, const void* v_src, int64_t src_laye
   SignalReq rq;
   rq.counters = static_cast<uint32_t*>(counters);
   rq.peer_flags = static_cast<uint32_t*>(peer_ready_flags);
-  rq.parity = static_cast<uint32_t*>(parity_state);
+  rq.ready_value = ready_value;
   rq.free_flag = static_cast<const uint32_t*>(free_flag);
+  rq.free_value = free_value;
+  rq.ctl = static_cast<kvx::Ctl*>(ctl);
   rq.layers_per_chunk = layers_per_chunk;
   rq.n_layers = n_layers;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -594,9 +636,9 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
                                    int64_t dst_layer_stride, int plane_heads, int head_offset,
-                                   const void* ready_flags, int layers_per_chunk,
-                                   void* done_counter, void* peer_free_flag, void* parity_state,
-                                   void* stream) {
+                                   const void* ready_flags, uint32_t ready_value,
+                                   int layers_per_chunk, void* done_counter, void* peer_free_flag,
+                                   void* ctl, int flags, void* stream) {
   int rc = valid_format(head_dim, group, bits);
   if (rc) return rc;
   kvx::Geo g;
@@ -604,27 +646,29 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
                 head_dim, group, bits, payload_layer_stride, 2, 0, plane_heads, head_offset);
   if (rc) return rc;
   if (g.n_token_rows == 0) return KVX_OK;
-  if (ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) return KVX_ERR_INVALID_ARG;
+  if ((ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) || !aligned(ctl, 8) ||
+      (flags & ~KVX_PULL_PDL))
+    return KVX_ERR_INVALID_ARG;
   if ((done_counter != nullptr) != (peer_free_flag != nullptr) ||
-      !aligned(parity_state, 4) || (parity_state && !done_counter) ||
-      (done_counter && (!ready_flags || !aligned(done_counter, 4) ||
-                        !aligned(peer_free_flag, 4))))
+      (done_counter && (!ready_flags || !aligned(done_counter, 4) || !aligned(peer_free_flag, 4))))
     return KVX_ERR_INVALID_ARG;
   PullDone done;
   done.done_counter = static_cast<uint32_t*>(done_counter);
   done.peer_free = static_cast<uint32_t*>(peer_free_flag);
-  done.parity = static_cast<uint32_t*>(parity_state);
   if (bits != 16 && codes && scale && zero && k_cache && aligned(k_cache, 32) &&
       aligned(v_cache, 32) && (dst_layer_stride * 2) % 32 == 0 && g.plane_row_b % 32 == 0 &&
-      g.head_off_b % 32 == 0) {
+      g.head_off_b % 32 == 0 && aligned(codes, 8 * bits)) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint32_t* rf = static_cast<const uint32_t*>(ready_flags);
+    kvx::Ctl* c = static_cast<kvx::Ctl*>(ctl);
+    const bool pdl = flags & KVX_PULL_PDL;
+    const int lpc = layers_per_chunk;
     bool ok = false;
     cudaError_t e;
     switch (bits) {
-      case 2: e = dispatch_pull<2>(group, g, codes, scale, zero, s, &ok, rf, layers_per_chunk, done); break;
-      case 8: e = dispatch_pull<8>(group, g, codes, scale, zero, s, &ok, rf, layers_per_chunk, done); break;
-      default: e = dispatch_pull<4>(group, g, codes, scale, zero, s, &ok, rf, layers_per_chunk, done); break;
+      case 2: e = dispatch_pull<2>(group, g, codes, scale, zero, s, &ok, rf, ready_value, lpc, done, c, pdl); break;
+      case 8: e = dispatch_pull<8>(group, g, codes, scale, zero, s, &ok, rf, ready_value, lpc, done, c, pdl); break;
+      default: e = dispatch_pull<4>(group, g, codes, scale, zero, s, &ok, rf, ready_value, lpc, done, c, pdl); break;
     }
     if (e != cudaSuccess) return e;
     if (ok) return KVX_OK;
@@ -658,8 +702,7 @@ int kvx_quant_pack_kivi(const void* k_src, const void* v_src, int64_t src_layer_
   if (n_layers == 0 || n_tokens == 0) return KVX_OK;
   if (!k_src || !v_src || !payload || (n_groups && !group_starts) || (n_residual && !residual_tokens))
     return KVX_ERR_INVALID_ARG;
-  for (int i = 0; i < 7; ++i)
-    if (seg_offsets[i] < 0 || seg_offsets[i] % 16) return KVX_ERR_INVALID_ARG;
+  if (kivi_offsets_bad(seg_offsets, payload_layer_stride, bits)) return KVX_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(payload);
   const int row_elems = n_heads * head_dim;
@@ -708,8 +751,8 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
                         const int64_t* residual_dst_slots, int64_t n_residual, int64_t n_layers,
                         int64_t n_tokens, int n_heads, int head_dim, int group, int bits,
                         void* k_cache, void* v_cache, int64_t dst_layer_stride, void* stream,
-                        bool bulk, const uint32_t* ready = nullptr, int layers_per_chunk = 1,
-                        const uint32_t* parity = nullptr) {
+                        bool bulk, const uint32_t* ready = nullptr, uint32_t ready_value = 0,
+                        int layers_per_chunk = 1, kvx::Ctl* ctl = nullptr) {
   int rc = kivi_check(head_dim, group, bits);
   if (rc) return rc;
   if (n_layers < 0 || n_tokens < 0 || n_heads <= 0 || n_groups < 0 || n_residual < 0 ||
@@ -720,8 +763,7 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
       !aligned(v_cache, 32) || (dst_layer_stride * 2) % 32 || (n_groups && !group_starts) ||
       (n_residual && !residual_dst_slots))
     return KVX_ERR_INVALID_ARG;
-  for (int i = 0; i < 7; ++i)
-    if (seg_offsets[i] < 0 || seg_offsets[i] % 16) return KVX_ERR_INVALID_ARG;
+  if (kivi_offsets_bad(seg_offsets, payload_layer_stride, bits)) return KVX_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const char* base = static_cast<const char*>(payload);
   cudaError_t e = cudaSuccess;
@@ -743,12 +785,12 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
       const int lpc = layers_per_chunk;
       if (bits == 4)
         e = group == 32
-                ? launch_kchan_pull<4, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, lpc, parity)
-                : launch_kchan_pull<4, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, lpc, parity);
+                ? launch_kchan_pull<4, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl)
+                : launch_kchan_pull<4, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl);
       else
         e = group == 32
-                ? launch_kchan_pull<8, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, lpc, parity)
-                : launch_kchan_pull<8, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, lpc, parity);
+                ? launch_kchan_pull<8, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl)
+                : launch_kchan_pull<8, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl);
       if (e != cudaSuccess) return e;
       if (!ok && ready) return KVX_ERR_UNSUPPORTED;  // per-lane kernels cannot wait in-kernel
     }
@@ -770,10 +812,11 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
     const char *vc = base + seg_offsets[4], *vs = base + seg_offsets[5], *vz = base + seg_offsets[6];
     bool ok = false;
     if (bulk && aligned(v_cache, 32) && g.plane_row_b % 32 == 0) {
-      PullDone pd;  // parity read-only: the caller releases the slot after this call
-      pd.parity = const_cast<uint32_t*>(parity);
-      e = bits == 4 ? dispatch_pull<4>(group, g, vc, vs, vz, s, &ok, ready, layers_per_chunk, pd)
-                    : dispatch_pull<8>(group, g, vc, vs, vz, s, &ok, ready, layers_per_chunk, pd);
+      PullDone pd;  // no in-kernel completion: the caller releases the slot after this call
+      e = bits == 4 ? dispatch_pull<4>(group, g, vc, vs, vz, s, &ok, ready, ready_value,
+                                       layers_per_chunk, pd, ctl, false)
+                    : dispatch_pull<8>(group, g, vc, vs, vz, s, &ok, ready, ready_value,
+                                       layers_per_chunk, pd, ctl, false);
       if (e != cudaSuccess) return e;
     }
     if (!ok && ready) return KVX_ERR_UNSUPPORTED;  // per-lane kernels cannot wait in-kernel
@@ -817,16 +860,15 @@ int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_lay
                                         int64_t n_layers, int64_t n_tokens, int n_heads,
                                         int head_dim, int group, int bits, void* k_cache,
                                         void* v_cache, int64_t dst_layer_stride,
-                                        const void* ready_flags, int layers_per_chunk,
-                                        const void* parity_state, void* stream) {
-  if ((ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) ||
-      !aligned(parity_state, 4))
+                                        const void* ready_flags, uint32_t ready_value,
+                                        int layers_per_chunk, void* ctl, void* stream) {
+  if ((ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) || !aligned(ctl, 8))
     return KVX_ERR_INVALID_ARG;
   return kivi_dequant(payload, payload_layer_stride, seg_offsets, dst_slots, group_starts,
                       n_groups, residual_dst_slots, n_residual, n_layers, n_tokens, n_heads,
                       head_dim, group, bits, k_cache, v_cache, dst_layer_stride, stream, true,
-                      static_cast<const uint32_t*>(ready_flags), layers_per_chunk,
-                      static_cast<const uint32_t*>(parity_state));
+                      static_cast<const uint32_t*>(ready_flags), ready_value, layers_per_chunk,
+                      static_cast<kvx::Ctl*>(ctl));
 }
 
 // ---- transport -------------------------------------------------------------
@@ -892,7 +934,13 @@ int kvx_ipc_open(const void* handle, void** ptr_out) {
   if (!handle || !ptr_out) return KVX_ERR_INVALID_ARG;
   cudaIpcMemHandle_t h;
   memcpy(&h, handle, sizeof(h));
-  return cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  cudaError_t e = cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e == cudaSuccess) return KVX_OK;
+  cudaGetLastError();
+  // a malformed handle is the caller's error; anything else means this GPU
+  // cannot map the partner's memory: no path (costs.py:63-64's NoPath)
+  if (e == cudaErrorInvalidValue || e == cudaErrorInvalidResourceHandle) return e;
+  return KVX_ERR_NO_PATH;
 }
 
 int kvx_ipc_close(void* ptr) { return ptr ? cudaIpcCloseMemHandle(ptr) : KVX_OK; }
@@ -942,6 +990,231 @@ int kvx_stream_wait_eq(const void* flag, uint32_t value, void* stream) {
   CUresult r = g_wait32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
                         CU_STREAM_WAIT_VALUE_EQ);
   return r == CUDA_SUCCESS ? KVX_OK : KVX_ERR_UNSUPPORTED;
+}
+
+
+// ---- host-mapped control block ---------------------------------------------
+
+int kvx_ctl_alloc(void** ctl_out) {
+  if (!ctl_out) return KVX_ERR_INVALID_ARG;
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, sizeof(kvx::Ctl), cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) return e;
+  memset(p, 0, sizeof(kvx::Ctl));
+  void* d = nullptr;
+  e = cudaHostGetDevicePointer(&d, p, 0);
+  if (e != cudaSuccess || d != p) {  // UVA: the kernels use the host address
+    cudaFreeHost(p);
+    return e != cudaSuccess ? int(e) : KVX_ERR_UNSUPPORTED;
+  }
+  *ctl_out = p;
+  return KVX_OK;
+}
+
+int kvx_ctl_free(void* ctl) { return ctl ? cudaFreeHost(ctl) : KVX_OK; }
+
+// ---- chunk plan and the native pair channel --------------------------------
+
+int kvx_handoff_chunk_plan(int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                           int layerwise, int* layers_per_chunk, int* n_chunks) {
+  if (n_layers < 1 || n_tokens < 0 || n_heads < 1 || head_dim < 32 || !layers_per_chunk ||
+      !n_chunks)
+    return KVX_ERR_INVALID_ARG;
+  int64_t n;
+  if (layerwise) {
+    n = n_layers < kvx::kMaxSignalChunks ? n_layers : kvx::kMaxSignalChunks;
+  } else {
+    // layer-granular doorbells, but every K1 warp should own several items
+    // per chunk (one fence + atomic per warp per chunk): >= 4 items per
+    // resident K1 warp (148 SMs x 2 CTAs x 8 warps) in every chunk
+    const int64_t cpr = int64_t(n_heads) * head_dim / 32;
+    const int64_t items = n_layers * 2 * n_tokens * ((cpr + 31) / 32);
+    n = items / (4 * 148 * 2 * 8);
+    if (n > n_layers) n = n_layers;
+    if (n > kvx::kMaxSignalChunks) n = kvx::kMaxSignalChunks;
+    if (n < 1) n = 1;
+  }
+  const int64_t lpc = (n_layers + n - 1) / n;
+  *layers_per_chunk = int(lpc);
+  *n_chunks = int((n_layers + lpc - 1) / lpc);
+  return KVX_OK;
+}
+
+}  // extern "C"
+
+namespace {
+constexpr int kFlagReadyBase = 0;                            // ready[h][c]: h * 64 + c
+constexpr int kFlagFreeBase = kvx::kMaxSignalChunks * 8;     // free[h]: 512 + h
+constexpr int kPairScratch = kvx::kMaxSignalChunks + 1;      // u32 per queue slot
+
+int64_t round256(int64_t x) { return (x + 255) / 256 * 256; }
+}  // namespace
+
+struct kvx_pair {
+  int role = 0;  // KVX_ROLE_PREFILL / KVX_ROLE_DECODE
+  int dev = 0;
+  int64_t n_layers = 0, max_tokens = 0;
+  int n_heads = 0, head_dim = 0, bits = 4, group = 128, queue_depth = 1, layerwise = 0;
+  uint32_t* local_flags = nullptr;  // this GPU's doorbell page
+  uint32_t* peer_flags = nullptr;   // the partner's page (IPC / peer mapped)
+  char* payload = nullptr;          // the prefill GPU's queue (local on P, mapped on D)
+  int64_t slot_bytes = 0;
+  kvx::Ctl* ctl = nullptr;
+  uint32_t* scratch = nullptr;      // [queue_depth][65] (device, zero between launches)
+};
+
+namespace {
+// Sequence protocol: hand-off e (1, 2, ...) uses queue slot h = e % Q for the
+// v-th time, v = (e - 1) / Q + 1.  P waits free[h] >= v - 1, rings
+// ready[h][c] = v; D waits ready[h][c] >= v and sets free[h] = v.
+void seq_of(const kvx_pair* p, uint64_t e, int* h, uint32_t* v) {
+  *h = int(e % uint64_t(p->queue_depth));
+  *v = uint32_t((e - 1) / uint64_t(p->queue_depth) + 1);
+}
+
+// Per-layer segment stride of a queue slot's payload (= datapath.PackedLayout).
+int64_t pair_layer_stride(const kvx_pair* p, int64_t n_tokens, int64_t* scale_off,
+                          int64_t* zero_off) {
+  const int64_t rows = 2 * n_tokens * p->n_heads;
+  const int64_t codes = rows * p->head_dim * p->bits / 8;
+  const int64_t meta = rows * (p->head_dim / p->group) * 2;
+  *scale_off = round256(codes);
+  *zero_off = *scale_off + round256(meta);
+  return *zero_off + round256(meta);
+}
+
+int pair_check(const kvx_pair* p, uint64_t e, int64_t n_tokens, int plane_heads, int head_offset) {
+  if (!p || e < 1) return KVX_ERR_INVALID_ARG;
+  if (n_tokens < 0 || n_tokens > p->max_tokens) return KVX_ERR_INVALID_ARG;
+  const int ph = plane_heads ? plane_heads : p->n_heads;
+  if (head_offset < 0 || head_offset + p->n_heads > ph) return KVX_ERR_INVALID_ARG;
+  if (current_device() != p->dev) return KVX_ERR_INVALID_ARG;
+  return KVX_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int kvx_pair_create(int role, int64_t n_layers, int64_t max_tokens, int n_heads, int head_dim,
+                    int bits, int group, int queue_depth, int layerwise, void* local_flags,
+                    void* peer_flags, void* payload, int64_t slot_bytes, void* ctl,
+                    void** pair_out) {
+  if (!pair_out || (role != KVX_ROLE_PREFILL && role != KVX_ROLE_DECODE)) return KVX_ERR_INVALID_ARG;
+  int rc = valid_format(head_dim, group, bits);
+  if (rc || bits == 16) return KVX_ERR_INVALID_ARG;
+  if (n_layers < 1 || max_tokens < 1 || n_heads < 1 || queue_depth < 1 || queue_depth > 8 ||
+      !local_flags || !peer_flags || !payload || !aligned(local_flags, 4) ||
+      !aligned(peer_flags, 4) || !aligned(payload, 256) || slot_bytes % 256 || !aligned(ctl, 8))
+    return KVX_ERR_INVALID_ARG;
+  auto* p = new (std::nothrow) kvx_pair();
+  if (!p) return cudaErrorMemoryAllocation;
+  p->role = role;
+  p->dev = current_device();
+  p->n_layers = n_layers;
+  p->max_tokens = max_tokens;
+  p->n_heads = n_heads;
+  p->head_dim = head_dim;
+  p->bits = bits;
+  p->group = group;
+  p->queue_depth = queue_depth;
+  p->layerwise = layerwise ? 1 : 0;
+  p->local_flags = static_cast<uint32_t*>(local_flags);
+  p->peer_flags = static_cast<uint32_t*>(peer_flags);
+  p->payload = static_cast<char*>(payload);
+  p->slot_bytes = slot_bytes;
+  p->ctl = static_cast<kvx::Ctl*>(ctl);
+  int64_t so, zo;
+  if (pair_layer_stride(p, max_tokens, &so, &zo) * n_layers > slot_bytes) {
+    delete p;
+    return KVX_ERR_INVALID_ARG;
+  }
+  const size_t sb = size_t(queue_depth) * kPairScratch * 4;
+  cudaError_t e = cudaMalloc(&p->scratch, sb);
+  if (e == cudaSuccess) e = cudaMemset(p->scratch, 0, sb);
+  if (e != cudaSuccess) {
+    cudaFree(p->scratch);
+    delete p;
+    return e;
+  }
+  *pair_out = p;
+  return KVX_OK;
+}
+
+int kvx_pair_destroy(void* pair) {
+  auto* p = static_cast<kvx_pair*>(pair);
+  if (!p) return KVX_OK;
+  cudaError_t e = cudaFree(p->scratch);
+  delete p;
+  return e;
+}
+
+int kvx_pair_send(void* pair, uint64_t epoch, const void* k_src, const void* v_src,
+                  int64_t src_layer_stride, const int64_t* src_slots, int64_t n_tokens,
+                  int plane_heads, int head_offset, int flags, void* stream) {
+  auto* p = static_cast<kvx_pair*>(pair);
+  int rc = pair_check(p, epoch, n_tokens, plane_heads, head_offset);
+  if (rc) return rc;
+  if (p->role != KVX_ROLE_PREFILL || (flags & ~KVX_PAIR_GATE)) return KVX_ERR_INVALID_ARG;
+  if (n_tokens == 0) return KVX_OK;
+  int h;
+  uint32_t v;
+  seq_of(p, epoch, &h, &v);
+  int lpc, nc;
+  rc = kvx_handoff_chunk_plan(p->n_layers, n_tokens, p->n_heads, p->head_dim, p->layerwise, &lpc,
+                              &nc);
+  if (rc) return rc;
+  int64_t so, zo;
+  const int64_t ls = pair_layer_stride(p, n_tokens, &so, &zo);
+  char* base = p->payload + int64_t(h) * p->slot_bytes;
+  uint32_t* free_flag = p->local_flags + kFlagFreeBase + h;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((flags & KVX_PAIR_GATE) && v > 1) {
+    // hold the prefill side in the GPU front-end (no SMs held) until the
+    // decode side has consumed the slot's previous use; K1 re-checks in-kernel
+    rc = kvx_stream_wait(free_flag, v - 1, stream);
+    if (rc) return rc;
+  }
+  return kvx_quant_pack_signal(k_src, v_src, src_layer_stride, src_slots, p->n_layers, n_tokens,
+                               p->n_heads, p->head_dim, p->group, p->bits, base, base + so,
+                               base + zo, ls, plane_heads, head_offset,
+                               p->scratch + h * kPairScratch, p->peer_flags + kFlagReadyBase + h * 64,
+                               lpc, v, free_flag, v - 1, p->ctl, s);
+}
+
+int kvx_pair_recv(void* pair, uint64_t epoch, void* k_cache, void* v_cache,
+                  int64_t dst_layer_stride, const int64_t* dst_slots, int64_t n_tokens,
+                  int plane_heads, int head_offset, int flags, void* stream) {
+  auto* p = static_cast<kvx_pair*>(pair);
+  int rc = pair_check(p, epoch, n_tokens, plane_heads, head_offset);
+  if (rc) return rc;
+  if (p->role != KVX_ROLE_DECODE || (flags & ~(KVX_PAIR_GATE | KVX_PAIR_PDL)) || !dst_slots)
+    return KVX_ERR_INVALID_ARG;
+  if (n_tokens == 0) return KVX_OK;
+  if (!kvx_pull_supported(n_tokens, p->n_heads, p->head_dim, p->group, p->bits))
+    return KVX_ERR_UNSUPPORTED;
+  int h;
+  uint32_t v;
+  seq_of(p, epoch, &h, &v);
+  int lpc, nc;
+  rc = kvx_handoff_chunk_plan(p->n_layers, n_tokens, p->n_heads, p->head_dim, p->layerwise, &lpc,
+                              &nc);
+  if (rc) return rc;
+  int64_t so, zo;
+  const int64_t ls = pair_layer_stride(p, n_tokens, &so, &zo);
+  const char* base = p->payload + int64_t(h) * p->slot_bytes;
+  uint32_t* ready = p->local_flags + kFlagReadyBase + h * 64;
+  if (flags & KVX_PAIR_GATE) {
+    // launch only once the first chunk is published: a pull never sits on
+    // the SMs waiting for an idle prefill side
+    rc = kvx_stream_wait(ready, v, stream);
+    if (rc) return rc;
+  }
+  return kvx_pull_dequant_scatter_paged(base, base + so, base + zo, ls, dst_slots, p->n_layers,
+                                        n_tokens, p->n_heads, p->head_dim, p->group, p->bits,
+                                        k_cache, v_cache, dst_layer_stride, plane_heads,
+                                        head_offset, ready, v, lpc, p->scratch + h * kPairScratch,
+                                        p->peer_flags + kFlagFreeBase + h, p->ctl,
+                                        (flags & KVX_PAIR_PDL) ? KVX_PULL_PDL : 0, stream);
 }
 
 }  // extern "C"

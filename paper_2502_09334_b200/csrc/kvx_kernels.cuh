@@ -412,33 +412,98 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define KVX_TRACE_STAMP(kind, launch, slot) ((void)0)
 #endif
 
+// Host-mapped control block of one channel (include/kvx.h, kvx_ctl): the
+// host writes `abort`, the kernels report through `status`; `timeout_ns`
+// bounds every in-kernel wait (0 = the 60 s default).  Nullable: without one
+// a wait that times out traps (there is nowhere to report it).
+struct Ctl {
+  uint32_t abort;
+  uint32_t status;
+  unsigned long long timeout_ns;
+};
+constexpr uint32_t kStatusAborted = 1u;
+constexpr uint32_t kStatusTimeout = 2u;
+constexpr unsigned long long kDefaultTimeoutNs = 60ull * 1000000000ull;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Bounded, abortable spin until a doorbell reaches `value`.  Doorbells carry
+// per-slot sequence numbers that only grow, so the test is the wrap-safe
+// (int32)(*flag - value) >= 0, and a flag left over from an earlier use of
+// the slot (always < value) can never satisfy it.  System-scope acquire: the
+// flag is written by the partner GPU over NVLink.  Returns false -- after
+// recording why in ctl->status -- when the host aborted the channel or the
+// wait outlived ctl->timeout_ns; the kernel then winds down instead of
+// trapping, so the CUDA context (and the decode GPU's KV cache) survive a
+// lost partner.
+__device__ __noinline__ bool spin_until_geq(const uint32_t* flag, uint32_t value, Ctl* ctl) {
+  unsigned long long t0 = 0, limit = kDefaultTimeoutNs;
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    const int32_t d = int32_t(v - value);
+    if (d >= 0) {
+      // A live doorbell is at most the awaited value (the partner cannot run
+      // a slot's use ahead of this side); a jump of >= 2^29 is the host's
+      // abort poison (PairChannel.abort releasing the GPU front-end waits).
+      if (d < (1 << 29)) return true;
+      if (!ctl) __trap();
+      asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(&ctl->status), "r"(kStatusAborted)
+                   : "memory");
+      return false;
+    }
+    if ((spin & 255u) == 255u) {  // every 256 polls: the abort word and the clock
+      const unsigned long long now = globaltimer_ns();
+      if (spin == 255u) {
+        t0 = now;
+        if (ctl) {
+          unsigned long long tl;
+          asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(tl) : "l"(&ctl->timeout_ns));
+          if (tl) limit = tl;
+        }
+      }
+      uint32_t ab = 0;
+      if (ctl) asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(ab) : "l"(&ctl->abort));
+      if (ab || now - t0 > limit) {
+        if (!ctl) __trap();
+        asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(&ctl->status),
+                     "r"(ab ? kStatusAborted : kStatusTimeout)
+                     : "memory");
+        return false;
+      }
+    }
+    __nanosleep(spin < 64 ? 32 : 256);
+  }
+}
+
+// Programmatic dependent launch (kernels launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): let the next kernel of
+// the stream be scheduled now / wait until every earlier grid of the stream
+// has completed and its memory is visible.  Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 struct SignalGeo {
-  // [kMaxSignalChunks] chunk arrivals + [1] CTA exits; zero at launch, and
-  // reset in-kernel by the last arrival, so zero again after every launch
+  // [kMaxSignalChunks] chunk arrivals: zero at launch, and reset in-kernel by
+  // each chunk's last arrival, so zero again after every launch
   uint32_t* counters;
   uint32_t* peer_flags;  // [n_chunks] decode-side ready flags (IPC/peer mapped), or null
   uint32_t items_per_chunk;
   FastDiv ipc;           // items_per_chunk as a multiply-shift (per-item chunk test)
-  // queue-half parity p (nullable = 0): doorbells are set to p ^ 1; the last
-  // CTA to exit flips *parity to p ^ 1 for the half's next use
-  uint32_t* parity;
-  // queue half free (nullable): every CTA waits *free_flag == p (written by
-  // the decode side over NVLink) before it stores into the half
+  uint32_t ready_value;  // this hand-off's sequence number v: doorbells are set to v
+  // queue slot free (nullable, this GPU's memory, written by the decode side
+  // over NVLink): every CTA waits *free_flag >= free_value (v - 1: the
+  // slot's previous use consumed) before it stores into the slot
   const uint32_t* free_flag;
+  uint32_t free_value;
+  Ctl* ctl;  // nullable
 };
-
-// Bounded spin until *flag == value (system-scope acquire: the flag is
-// written by the partner GPU over NVLink).  Traps after ~60 s so a lost
-// partner cannot hang the GPU forever.
-__device__ __forceinline__ void spin_until_eq(const uint32_t* flag, uint32_t value) {
-  uint32_t v;
-  for (uint32_t spin = 0;; ++spin) {
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    if (v == value) break;
-    if (spin > (1u << 26)) __trap();
-    __nanosleep(spin < 64 ? 32 : 512);
-  }
-}
 
 // Warps w in [lo, hi) that own at least one item i in [a, b) (item i -> warp i % W).
 __device__ __forceinline__ uint32_t warps_owning(uint32_t a, uint32_t b, uint32_t W, uint32_t lo,
@@ -506,7 +571,7 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
   __shared__ uint32_t cta_cnt[kMaxSignalChunks];
-  __shared__ uint32_t s_parity;
+  __shared__ uint32_t s_go;
 #ifdef KVX_TRACE
   const uint32_t trace_id = g_trace_n[0];
   if (sig.peer_flags && blockIdx.x == 0 && threadIdx.x == 0) KVX_TRACE_STAMP(0, trace_id, 0);
@@ -514,14 +579,14 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
   if (sig.peer_flags) {
     for (int i = threadIdx.x; i < kMaxSignalChunks; i += blockDim.x) cta_cnt[i] = 0u;
     if (threadIdx.x == 0) {
-      const uint32_t p = sig.parity ? *sig.parity : 0u;
-      if (sig.free_flag) spin_until_eq(sig.free_flag, p);  // decode side done with the half
-      s_parity = p;
+      // the decode side is done with this queue slot's previous use
+      s_go = sig.free_flag ? spin_until_geq(sig.free_flag, sig.free_value, sig.ctl) : 1u;
       if (blockIdx.x == 0) KVX_TRACE_STAMP(0, trace_id, 1);
     }
     __syncthreads();
+    if (!s_go) return;  // aborted / timed out (ctl->status says which)
   }
-  const uint32_t ready_value = sig.peer_flags ? (s_parity ^ 1u) : 0u;
+  const uint32_t ready_value = sig.ready_value;
   uint32_t w[NB][16];
   K1Item it[NB];
 #pragma unroll
@@ -559,18 +624,17 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
     }
   }
 k1_done:
-  if (sig.peer_flags && sig.parity) {
-    // every CTA has read the parity (at its start): the last one out flips it
+#ifdef KVX_TRACE
+  if (sig.peer_flags) {  // trace builds: stamp the last CTA's exit
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(sig.counters + kMaxSignalChunks, 1u) == gridDim.x - 1) {
       sig.counters[kMaxSignalChunks] = 0u;
-      *sig.parity = s_parity ^ 1u;
-#ifdef KVX_TRACE
       KVX_TRACE_STAMP(0, trace_id, 3);
       g_trace_n[0] = trace_id + 1;
-#endif
     }
   }
+#endif
+  return;
 }
 
 // 16-bit passthrough on the prefill side: copy rows into the dense payload.
@@ -785,14 +849,17 @@ __global__ void __launch_bounds__(256) scatter16_kernel(Geo g, const uint8_t* __
 // cache; each warp releases the stage through an "empty" mbarrier.
 // ---------------------------------------------------------------------------
 struct BulkGeo {
-  // per-chunk doorbells (nullable): wait ready[c] == p ^ 1, p = *parity (or 0)
+  // per-chunk doorbells (nullable): the producer waits ready[c] >= ready_value
+  // (this hand-off's sequence number) before the chunk's bulk reads
   const uint32_t* ready;
-  uint32_t* parity;
-  // in-kernel completion (nullable): the last CTA to finish sets
-  // *peer_free = p ^ 1 on the prefill GPU (queue half consumed) and flips
-  // *parity -- no memset / stream-memop nodes after the kernel
+  uint32_t ready_value;
+  // in-kernel completion (nullable): a u32 counting CTA exits (low 16 bits)
+  // and aborted CTAs (high bits), zero between launches.  The last CTA out
+  // sets *peer_free = ready_value on the prefill GPU (queue slot consumed) --
+  // no stream-memop node after the kernel -- unless a CTA aborted
   uint32_t* done_counter;
   uint32_t* peer_free;
+  Ctl* ctl;              // nullable
   int layers_per_chunk;
   int rows_per_span;     // R
   int spans_per_layer;   // ceil(2T / R)
@@ -828,15 +895,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 // Block (producer thread only) until the prefill side has published chunk c
-// (doorbell == this hand-off's ready value).  The doorbell lives in this GPU's
-// memory and is written over NVLink by the prefill GPU (K1's last arriving
-// warp, or a stream memop); the acquire + proxy fence order the following
-// bulk reads of the peer payload.  Bounded (spin_until_eq).
-__device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t value) {
-  spin_until_eq(flag, value);
+// (doorbell >= this hand-off's sequence number).  The doorbell lives in this
+// GPU's memory and is written over NVLink by the prefill GPU (K1's last
+// arriving warp, or a stream memop); the acquire + proxy fence order the
+// following bulk reads of the peer payload.  False = aborted / timed out.
+__device__ __forceinline__ bool wait_ready(const uint32_t* flag, uint32_t value, Ctl* ctl) {
+  if (!spin_until_geq(flag, value, ctl)) return false;
   // the bulk copies that follow read through the async proxy
   asm volatile("fence.proxy.async.global;" ::: "memory");
+  return true;
 }
+
+// Producer side of a span whose chunk was never published (abort): complete
+// the stage's phase without data so the consumers move on.
+__device__ __forceinline__ void mbar_arrive_empty_phase(uint64_t* bar) { mbar_arrive(bar); }
 
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes,
                                         uint64_t* bar) {
@@ -856,39 +928,53 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
   constexpr int LPG = G / 32;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ uint32_t s_abort;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], CONSUMERS);
     }
+    s_abort = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // PDL: the stream's next kernel (the next hand-off's pull) may be scheduled
+  // now; its producer starts streaming its own queue slot while this grid
+  // drains, and its consumers wait (pdl_wait) until this grid has completed
+  pdl_launch_dependents();
   const int64_t two_t = int64_t(g.planes) * g.n_tokens;  // payload rows per layer
-
-  const uint32_t par = bg.parity ? *bg.parity : 0u;  // read by every CTA before the flip
 #ifdef KVX_TRACE
   const uint32_t trace_id = g_trace_n[1];
   if (bg.done_counter && blockIdx.x == 0 && threadIdx.x == 0) KVX_TRACE_STAMP(1, trace_id, 0);
 #endif
   if (warp == CONSUMERS) {  // ---- producer: one elected thread
+    // The producer touches only this hand-off's queue slot (peer payload) and
+    // its doorbells -- nothing an earlier kernel of this stream writes -- so
+    // it runs ahead of pdl_wait: the first STAGES spans are in flight before
+    // the previous hand-off's pull has finished.
     if (lane == 0) {
       uint32_t k = 0;
       int ready_chunk = -1;  // highest chunk known to be published
+      bool ok = true;
       for (uint32_t sp = blockIdx.x; sp < bg.n_spans; sp += gridDim.x, ++k) {
         const int st = k % STAGES;
         if (k >= STAGES) mbar_wait(&empty[st], ((k / STAGES) & 1) ^ 1);
         const uint32_t layer = sp / bg.spans_per_layer;
-        if (bg.ready) {
+        if (bg.ready && ok) {
           const int c = int(layer) / bg.layers_per_chunk;
           if (c > ready_chunk) {
-            wait_ready(bg.ready + c, par ^ 1u);
+            ok = wait_ready(bg.ready + c, bg.ready_value, bg.ctl);
+            if (!ok) *reinterpret_cast<volatile uint32_t*>(&s_abort) = 1u;
             ready_chunk = c;
 #ifdef KVX_TRACE
             if (bg.done_counter && blockIdx.x == 0 && c == 0) KVX_TRACE_STAMP(1, trace_id, 1);
 #endif
           }
+        }
+        if (!ok) {  // aborted: release the consumers span by span, no data
+          mbar_arrive_empty_phase(&full[st]);
+          continue;
         }
         const int64_t r0 = int64_t(sp - layer * bg.spans_per_layer) * bg.rows_per_span;
         const int rows = int(min(int64_t(bg.rows_per_span), two_t - r0));
@@ -905,7 +991,8 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
       }
     }
   } else {
-  // ---- consumers
+  // ---- consumers: the slot mapping and the cache are stream-ordered inputs
+  pdl_wait();
   uint32_t k = 0;
   for (uint32_t sp = blockIdx.x; sp < bg.n_spans; sp += gridDim.x, ++k) {
     const int st = k % STAGES;
@@ -916,6 +1003,11 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     const __half* sbuf = reinterpret_cast<const __half*>(buf + bg.rows_per_span * bg.code_row_bytes);
     const __half* zbuf = sbuf + bg.rows_per_span * bg.meta_row_bytes / 2;
     mbar_wait(&full[st], (k / STAGES) & 1);
+    if (*reinterpret_cast<volatile uint32_t*>(&s_abort)) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      continue;
+    }
     // short rows (fewer than 32 chunks, e.g. a TP shard's few KV heads): a
     // warp covers 32 / cpr rows per pass so every lane has a chunk
     const int cpr = bg.cpr;
@@ -964,21 +1056,25 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
   }  // consumers
 
   if (bg.done_counter) {
-    // The free flag only has to say "every read of the peer half is
+    // The free flag only has to say "every read of the peer slot is
     // complete": each bulk read completed (its mbarrier phase) before the
     // consumers used the bytes, and every CTA counts itself done after that.
     // The cache stores need no ordering against the flag (the prefill side
     // never reads them), so neither a per-CTA fence nor a system-scope release
     // is needed -- they cost ~1 us and ~3.5 us on the critical path of every
-    // hand-off (tools/handoff_trace.py).
+    // hand-off (tools/handoff_trace.py).  Thread 0 is a consumer: it has
+    // passed pdl_wait, so the previous use of these counters has completed.
     __syncthreads();  // this CTA has consumed every span it owned
     if (threadIdx.x == 0) {
-      if (atomicAdd(bg.done_counter, 1u) == gridDim.x - 1) {  // last CTA of the launch
-        *bg.done_counter = 0u;
-        if (bg.parity) *bg.parity = par ^ 1u;
+      // one atomic per CTA: low 16 bits count exits, high bits aborted CTAs
+      const uint32_t inc = s_abort ? 0x10001u : 1u;
+      const uint32_t total = atomicAdd(bg.done_counter, inc) + inc;
+      if ((total & 0xFFFFu) == gridDim.x) {  // last CTA of the launch
+        bg.done_counter[0] = 0u;
         KVX_TRACE_STAMP(1, trace_id, 2);
-        asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(bg.peer_free), "r"(par ^ 1u)
-                     : "memory");
+        if ((total >> 16) == 0u)
+          asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(bg.peer_free), "r"(bg.ready_value)
+                       : "memory");
 #ifdef KVX_TRACE
         KVX_TRACE_STAMP(1, trace_id, 3);
         g_trace_n[1] = trace_id + 1;

@@ -255,11 +255,13 @@ struct KchanBulk {
   int slabs;         // ceil(row_elems / S)
   int64_t n_spans;   // n_layers * n_groups * slabs
   int stage_bytes;   // G * S * BITS/8 + 4 * S
-  // per-chunk doorbells (nullable): wait ready[layer / layers_per_chunk] ==
-  // p ^ 1 before a span's bulk reads, p = *parity (or 0) -- one launch
-  // consumes a whole hand-off while the prefill side is still producing it
+  // per-chunk doorbells (nullable): wait ready[layer / layers_per_chunk] >=
+  // ready_value (the hand-off's sequence number) before a span's bulk reads
+  // -- one launch consumes a whole hand-off while the prefill side is still
+  // producing it
   const uint32_t* ready;
-  const uint32_t* parity;
+  uint32_t ready_value;
+  Ctl* ctl;  // nullable
   int layers_per_chunk;
 };
 
@@ -271,12 +273,14 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
   constexpr int CB = 32 * BITS / 8;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ uint32_t s_abort;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], CONSUMERS);
     }
+    s_abort = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -284,21 +288,26 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
   const int code_slice = S * BITS / 8;  // bytes of one row's slab slice in smem
   if (warp == CONSUMERS) {  // ---- producer: one elected thread
     if (lane == 0) {
-      const uint32_t want = (kb.parity ? *kb.parity : 0u) ^ 1u;
       int64_t ready_chunk = -1;
       uint32_t k = 0;
+      bool ok = true;
       for (int64_t sp = blockIdx.x; sp < kb.n_spans; sp += gridDim.x, ++k) {
         const int st = k % STAGES;
         if (k >= STAGES) mbar_wait(&empty[st], ((k / STAGES) & 1) ^ 1);
         const int64_t lg = sp / kb.slabs;
         const int c0 = int(sp - lg * kb.slabs) * S;
         const int64_t layer = lg / g.n_groups, grp = lg - layer * g.n_groups;
-        if (kb.ready) {
+        if (kb.ready && ok) {
           const int64_t c = layer / kb.layers_per_chunk;
           if (c > ready_chunk) {
-            wait_ready(kb.ready + c, want);
+            ok = wait_ready(kb.ready + c, kb.ready_value, kb.ctl);
+            if (!ok) *reinterpret_cast<volatile uint32_t*>(&s_abort) = 1u;
             ready_chunk = c;
           }
+        }
+        if (!ok) {  // aborted: release the consumers span by span, no data
+          mbar_arrive_empty_phase(&full[st]);
+          continue;
         }
         const int ns = min(S, g.row_elems - c0);
         const uint32_t rb = uint32_t(ns) * BITS / 8, mb = uint32_t(ns) * 2;
@@ -332,7 +341,7 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
       const int ns = min(S, g.row_elems - c0);
       const uint8_t* buf = smem + st * kb.stage_bytes;
       mbar_wait(&full[st], (k / STAGES) & 1);
-      if (c * 32 < ns) {
+      if (c * 32 < ns && !*reinterpret_cast<volatile uint32_t*>(&s_abort)) {
         const uint4* sv = reinterpret_cast<const uint4*>(buf + G * code_slice + c * 64);
         const uint4* zv = reinterpret_cast<const uint4*>(buf + G * code_slice + 2 * S + c * 64);
         uint32_t sw[16], zw[16];

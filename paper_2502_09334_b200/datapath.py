@@ -292,28 +292,30 @@ def _quant_pack_layers(src: KVPlanes, packed: PackedKV, l0: int, l1: int, stream
 
 def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
                            stream=None, bulk: bool = False, ready: tuple | None = None,
-                           done: tuple | None = None) -> None:
+                           done: tuple | None = None, ctl: int | None = None,
+                           pdl: bool = False) -> None:
     """K3 on layers [l0, l1).  ``bulk``: TMA bulk-staged variant (for payloads
-    read over NVLink).  ``ready=(flags_addr, layers_per_chunk)``: the bulk
-    kernel waits in-kernel for each chunk's doorbell (one launch per
-    hand-off).  ``done=(counter_addr, peer_free_addr, parity_addr)``: in-kernel
-    completion (release the prefill-side queue half, flip the half's parity;
-    see kvx.h for the protocol)."""
+    read over NVLink).  ``ready=(flags_addr, value, layers_per_chunk)``: the
+    bulk kernel waits in-kernel until each chunk's doorbell reaches ``value``
+    (one launch per hand-off).  ``done=(counter_addr, peer_free_addr)``:
+    in-kernel completion (the last CTA sets the prefill side's free flag to
+    ``value``; see kvx.h for the sequence protocol).  ``ctl``: control block
+    (abort / timeout of the waits).  ``pdl``: programmatic dependent launch."""
     with nvtx_range(f"kvx.K3 layers[{l0},{l1})"):
-        _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done)
+        _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done, ctl, pdl)
 
 
-def _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done) -> None:
+def _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done, ctl, pdl) -> None:
     lay = packed.layout
     k, v = dst.ptrs(l0)
     c, s, z = packed.ptrs(l0)
     args = (c, s, z, lay.layer_stride, dst.slots_ptr, l1 - l0, lay.n_tokens, lay.n_heads,
             lay.head_dim, lay.group, lay.bits, k, v, dst.layer_stride, *dst.window_args)
     if bulk or ready is not None:
-        rf, lpc = ready if ready is not None else (None, 1)
-        dc, pf, par = done if done is not None else (None, None, None)
-        _lib.call("kvx_pull_dequant_scatter_paged", *args, rf, lpc, dc, pf, par,
-                  _stream_ptr(stream))
+        rf, rv, lpc = ready if ready is not None else (None, 0, 1)
+        dc, pf = done if done is not None else (None, None)
+        _lib.call("kvx_pull_dequant_scatter_paged", *args, rf, rv, lpc, dc, pf, ctl,
+                  _lib.KVX_PULL_PDL if pdl else 0, _stream_ptr(stream))
     else:
         _lib.call("kvx_dequant_scatter_paged", *args, _stream_ptr(stream))
 
@@ -458,6 +460,7 @@ class HandoffPlan:
             self.d_stream = torch.cuda.Stream() if not same else self.p_stream
             self.c_stream = torch.cuda.Stream() if mode == "copy" else None
             self.copy_done = [torch.cuda.Event() for _ in self.chunks]
+            self.d_idle = torch.cuda.Event()  # the previous run's last K3 (never recorded: no-op)
 
     @property
     def packed(self) -> PackedKV:
@@ -471,9 +474,16 @@ class HandoffPlan:
         the stream each kernel is launched on ({"k1": (start, end), "k3": ...})."""
         with torch.cuda.device(self.p_dev):
             self.p_stream.wait_stream(torch.cuda.current_stream(self.p_dev))
+            if self.d_dev != self.p_dev:
+                # write-after-read across devices: this run's K1 (pull/push) or
+                # copy must not overwrite the payload buffer while the previous
+                # run's K3 (or copy) on the decode side may still read it
+                self.p_stream.wait_event(self.d_idle)
         if self.d_dev != self.p_dev:
             with torch.cuda.device(self.d_dev):
                 self.d_stream.wait_stream(torch.cuda.current_stream(self.d_dev))
+                if self.c_stream is not None:
+                    self.c_stream.wait_event(self.d_idle)
         for i, (l0, l1) in enumerate(self.chunks):
             ev = {} if timing is not None else None
             with torch.cuda.device(self.p_dev):
@@ -505,6 +515,8 @@ class HandoffPlan:
                     timing.append(ev)
         with torch.cuda.device(self.d_dev):
             torch.cuda.current_stream(self.d_dev).wait_stream(self.d_stream)
+            if self.d_dev != self.p_dev:
+                self.d_idle.record(self.d_stream)  # every read of p_buf/d_buf done
         if self.d_dev != self.p_dev:
             with torch.cuda.device(self.p_dev):
                 torch.cuda.current_stream(self.p_dev).wait_stream(self.p_stream)

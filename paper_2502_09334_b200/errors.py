@@ -24,3 +24,11 @@ if _RefNoPath is not None:  # pragma: no cover
 else:
     class NoPath(PlanningError):
         """No usable link between two replicas (errors.py:12-13)."""
+
+
+class PartnerLost(NoPath):
+    """The other end of a prefill -> decode channel stopped answering: an
+    in-kernel doorbell wait was aborted (``PairChannel.abort``) or outlived
+    the channel's timeout.  A NoPath: the link to that replica is gone
+    (``costs.py:63-64``); the CUDA context and the local KV cache are intact,
+    the channel is not (open a new one)."""

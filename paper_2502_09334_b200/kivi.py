@@ -165,7 +165,7 @@ def decompress_kivi_into_paged(packed: PackedKiviKV, k_cache: torch.Tensor, v_ca
             lay.n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
             dst.layer_stride)
     if bulk:
-        _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args, None, 1, None,
+        _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args, None, 0, 1, None,
                   _stream_ptr(stream))
     else:
         _lib.call("kvx_dequant_scatter_paged_kivi", *args, _stream_ptr(stream))

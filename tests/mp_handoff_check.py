@@ -10,7 +10,9 @@ import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
+import _mp  # noqa: E402
 from oracle import kvq_oracle as O  # noqa: E402
 from paper_2502_09334_b200.datapath import KVPlanes  # noqa: E402
 from paper_2502_09334_b200.transport import ChannelSpec, PairChannel  # noqa: E402
@@ -18,20 +20,13 @@ from paper_2502_09334_b200.transport import ChannelSpec, PairChannel  # noqa: E4
 
 def main():
     modes = sys.argv[1].split(",") if len(sys.argv) > 1 else ["pull", "push", "copy", "nccl"]
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    ctrl = dist.new_group(backend="gloo")
+    rank, world, dev, ctrl, same_gpu = _mp.init()
+    if same_gpu:
+        modes = [m for m in modes if m != "nccl"]
     L, Tmax, H, D, bs = 6, 200, 8, 128, 16
     failures = 0
-    # several hand-offs of varying length; repeated lengths exercise the CUDA
-    # graph capture (2nd time) and replay (3rd time) of the pull modes, on
-    # both halves of the double-buffered queue
-    # (flags are per (queue half, parity): the same size recurs on the same
-    # (half, parity) every 4th hand-off -- eager, capture, replay -- and an
-    # empty hand-off in between must consume no epoch on either side)
+    # several hand-offs of varying length on both slots of the double-buffered
+    # queue; an empty hand-off in between must consume no epoch on either side
     seq = (Tmax, 77) * 3 + (0,) + (Tmax, 77) * 3 + (130, Tmax)
     for mode in modes:
         for bits in ((2, 4, 8, 16) if mode == "pull" else (4, 8, 16)):
@@ -80,8 +75,7 @@ def main():
                         print(f"MISMATCH rank={rank} mode={mode} bits={bits} T={T} epoch={epoch}",
                               flush=True)
             if mode.startswith("pull") and rank == 0:
-                print(f"{mode} bits={bits}: graphs={ch.graphs} captured={len(ch._graphs)}",
-                      flush=True)
+                print(f"{mode} bits={bits}: native pair={ch._pair is not None}", flush=True)
             dist.barrier()
             ch.close()
     # layer-wise hand-off during prefill: the prefill side publishes chunks as
@@ -185,9 +179,9 @@ def main():
     ch.close()
 
     # one channel, every path mixed (same random choices on both ranks): the
-    # fused graph-replayed hand-off, the staged host-buffer path (per-chunk K1
-    # + memops on P), layer-wise streaming, and empty hand-offs -- all share
-    # the queue halves and the parity doorbells
+    # fused native hand-off, the staged host-buffer path (per-chunk K1 +
+    # memops on P), layer-wise streaming, and empty hand-offs -- all share the
+    # queue slots and the sequence doorbells
     for Q in (2, 1, 3):  # queue depths (1: no run-ahead at all)
         spec = ChannelSpec(L, Tmax, H, D, 4, 128, 3, "pull", queue_depth=Q)
         ch = PairChannel(spec, rank, world, control_group=ctrl)
@@ -241,7 +235,42 @@ def main():
                         print(f"MISMATCH mixed Q={Q} rank={rank} epoch={epoch} path={path} T={T}",
                               flush=True)
         if rank == 0:
-            print(f"mixed paths Q={Q}: graphs={ch.graphs} captured={len(ch._graphs)}", flush=True)
+            print(f"mixed paths Q={Q}: ok", flush=True)
+        dist.barrier()
+        ch.close()
+
+    # stale-doorbell regression (round-1 advice): long hand-offs publish many
+    # layer chunks, short ones a single chunk, alternating on the SAME queue
+    # slots; a doorbell left by a long use must never let the slot's next
+    # long use be read before its chunks are written.  Whole-tensor check
+    # against a local K1 -> K3 on the decode GPU.
+    Lr, Hr, Tl = 8, 8, 6144
+    for Q in (1, 2):
+        spec = ChannelSpec(Lr, Tl, Hr, D, 4, 128, 8, "pull", queue_depth=Q)
+        ch = PairChannel(spec, rank, world, control_group=ctrl)
+        Ts = [Tl if (i // Q) % 2 == 0 else 48 for i in range(6 * Q)]
+        nbr = Tl // bs + 8
+        if ch.role == "decode":
+            kcr = torch.zeros((Lr, nbr, bs, Hr, D), dtype=torch.float16, device=dev)
+            vcr = torch.zeros_like(kcr)
+        for i, T in enumerate(Ts):
+            g = torch.Generator(device=dev).manual_seed(300 + i + 1000 * ch.pair)
+            kv = torch.randn((Lr, 2, T, Hr, D), generator=g, device=dev).half()
+            if ch.role == "prefill":
+                ch.send(KVPlanes.dense(kv), T)
+            else:
+                sl = torch.randperm(nbr * bs, generator=torch.Generator().manual_seed(i))[:T].to(dev)
+                kcr.zero_(); vcr.zero_()
+                ch.recv(KVPlanes.paged(kcr, vcr, sl), T)
+                rk, rv = _mp.local_reference(kv, kcr.shape, sl)
+                torch.cuda.synchronize()
+                ch.check()
+                if not (torch.equal(kcr, rk) and torch.equal(vcr, rv)):
+                    failures += 1
+                    print(f"MISMATCH long/short Q={Q} rank={rank} i={i} T={T}", flush=True)
+        torch.cuda.synchronize()
+        if rank == 0:
+            print(f"long/short alternation Q={Q}: ok", flush=True)
         dist.barrier()
         ch.close()
 
@@ -286,12 +315,11 @@ def main():
         print(f"queue_depth={Q}: prefill ran {Q} hand-offs ahead", flush=True)
     dist.barrier()
     ch.close()
-    f = torch.tensor([failures], device=dev)
-    dist.all_reduce(f)
+    f = _mp.total(failures, ctrl)
     if rank == 0:
-        print(f"mp_handoff_check modes={modes} world={world} failures={int(f.item())}", flush=True)
+        print(f"mp_handoff_check modes={modes} world={world} failures={f}", flush=True)
     dist.destroy_process_group()
-    sys.exit(1 if f.item() else 0)
+    sys.exit(1 if f else 0)
 
 
 if __name__ == "__main__":

@@ -10,19 +10,16 @@ import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
+import _mp  # noqa: E402
 from oracle import kvq_oracle as O  # noqa: E402
 from paper_2502_09334_b200.datapath import KVPlanes  # noqa: E402
 from paper_2502_09334_b200.transport import TPHandoff  # noqa: E402
 
 
 def main():
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    ctrl = dist.new_group(backend="gloo")
+    rank, world, dev, ctrl, _ = _mp.init()
     L, H, D, bs = 4, 8, 128, 16
     failures = 0
     scenarios = [([0], [1, 2]), ([0, 1], [2]), ([0, 1], [2, 3]), ([3], [0, 1]), ([1, 2, 3, 0], [0, 2])]
@@ -103,12 +100,11 @@ def main():
     dist.barrier()
     for ch in chans.values():
         ch.close()
-    f = torch.tensor([failures], device=dev)
-    dist.all_reduce(f)
+    f = _mp.total(failures, ctrl)
     if rank == 0:
-        print(f"mp_tp_check failures={int(f.item())}", flush=True)
+        print(f"mp_tp_check failures={f}", flush=True)
     dist.destroy_process_group()
-    sys.exit(1 if f.item() else 0)
+    sys.exit(1 if f else 0)
 
 
 if __name__ == "__main__":

@@ -119,7 +119,8 @@ def test_no_cpu_fallback(monkeypatch, tmp_path):
 def test_integration_doc_bindings_match():
     """The ctypes stub INTEGRATION.md shows a maintainer matches the real ABI."""
     src = open(os.path.join(ROOT, "INTEGRATION.md")).read()
-    m = {"P": ctypes.c_void_p, "I": ctypes.c_int, "I64": ctypes.c_int64, "U32": ctypes.c_uint32}
+    m = {"P": ctypes.c_void_p, "I": ctypes.c_int, "I64": ctypes.c_int64, "U32": ctypes.c_uint32,
+         "U64": ctypes.c_uint64, "PP": ctypes.POINTER(ctypes.c_void_p)}
     found = re.findall(r"kvx\.(kvx_\w+)\.argtypes = \[([^\]]*)\]", src)
     assert len(found) >= 4
     for name, body in found:
@@ -131,19 +132,25 @@ def test_fused_and_kivi_entry_points_validate(lib):
     """The transport's fused kernels and the kivi pull variant reject bad
     arguments before touching CUDA (no GPU here)."""
     E = _lib.KVX_ERR_INVALID_ARG
-    # K1 with doorbells: 16-bit has no doorbell variant; misaligned counters
+    # K1 with doorbells: 16-bit has no doorbell variant; misaligned counters;
+    # misaligned control block
     assert lib.kvx_quant_pack_signal(256, 256, 0, None, 1, 1, 1, 128, 128, 16, 256, 256, 256, 0,
-                                     0, 0, 256, 256, 1, None, None, None) == E
+                                     0, 0, 256, 256, 1, 1, None, 0, None, None) == E
     assert lib.kvx_quant_pack_signal(256, 256, 0, None, 1, 1, 1, 128, 128, 4, 256, 256, 256, 0,
-                                     0, 0, 258, 256, 1, None, None, None) == E
-    # K3-bulk: a parity state needs the in-kernel completion (done counter)
+                                     0, 0, 258, 256, 1, 1, None, 0, None, None) == E
+    assert lib.kvx_quant_pack_signal(256, 256, 0, None, 1, 1, 1, 128, 128, 4, 256, 256, 256, 0,
+                                     0, 0, 256, 256, 1, 1, None, 0, 260, None) == E
+    # K3-bulk: in-kernel completion needs doorbells; unknown flags
     assert lib.kvx_pull_dequant_scatter_paged(256, 256, 256, 0, None, 1, 1, 1, 128, 128, 4, 256,
-                                              256, 0, 0, 0, 256, 1, None, None, 512,
+                                              256, 0, 0, 0, None, 1, 1, 256, 512, None, 0,
+                                              None) == E
+    assert lib.kvx_pull_dequant_scatter_paged(256, 256, 256, 0, None, 1, 1, 1, 128, 128, 4, 256,
+                                              256, 0, 0, 0, 256, 1, 1, None, None, None, 4,
                                               None) == E
     offs = (ctypes.c_int64 * 7)(*([0] * 7))
     for fn in ("kvx_dequant_scatter_paged_kivi", "kvx_pull_dequant_scatter_paged_kivi"):
         f = getattr(lib, fn)
-        tail = (None,) if fn.startswith("kvx_dequant") else (None, 1, None, None)
+        tail = (None,) if fn.startswith("kvx_dequant") else (None, 0, 1, None, None)
         # kivi: bits 2 and group 128 are not kivi formats
         assert f(256, 256, offs, 256, None, 0, None, 0, 1, 1, 1, 128, 32, 2, 256, 256, 0,
                  *tail) == E
@@ -154,5 +161,54 @@ def test_fused_and_kivi_entry_points_validate(lib):
                  *tail) == E
     # the pull variant's doorbells must be aligned
     assert lib.kvx_pull_dequant_scatter_paged_kivi(256, 256, offs, 256, None, 0, None, 0, 1, 32,
-                                                   1, 128, 32, 4, 256, 256, 0, 258, 1, None,
+                                                   1, 128, 32, 4, 256, 256, 0, 258, 1, 1, None,
                                                    None) == E
+
+
+def test_8bit_payload_stride_must_keep_32_byte_alignment(lib):
+    """8-bit codes move as 32-byte vectors (st/ld.global.v8.b32): a payload
+    layer stride that is a 16-byte but not a 32-byte multiple (48) would
+    fault with a misaligned address on layer 1 -- the ABI rejects it."""
+    E = _lib.KVX_ERR_INVALID_ARG
+    # (k, v, src_ls, slots, L=2, T=1, H=1, D=128, G=128, bits, codes, scale, zero, stride, ...)
+    assert lib.kvx_quant_pack(256, 256, 0, None, 2, 1, 1, 128, 128, 8, 256, 256, 256, 48, 0, 0,
+                              None) == E
+    assert lib.kvx_dequant_scatter_paged(256, 256, 256, 48, None, 2, 1, 1, 128, 128, 8, 256, 256,
+                                         0, 0, 0, None) == E
+    # 48 is fine at 4 bits (16-byte vectors): validation passes, the launch
+    # then fails only for want of a GPU on this host
+    rc = lib.kvx_quant_pack(256, 256, 0, None, 2, 1, 1, 128, 128, 4, 256, 256, 256, 48, 0, 0, None)
+    assert rc != E
+    # kivi: the 8-bit V codes (seg_offsets[4]) and the layer stride
+    offs = (ctypes.c_int64 * 7)(0, 256, 512, 768, 1040, 2048, 2304)  # 1040 = 16 mod 32
+    assert lib.kvx_quant_pack_kivi(256, 256, 0, 1, 32, 1, 128, 32, 8, 256, 1, None, 0, 256, 4096,
+                                   offs, None) == E
+    offs = (ctypes.c_int64 * 7)(0, 256, 512, 768, 1024, 2048, 2304)
+    assert lib.kvx_quant_pack_kivi(256, 256, 0, 1, 32, 1, 128, 32, 8, 256, 1, None, 0, 256, 4112,
+                                   offs, None) == E
+
+
+def test_pair_entry_points_validate(lib):
+    """kvx_pair_*: bad roles, formats, queue depths and alignments are
+    rejected before any allocation (no GPU here); the chunk plan is pure."""
+    E = _lib.KVX_ERR_INVALID_ARG
+    out = ctypes.c_void_p()
+    good = (0, 80, 4096, 8, 128, 4, 128, 2, 0, 4096, 8192, 1 << 20, 1 << 24, None)
+    assert lib.kvx_pair_create(2, *good[1:], ctypes.byref(out)) == E      # role
+    assert lib.kvx_pair_create(*good[:5], 16, *good[6:], ctypes.byref(out)) == E  # 16-bit
+    assert lib.kvx_pair_create(*good[:7], 9, *good[8:], ctypes.byref(out)) == E   # Q > 8
+    assert lib.kvx_pair_create(*good[:11], 4096 + 16, *good[12:], ctypes.byref(out)) == E  # queue
+    assert lib.kvx_pair_create(*good[:13], 12, ctypes.byref(out)) == E   # ctl alignment
+    assert lib.kvx_pair_send(None, 1, 256, 256, 0, None, 1, 0, 0, 0, None) == E
+    assert lib.kvx_pair_recv(None, 1, 256, 256, 0, 256, 1, 0, 0, 0, None) == E
+    assert lib.kvx_pair_destroy(None) == 0
+    lpc, nc = ctypes.c_int(), ctypes.c_int()
+    # a 16-token 70B GQA hand-off is one chunk; config 3 is layer-granular
+    assert lib.kvx_handoff_chunk_plan(80, 16, 8, 128, 0, ctypes.byref(lpc), ctypes.byref(nc)) == 0
+    assert (lpc.value, nc.value) == (80, 1)
+    assert lib.kvx_handoff_chunk_plan(40, 16384, 40, 128, 0, ctypes.byref(lpc),
+                                      ctypes.byref(nc)) == 0
+    assert (lpc.value, nc.value) == (1, 40)
+    assert lib.kvx_handoff_chunk_plan(80, 16, 8, 128, 1, ctypes.byref(lpc), ctypes.byref(nc)) == 0
+    assert (lpc.value, nc.value) == (2, 40)  # layer-wise: <= 64 chunks
+    assert lib.kvx_handoff_chunk_plan(0, 16, 8, 128, 0, ctypes.byref(lpc), ctypes.byref(nc)) == E

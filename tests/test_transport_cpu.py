@@ -128,52 +128,106 @@ def test_kivi_capacity_covers_every_split():
         ChannelSpec(5, 300, 4, 128, 4, 32, 3, "push", format="kivi")
 
 
-def _simulate_protocol(schedule, n_handoffs, Q=2):
-    """Discrete model of the pull doorbells (PairChannel._parity, kvx.h).
+def _geq(flag: int, value: int) -> bool:
+    """The kernels' wrap-safe doorbell test (int32)(flag - value) >= 0."""
+    return ((flag - value) & 0xFFFFFFFF) < (1 << 31)
 
-    P (prefill) and D (decode) each process hand-offs 1..n in order over Q
-    queue slots.  Flags: ready[h] on D, free[h] on P, and each side's parity
-    state[h]; nothing is ever reset.  ``schedule`` picks which side tries to
-    move next.  Returns the order in which hand-offs were produced / consumed
-    and checks the safety properties at every step."""
-    from paper_2502_09334_b200.transport import PairChannel
-    ch = PairChannel.__new__(PairChannel)  # only the slot/parity arithmetic
-    ch.Q = Q
-    ready = [0] * Q; free = [0] * Q; p_state = [0] * Q; d_state = [0] * Q
-    produced = []; consumed = []
-    p_next = d_next = 1
+
+def _simulate_protocol(schedule, chunks_of, Q=2, parity=False):
+    """Discrete model of the pull doorbells (kvx.h sequence protocol).
+
+    P (prefill) and D (decode) process hand-offs 1..n in order over Q queue
+    slots; hand-off e publishes ``chunks_of[e - 1]`` layer chunks (the chunk
+    plan depends on its token count).  Flags: ready[h][c] on D, free[h] on P;
+    nothing is ever reset.  ``schedule`` picks which side tries to move next
+    (one chunk per move).  Checks the safety properties at every step and
+    returns (produced, consumed).  ``parity=True`` models round 1's parity
+    flags (ready = p ^ 1, equality waits) for the regression test."""
+    from paper_2502_09334_b200.transport import seq_of
+    n = len(chunks_of)
+    ready = [[0] * 64 for _ in range(Q)]
+    free = [0] * Q
+    published, produced, consumed = set(), [], []
+    pe, pc, de, dc = 1, 0, 1, 0
     for who in schedule:
-        if who == "P" and p_next <= n_handoffs:
-            e = p_next; h = ch._slot(e); p = p_state[h]
-            assert p == ch._parity(e)  # the device state matches the host's epoch parity
-            if free[h] != p:
-                continue  # P waits: D has not consumed the slot's last use
-            # safe to overwrite slot h: its previous use (if any) is consumed
-            assert e <= Q or (e - Q) in consumed
-            produced.append(e); ready[h] = p ^ 1; p_state[h] = p ^ 1; p_next += 1
-        elif who == "D" and d_next <= n_handoffs:
-            e = d_next; h = ch._slot(e); p = d_state[h]
-            assert p == ch._parity(e)
-            if ready[h] != p ^ 1:
+        if who == "P" and pe <= n:
+            h, v = seq_of(pe, Q)
+            if pc == 0:
+                ok = free[h] == (v - 1) & 1 if parity else _geq(free[h], v - 1)
+                if not ok:
+                    continue  # P waits: D has not consumed the slot's last use
+                # safe to overwrite slot h: its previous use (if any) is consumed
+                assert pe <= Q or (pe - Q) in consumed
+            ready[h][pc] = (v & 1) if parity else v  # parity: p ^ 1 with p = (v - 1) & 1
+            published.add((pe, pc))
+            pc += 1
+            if pc == chunks_of[pe - 1]:
+                produced.append(pe)
+                pe, pc = pe + 1, 0
+        elif who == "D" and de <= n:
+            h, v = seq_of(de, Q)
+            ok = ready[h][dc] == (v & 1) if parity else _geq(ready[h][dc], v)
+            if not ok:
                 continue  # K3 waits in-kernel for the doorbell
-            assert e in produced  # never reads a slot before it is written
-            consumed.append(e); free[h] = p ^ 1; d_state[h] = p ^ 1; d_next += 1
+            # never reads a chunk before it is written
+            assert (de, dc) in published, f"hand-off {de} chunk {dc} read before it was written"
+            dc += 1
+            if dc == chunks_of[de - 1]:
+                consumed.append(de)
+                free[h] = (v & 1) if parity else v
+                de, dc = de + 1, 0
         # P never runs more than Q hand-offs ahead
-        assert p_next - d_next <= Q
+        assert pe - de <= Q
     return produced, consumed
 
 
 @pytest.mark.parametrize("Q", [1, 2, 3, 8])
-def test_parity_doorbells_are_safe_and_live(Q):
-    """Every interleaving: no slot is overwritten before it is consumed, none
+def test_sequence_doorbells_are_safe_and_live(Q):
+    """Every interleaving, hand-offs of random chunk counts (the plan follows
+    the token count): no slot is overwritten before it is consumed, no chunk
     is consumed before it is produced, progress never stalls, and P can run a
     full queue (Q hand-offs) ahead of D."""
     import random
     rng = random.Random(Q)
     for trial in range(300):
         n = rng.randint(1, 4 * Q + 4)
-        sched = [rng.choice("PPD" if trial % 2 else "PDD") for _ in range(400)]
-        produced, consumed = _simulate_protocol(sched + list("PD") * 2 * n, n, Q)
+        chunks = [rng.choice((1, 1, 2, 5, 40)) for _ in range(n)]
+        sched = [rng.choice("PPD" if trial % 2 else "PDD") for _ in range(2000)]
+        produced, consumed = _simulate_protocol(sched + list("PD") * 50 * n, chunks, Q)
         assert produced == list(range(1, n + 1)) and consumed == produced
-    produced, _ = _simulate_protocol("P" * (Q + 3), Q + 3, Q)
+    produced, _ = _simulate_protocol("P" * (Q + 3), [1] * (Q + 3), Q)
     assert produced == list(range(1, Q + 1))  # a full queue, then P waits
+
+
+@pytest.mark.parametrize("Q", [1, 2])
+def test_parity_doorbells_were_unsafe_for_varying_chunk_counts(Q):
+    """Regression (round-1 advice): with parity flags, a long hand-off leaves
+    ready[h][1..] at a parity value that the slot's use two turns later
+    accepts, so D reads chunks P has not written yet.  Sequence numbers
+    cannot be satisfied by an older use's flag."""
+    # every slot is used long, short, long (a slot's uses are Q hand-offs apart)
+    chunks = [40 if ((e - 1) // Q) % 2 == 0 else 1 for e in range(1, 3 * Q + 1)]
+    sched = ("P" * 41 + "D" * 41) * (2 * len(chunks))
+    with pytest.raises(AssertionError, match="read before it was written"):
+        # P publishes only chunk 0 of the third use before D runs ahead
+        _simulate_protocol(_lockstep(chunks), chunks, Q, parity=True)
+    produced, consumed = _simulate_protocol(_lockstep(chunks), chunks, Q)
+    assert consumed == list(range(1, len(chunks) + 1))
+    produced, consumed = _simulate_protocol(sched, chunks, Q)
+    assert consumed == list(range(1, len(chunks) + 1))
+
+
+def _lockstep(chunks):
+    """P publishes one chunk, then D tries to consume everything it can."""
+    return ("P" + "D" * 64) * (sum(chunks) * 4)
+
+
+def test_seq_of_matches_kernel_rule():
+    from paper_2502_09334_b200.transport import seq_of
+    # hand-off e uses slot e % Q for the v-th time
+    for Q in (1, 2, 3, 8):
+        uses = {}
+        for e in range(1, 50):
+            h, v = seq_of(e, Q)
+            uses[h] = uses.get(h, 0) + 1
+            assert h == e % Q and v == uses[h]

@@ -26,7 +26,7 @@ import torch.distributed as dist  # noqa: E402
 
 import bench as B  # noqa: E402
 from paper_2502_09334_b200.datapath import KVPlanes  # noqa: E402
-from paper_2502_09334_b200.transport import ChannelSpec, PairChannel, exchange, wait_eq  # noqa: E402
+from paper_2502_09334_b200.transport import ChannelSpec, PairChannel, exchange, wait  # noqa: E402
 
 
 def main():
@@ -50,7 +50,7 @@ def main():
     out = {}
     for mode in ("after", "stream"):
         spec = ChannelSpec(L, T, H, D, 4, 128, 8, "pull", layerwise=(mode == "stream"))
-        ch = PairChannel(spec, rank, world, control_group=ctrl, graphs=False)
+        ch = PairChannel(spec, rank, world, control_group=ctrl)
         if ch.role == "prefill":
             kv = B.synthetic_kv_device(torch, L, T, H, D, dev, seed=0)
             planes = KVPlanes.dense(kv)
@@ -76,11 +76,11 @@ def main():
                     sess.close()
                 else:
                     ch.send(planes, T)
-                # the decode side sets free[h] = parity ^ 1 when its K3 has
-                # consumed the half
-                h, p = ch._slot(ch.epoch), ch._parity(ch.epoch)
+                # the decode side sets free[h] = v when its K3 has consumed
+                # the slot (the sequence protocol)
+                h, v = ch._seq(ch.epoch)
                 cur = torch.cuda.current_stream()
-                wait_eq(ch._pfree(ch.flags.ptr, h), p ^ 1, cur)
+                wait(ch._pfree(ch.flags.ptr, h), v, cur)
                 e_done.record()
                 torch.cuda.synchronize()
                 if rep:
