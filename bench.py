@@ -191,10 +191,25 @@ def cpu_reference(workload: str, bits: int, group: int, budget_s: float | None =
             break
     fp16_bytes = layers * 2 * T * H * D * 2
     return dict(value=fp16_bytes / elapsed / 1e9, unit=UNIT, cores=C.threads(), kind="port",
+                cpu_model=cpu_model(), affinity=len(os.sched_getaffinity(0)),
+                simd="avx2+f16c+fma" if C.simd() else "scalar",
                 sample=f"{layers} layers ({layers / L:.2f} passes over the {L}) of {workload} "
                        f"({fp16_bytes / 1e9:.2f} GB fp16), "
-                       f"oracle/kvq_oracle.c quant+pack+dequant+paged-scatter, "
-                       f"{C.threads()} OpenMP threads, {elapsed:.2f} s")
+                       f"oracle/kvq_oracle.c quant+pack+dequant+paged-scatter "
+                       f"({'AVX2/F16C' if C.simd() else 'scalar'}), "
+                       f"{C.threads()} OpenMP threads on {cpu_model()}, {elapsed:.2f} s")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
 
 
 def run_reference(args, rank: int, world: int):
@@ -219,15 +234,35 @@ def run_reference(args, rank: int, world: int):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * statistics.median(secs), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp16->u4", "data": "synthetic",
-        "config": {"workload": wl, "bits": bits, "group": group, "block_size": BLOCK,
-                   "sample_layers_per_step": args.ref_layers},
+        "config": base_config(wl, bits, group, args.format, fp16_bytes_of(wl)),
+        "run": {"sample_layers_per_step": args.ref_layers},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": r["cores"],
-                         "kind": "port", "sample": r["sample"]},
+                         "kind": "port", "cpu_model": r["cpu_model"], "affinity": r["affinity"],
+                         "simd": r["simd"],
+                         "sample": f"each step: {args.ref_layers} of the workload's {L} layers "
+                                   f"(bounded sample; GB/s is per fp16 byte processed); "
+                                   + r["sample"]},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(out), flush=True)
+
+
+def fp16_bytes_of(wl: str):
+    """fp16 KV bytes of one step of a fixed workload (None for traces)."""
+    if wl not in WORKLOADS:
+        return None
+    L, H, D, b, s = WORKLOADS[wl]
+    return L * 2 * b * s * H * D * 2
+
+
+def base_config(wl, bits, group, fmt, fp16_bytes):
+    """The workload identity both arms print (the same dict for the same run)."""
+    l2 = ("inputs larger than L2 (no flush)" if fp16_bytes and fp16_bytes > L2_BYTES else
+          "inputs fit in L2 (126 MB): a latency-bound workload, no bandwidth claim")
+    return {"workload": wl, "bits": bits, "group": group, "block_size": BLOCK,
+            "format": fmt, "l2": l2}
 
 
 def default_pair_workload(world: int) -> str:
@@ -707,12 +742,10 @@ def emit(args, r, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp16" if args.bits == 16 else f"fp16->u{args.bits}",
         "data": "synthetic",
-        "config": {"workload": r["workload"], "bits": args.bits, "group": args.group,
-                   "block_size": BLOCK, "fp16_bytes_per_step": r["fp16_bytes"],
-                   "wire_bytes_per_step": r["wire_bytes"],
-                   "l2": ("inputs larger than L2 (no flush)" if r["fp16_bytes"] > L2_BYTES else
-                          "inputs fit in L2 (126 MB): a latency-bound workload, no bandwidth "
-                          "claim"), **r.get("extra", {})},
+        "config": base_config(r["workload"], args.bits, args.group, args.format,
+                              r["fp16_bytes"]),
+        "run": {"fp16_bytes_per_step": r["fp16_bytes"], "wire_bytes_per_step": r["wire_bytes"],
+                **r.get("extra", {})},
         "roofline": r["roofline"],
         "cpu_baseline": r["cpu"],
         "e2e": r["e2e"],

@@ -33,6 +33,8 @@ def lib():
         L.kvq_quant_pack.argtypes = [P, I64, I, I, I, P, P, P]
         L.kvq_dequant.argtypes = [P, P, P, I64, I, I, I, P]
         L.kvq_dequant_scatter_paged.argtypes = [P, P, P, P, I64, I64, I, I, I, I, P, P, I64]
+        L.kvq_quant_pack_scalar.argtypes = [P, I64, I, I, I, P, P, P]
+        L.kvq_dequant_scalar.argtypes = [P, P, P, I64, I, I, I, P]
         L.kvq_threads.argtypes = []
         L.kvq_set_threads.argtypes = [ctypes.c_int]
         # all host threads this process may use (torchrun exports OMP_NUM_THREADS=1)
@@ -47,6 +49,35 @@ def _p(a):
 
 def threads() -> int:
     return lib().kvq_threads()
+
+
+def simd() -> bool:
+    """True when the library was built with its AVX2/F16C/FMA path."""
+    return bool(lib().kvq_simd())
+
+
+def quant_pack_scalar(x: np.ndarray, bits: int = 4, group: int = 128):
+    """The scalar statement of quant_pack (single thread), for SIMD == scalar checks."""
+    x = np.ascontiguousarray(x, dtype=np.float16)
+    rows, d = x.shape
+    ng = d // group
+    codes = np.empty((rows, d * bits // 8), np.uint8)
+    scale = np.empty((rows, ng), np.float16)
+    zero = np.empty((rows, ng), np.float16)
+    rc = lib().kvq_quant_pack_scalar(_p(x), rows, d, group, bits, _p(codes), _p(scale), _p(zero))
+    if rc:
+        raise ValueError(f"kvq_quant_pack_scalar rc={rc}")
+    return codes, scale, zero
+
+
+def unpack_dequant_scalar(codes, scale, zero, bits: int, group: int, head_dim: int):
+    out = np.empty((codes.shape[0], head_dim), np.float16)
+    rc = lib().kvq_dequant_scalar(_p(np.ascontiguousarray(codes)), _p(np.ascontiguousarray(scale)),
+                                  _p(np.ascontiguousarray(zero)), codes.shape[0], head_dim, group,
+                                  bits, _p(out))
+    if rc:
+        raise ValueError(f"kvq_dequant_scalar rc={rc}")
+    return out
 
 
 def quant_pack(x: np.ndarray, bits: int = 4, group: int = 128):

@@ -103,6 +103,39 @@ def test_numpy_and_c_restatements_agree(bits, group, patterns):
     assert np.isfinite(da).all()
 
 
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("group", [32, 64, 128])
+def test_c_simd_and_scalar_statements_agree(bits, group):
+    """The AVX2/F16C baseline path equals the scalar statement and numpy."""
+    assert C.simd(), "oracle/Makefile should build the AVX2/F16C path on x86-64"
+    x = _random_rows(3000, 77 + bits + group, True)
+    a = C.quant_pack(x, bits, group)
+    b = C.quant_pack_scalar(x, bits, group)
+    for p, q in zip(a, b):
+        assert np.array_equal(np.asarray(p).view(np.uint8), np.asarray(q).view(np.uint8))
+    assert np.array_equal(h16(C.unpack_dequant(*a, bits, group, 128)),
+                          h16(C.unpack_dequant_scalar(*b, bits, group, 128)))
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_dequant_arbitrary_scale_zero(bits):
+    """Dequantisation of arbitrary codes under arbitrary finite scale/zero bit
+    patterns (subnormals, ties, saturation): numpy == C SIMD == C scalar."""
+    rng = np.random.default_rng(100 + bits)
+    rows, group = 20000, 32
+    codes = rng.integers(0, 256, size=(rows, 128 * bits // 8), dtype=np.uint8)
+    def meta():
+        m = rng.integers(0, 0x10000, size=(rows, 128 // group), dtype=np.uint16).view(np.float16)
+        m = np.where(np.isfinite(m), m, np.float16(1))
+        return m
+    s, z = np.abs(meta()), meta()
+    a = O.unpack_dequant(codes, s, z, bits, group, 128)
+    b = C.unpack_dequant(codes, s, z, bits, group, 128)
+    c = C.unpack_dequant_scalar(codes, s, z, bits, group, 128)
+    assert np.array_equal(h16(a), h16(b))
+    assert np.array_equal(h16(a), h16(c))
+
+
 def test_pack_unpack_roundtrip():
     rng = np.random.default_rng(5)
     for bits in (2, 4, 8):
