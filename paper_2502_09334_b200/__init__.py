@@ -11,7 +11,10 @@ from .costs import (  # noqa: F401
     KvPrecision,
     bottleneck_link,
     kv_comm_cost,
+    HandoffTable,
+    install_measurements,
     kv_volume,
+    measured_cost_fn,
     measured_kv_comm_cost,
 )
 from .errors import NoPath, PlanningError  # noqa: F401

@@ -110,31 +110,104 @@ def kv_comm_cost(prefill_gpu_ids, decode_gpu_ids, b: int, s: int, model, prec, c
     return alpha + float(kv_volume(b, s, model, prec, params)) / beta
 
 
-def measured_kv_comm_cost(table: Callable[[int, int, int], float] | dict,
-                          fallback: Callable | None = kv_comm_cost) -> Callable:
-    """A ``kv_comm_cost``-signature function backed by measured hand-off times.
+class HandoffTable:
+    """Measured hand-off times of this data path on one link class.
 
-    ``table`` maps (bits, fp16_bytes) -> seconds (a callable, or a dict of
-    bits -> (alpha_s, bytes_per_s) fitted from ``bench.py`` / ``tools``
-    measurements).  The returned function keeps the reference's argument
-    checks and NoPath behaviour (it still resolves the bottleneck link), and
-    can be installed as ``hetplan.simulate.kv_comm_cost``.
-    """
+    ``entries`` maps bits -> (alpha_s, fp16_bytes_per_s): one hand-off of V
+    fp16-equivalent bytes takes ``alpha + V / rate`` (the bench's per-pair
+    two-point calibration, ``bench.py`` N>1 ``calibration``; one entry per
+    bit-width the reference plans with, ``cli.py:278``).  ``link_beta`` is the
+    cluster beta (bytes/s) of the link the table was measured on, kept as
+    provenance.  The table prices the kernels + transfer; the link the planner
+    resolves still bounds the result (``measured_kv_comm_cost``)."""
 
-    def _cost(prefill_gpu_ids, decode_gpu_ids, b, s, model, prec, cluster,
-              params: CostParams = CostParams()) -> float:
-        if b < 1 or s < 1:
-            raise ValueError("batch size and sequence length must be >= 1")
-        bottleneck_link(prefill_gpu_ids, decode_gpu_ids, cluster)  # NoPath semantics
-        bits = _bits(prec)
-        fp16_bytes = int(kv_volume(b, s, model, KvPrecision(16), params))
-        if callable(table):
-            return float(table(bits, fp16_bytes, len(tuple(prefill_gpu_ids))))
-        if bits in table:
-            alpha, rate = table[bits]
-            return float(alpha) + fp16_bytes / float(rate)
+    def __init__(self, entries: dict, link_beta: float | None = None, source: str = ""):
+        self.entries = {}
+        for bits, (alpha, rate) in entries.items():
+            bits = _bits(int(bits))
+            if not (alpha >= 0 and rate > 0):
+                raise ValueError(f"bad measurement for {bits}-bit: alpha={alpha}, rate={rate}")
+            self.entries[bits] = (float(alpha), float(rate))
+        self.link_beta = link_beta
+        self.source = source
+
+    def time(self, bits: int, fp16_bytes: int) -> float | None:
+        e = self.entries.get(bits)
+        return None if e is None else e[0] + fp16_bytes / e[1]
+
+    @classmethod
+    def from_json(cls, path: str) -> "HandoffTable":
+        """``{"entries": {"4": {"alpha_s": .., "fp16_bytes_per_s": ..}, ..},
+        "link_beta": .., "source": ..}`` (tools/handoff_table.py writes it)."""
+        import json
+        with open(path) as f:
+            d = json.load(f)
+        ent = {int(k): (v["alpha_s"], v["fp16_bytes_per_s"]) for k, v in d["entries"].items()}
+        return cls(ent, d.get("link_beta"), d.get("source", path))
+
+
+_ACTIVE_TABLE: HandoffTable | None = None
+
+
+def install_measurements(table) -> HandoffTable | None:
+    """Make ``table`` (a HandoffTable, a dict bits -> (alpha_s, rate) or a
+    path to its JSON; None to clear) the one ``measured_kv_comm_cost`` reads.
+    Returns the previous table."""
+    global _ACTIVE_TABLE
+    prev = _ACTIVE_TABLE
+    if table is None or isinstance(table, HandoffTable):
+        _ACTIVE_TABLE = table
+    elif isinstance(table, str):
+        _ACTIVE_TABLE = HandoffTable.from_json(table)
+    else:
+        _ACTIVE_TABLE = HandoffTable(table)
+    return prev
+
+
+def _measured(table, prefill_gpu_ids, decode_gpu_ids, b, s, model, prec, cluster, params,
+              fallback):
+    analytic = kv_comm_cost(prefill_gpu_ids, decode_gpu_ids, b, s, model, prec, cluster, params)
+    bits = _bits(prec)
+    t = table.time(bits, int(kv_volume(b, s, model, KvPrecision(16), params))) if table else None
+    if t is None:
         if fallback is None:
             raise ValueError(f"no measurement for {bits}-bit hand-off")
         return fallback(prefill_gpu_ids, decode_gpu_ids, b, s, model, prec, cluster, params)
+    # the measured kernels + NVLink path, but never faster than the link the
+    # planner resolved: a slower (e.g. cross-node) bottleneck keeps its model
+    return max(t, analytic)
+
+
+def measured_kv_comm_cost(prefill_gpu_ids, decode_gpu_ids, b: int, s: int, model, prec, cluster,
+                          params: CostParams = CostParams()) -> float:
+    """``kv_comm_cost``'s signature and contract (costs.py:83-103), priced by
+    the installed measured table (``install_measurements``):
+
+        max(alpha_m + V16 / rate_m[bits],  alpha + V(bits) / beta)
+
+    where the second term is the reference's own model over the bottleneck
+    link: the measured hand-off (quantise + NVLink + dequantise into the paged
+    cache, metadata included) where it is the slower one -- the NVLink class
+    it was measured on -- and the link model where the planner's link is
+    slower than the measured path (a cross-node pair).  ``ValueError`` for
+    bad bits / b / s and ``NoPath`` as the reference; a bit-width the table
+    lacks (or no table) falls back to the analytic model.  Install it with
+    ``hetplan.simulate.kv_comm_cost = hetplan.orchestrate.kv_comm_cost =
+    measured_kv_comm_cost`` (INTEGRATION.md)."""
+    return _measured(_ACTIVE_TABLE, prefill_gpu_ids, decode_gpu_ids, b, s, model, prec, cluster,
+                     params, kv_comm_cost)
+
+
+def measured_cost_fn(table, fallback: Callable | None = kv_comm_cost) -> Callable:
+    """A ``kv_comm_cost``-signature closure over its own ``table`` (a
+    HandoffTable or dict bits -> (alpha_s, fp16_bytes_per_s)); same pricing as
+    ``measured_kv_comm_cost`` without touching the installed table.
+    ``fallback=None`` raises ValueError for an unmeasured bit-width."""
+    tab = table if isinstance(table, HandoffTable) else HandoffTable(table)
+
+    def _cost(prefill_gpu_ids, decode_gpu_ids, b, s, model, prec, cluster,
+              params: CostParams = CostParams()) -> float:
+        return _measured(tab, prefill_gpu_ids, decode_gpu_ids, b, s, model, prec, cluster, params,
+                         fallback)
 
     return _cost
