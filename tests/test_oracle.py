@@ -232,3 +232,27 @@ def test_kivi_oracle_layout_and_accuracy():
     c, s, z = O.quant_pack(kv[:, 0].reshape(-1, 128), 4, 32)
     e_tok = np.abs(O.unpack_dequant(c, s, z, 4, 32, 128).astype(np.float64) - kv[:, 0].reshape(-1, 128)).mean()
     assert e_kivi < 0.75 * e_tok  # per-channel K isolates the outlier channels
+
+
+def test_oracle_volume_model_matches_reference_golden():
+    """The oracle's restatement of the reference's volume/time model
+    (kv_volume_bytes, kv_comm_time; costs.py:83-103) reproduces the
+    reference's own outputs bit for bit (tests/golden/kv_volume.json), and its
+    packed_layout byte counts equal the 4-bit code volume the reference charges."""
+    import json
+    import os
+    from fractions import Fraction
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "kv_volume.json")))
+    for c in gold["cases"]:
+        v = O.kv_volume_bytes(c["b"], c["s"], c["n_layers"], c["hidden_size"], c["bits"],
+                              c["kv_layer_factor"])
+        assert v == Fraction(c["volume"]), c["name"]
+        assert float(O.kv_comm_time(v, c["alpha"], c["beta"])).hex() == c["ref_time_hex"]
+        if c["bits"] in (8, 4, 2) and c["kv_layer_factor"] and c["hidden_size"] % 128 == 0:
+            rows = c["n_layers"] * 2 * c["b"] * c["s"] * (c["hidden_size"] // 128)
+            codes, scale, zero = O.packed_layout(rows, 128, 128, c["bits"])
+            assert codes == v and scale == zero == rows * 2
+    with pytest.raises(ValueError):
+        O.kv_volume_bytes(1, 1, 1, 1, 3)
+    with pytest.raises(ValueError):
+        O.kv_volume_bytes(0, 1, 1, 1, 4)
