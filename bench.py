@@ -709,6 +709,8 @@ def main():
                     help="pull: queue slots per pair in the prefill GPU's HBM")
     ap.add_argument("--no-pdl", action="store_true",
                     help="N>1: no programmatic dependent launch between consecutive pulls")
+    ap.add_argument("--tokens", type=int, default=None,
+                    help="override the workload's token count (batch 1 x TOKENS) for sweeps")
     ap.add_argument("--gate-recv", action="store_true",
                     help="N>1: hold each pull in the GPU front-end until chunk 0 is published")
     args = ap.parse_args()
@@ -717,6 +719,11 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.tokens:
+        base = args.workload or ("cfg2_7b_2048x8" if world == 1 else default_pair_workload(world))
+        L, H, D, _, _ = WORKLOADS[base]
+        args.workload = f"{base}@{args.tokens}x1"
+        WORKLOADS[args.workload] = (L, H, D, 1, args.tokens)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

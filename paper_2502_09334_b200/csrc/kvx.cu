@@ -190,6 +190,11 @@ cudaError_t make_items(const kvx::Geo& g, kvx::ItemGeo& ig) {
   return cudaSuccess;
 }
 
+#ifdef KVX_TRACE
+// trace builds: the epoch of the pair hand-off being launched on this thread
+thread_local uint32_t g_trace_epoch = 0;
+#endif
+
 // Doorbell request for kvx_quant_pack_signal (null peer_flags = plain K1).
 struct SignalReq {
   uint32_t* counters = nullptr;
@@ -217,6 +222,9 @@ cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero
   sig.free_flag = rq.free_flag;
   sig.free_value = rq.free_value;
   sig.ctl = rq.ctl;
+#ifdef KVX_TRACE
+  sig.trace_id = g_trace_epoch;
+#endif
   if (rq.peer_flags) {
     const int64_t per_layer = ig.n_items / (rq.n_layers > 0 ? rq.n_layers : 1);
     const int64_t ipc = per_layer * rq.layers_per_chunk;
@@ -293,6 +301,9 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   bg.done_counter = done.done_counter;
   bg.peer_free = done.peer_free;
   bg.ctl = ctl;
+#ifdef KVX_TRACE
+  bg.trace_id = g_trace_epoch;
+#endif
   bg.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
   bg.code_row_bytes = int(int64_t(g.row_elems) * BITS / 8);
   bg.meta_row_bytes = int(int64_t(g.row_elems) / G * 2);
@@ -1168,6 +1179,9 @@ int kvx_pair_send(void* pair, uint64_t epoch, const void* k_src, const void* v_s
   char* base = p->payload + int64_t(h) * p->slot_bytes;
   uint32_t* free_flag = p->local_flags + kFlagFreeBase + h;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+#ifdef KVX_TRACE
+  g_trace_epoch = uint32_t(epoch);
+#endif
   if ((flags & KVX_PAIR_GATE) && v > 1) {
     // hold the prefill side in the GPU front-end (no SMs held) until the
     // decode side has consumed the slot's previous use; K1 re-checks in-kernel
@@ -1203,6 +1217,9 @@ int kvx_pair_recv(void* pair, uint64_t epoch, void* k_cache, void* v_cache,
   const int64_t ls = pair_layer_stride(p, n_tokens, &so, &zo);
   const char* base = p->payload + int64_t(h) * p->slot_bytes;
   uint32_t* ready = p->local_flags + kFlagReadyBase + h * 64;
+#ifdef KVX_TRACE
+  g_trace_epoch = uint32_t(epoch);
+#endif
   if (flags & KVX_PAIR_GATE) {
     // launch only once the first chunk is published: a pull never sits on
     // the SMs waiting for an idle prefill side

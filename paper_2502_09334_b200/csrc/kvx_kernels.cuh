@@ -503,6 +503,9 @@ struct SignalGeo {
   const uint32_t* free_flag;
   uint32_t free_value;
   Ctl* ctl;  // nullable
+#ifdef KVX_TRACE
+  uint32_t trace_id;  // trace builds: the hand-off's epoch (row of the timeline ring)
+#endif
 };
 
 // Warps w in [lo, hi) that own at least one item i in [a, b) (item i -> warp i % W).
@@ -551,7 +554,7 @@ __device__ __forceinline__ void chunk_arrive(const SignalGeo& sig, uint32_t* cta
                      "r"(ready_value)
                      : "memory");
 #ifdef KVX_TRACE
-        if ((c + 1) * sig.items_per_chunk >= n_items) KVX_TRACE_STAMP(0, g_trace_n[0], 2);
+        if ((c + 1) * sig.items_per_chunk >= n_items) KVX_TRACE_STAMP(0, sig.trace_id, 2);
 #endif
       }
     }
@@ -573,7 +576,7 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
   __shared__ uint32_t cta_cnt[kMaxSignalChunks];
   __shared__ uint32_t s_go;
 #ifdef KVX_TRACE
-  const uint32_t trace_id = g_trace_n[0];
+  const uint32_t trace_id = sig.trace_id;
   if (sig.peer_flags && blockIdx.x == 0 && threadIdx.x == 0) KVX_TRACE_STAMP(0, trace_id, 0);
 #endif
   if (sig.peer_flags) {
@@ -630,7 +633,7 @@ k1_done:
     if (threadIdx.x == 0 && atomicAdd(sig.counters + kMaxSignalChunks, 1u) == gridDim.x - 1) {
       sig.counters[kMaxSignalChunks] = 0u;
       KVX_TRACE_STAMP(0, trace_id, 3);
-      g_trace_n[0] = trace_id + 1;
+      atomicMax(&g_trace_n[0], trace_id + 1);
     }
   }
 #endif
@@ -860,6 +863,9 @@ struct BulkGeo {
   uint32_t* done_counter;
   uint32_t* peer_free;
   Ctl* ctl;              // nullable
+#ifdef KVX_TRACE
+  uint32_t trace_id;     // trace builds: the hand-off's epoch
+#endif
   int layers_per_chunk;
   int rows_per_span;     // R
   int spans_per_layer;   // ceil(2T / R)
@@ -942,10 +948,12 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
   // PDL: the stream's next kernel (the next hand-off's pull) may be scheduled
   // now; its producer starts streaming its own queue slot while this grid
   // drains, and its consumers wait (pdl_wait) until this grid has completed
+#ifndef KVX_PDL_LATE
   pdl_launch_dependents();
+#endif
   const int64_t two_t = int64_t(g.planes) * g.n_tokens;  // payload rows per layer
 #ifdef KVX_TRACE
-  const uint32_t trace_id = g_trace_n[1];
+  const uint32_t trace_id = bg.trace_id;
   if (bg.done_counter && blockIdx.x == 0 && threadIdx.x == 0) KVX_TRACE_STAMP(1, trace_id, 0);
 #endif
   if (warp == CONSUMERS) {  // ---- producer: one elected thread
@@ -989,6 +997,10 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
         bulk_g2s(mbuf + bg.rows_per_span * bg.meta_row_bytes, zbase + r0 * bg.meta_row_bytes, mb,
                  &full[st]);
       }
+#ifdef KVX_PDL_LATE
+      // every span of this CTA is requested: the next pull may be scheduled
+      pdl_launch_dependents();
+#endif
     }
   } else {
   // ---- consumers: the slot mapping and the cache are stream-ordered inputs
@@ -1077,7 +1089,7 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
                        : "memory");
 #ifdef KVX_TRACE
         KVX_TRACE_STAMP(1, trace_id, 3);
-        g_trace_n[1] = trace_id + 1;
+        atomicMax(&g_trace_n[1], trace_id + 1);
 #endif
       }
     }

@@ -434,6 +434,17 @@ class PairChannel:
         return (self._pair is not None and self.spec.mode == "pull" and
                 self.spec.device_doorbells and pull_supported(lay))
 
+    def _fused_n(self, n_tokens: int) -> bool:
+        """``_fused`` by token count, memoised: the per-hand-off host path of
+        the fused pull does no layout arithmetic or library query."""
+        memo = self.__dict__.setdefault("_fused_memo", {})
+        f = memo.get(n_tokens)
+        if f is None:
+            if len(memo) >= 4096:
+                memo.clear()
+            f = memo[n_tokens] = self._fused(self.spec.layout(n_tokens))
+        return f
+
     def _pull_chunks(self, lay):
         """Chunk plan of a pull hand-off; identical on both ends (it depends
         on the spec and the token count only)."""
@@ -489,9 +500,8 @@ class PairChannel:
         if self.spec.format == "kivi":
             self.epoch += 1
             return self._send_kivi(src, n_tokens, seqlens, self.epoch)
-        lay = self.spec.layout(n_tokens)
         e = self.epoch + 1
-        if stage_in is None and self._fused(lay):
+        if stage_in is None and self._fused_n(n_tokens):
             # the default path: ONE native launch on the caller's stream
             cur = torch.cuda.current_stream(self.device)
             ev = _kernel_events(timing, cur, "k1")
@@ -504,6 +514,7 @@ class PairChannel:
             self.epoch = e
             return
         self.epoch = e
+        lay = self.spec.layout(n_tokens)
         mode = self.spec.mode
         s, cs = self.stream, self.cstream
         cur = torch.cuda.current_stream(self.device)
@@ -638,11 +649,9 @@ class PairChannel:
         if self.spec.format == "kivi":
             self.epoch += 1
             return self._recv_kivi(dst, n_tokens, seqlens, self.epoch)
-        lay = self.spec.layout(n_tokens)
         e = self.epoch + 1
         mode = self.spec.mode
-        if (stage_out is None and self._pair is not None and mode == "pull"
-                and pull_supported(lay)):
+        if stage_out is None and self._fused_n(n_tokens):
             # the default path: ONE native K3-bulk launch on the caller's stream
             cur = torch.cuda.current_stream(self.device)
             ev = _kernel_events(timing, cur, "k3")
@@ -655,6 +664,7 @@ class PairChannel:
             self.epoch = e
             return
         self.epoch = e
+        lay = self.spec.layout(n_tokens)
         s, cs = self.stream, self.cstream
         cur = torch.cuda.current_stream(self.device)
         if mode in PULL_MODES:

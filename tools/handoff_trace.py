@@ -38,14 +38,19 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tokens", type=int, default=16)
     ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--queue-depth", type=int, default=2)
+    ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--layers", type=int, default=80)
+    ap.add_argument("--heads", type=int, default=8)
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
     dist.init_process_group("nccl", device_id=dev)
     ctrl = dist.new_group(backend="gloo")
-    L, H, D, T = 80, 8, 128, a.tokens
-    ch = PairChannel(ChannelSpec(L, T, H, D, 4, 128, 8, "pull"), rank, 2, control_group=ctrl)
+    L, H, D, T = a.layers, a.heads, 128, a.tokens
+    ch = PairChannel(ChannelSpec(L, T, H, D, 4, 128, 8, "pull", queue_depth=a.queue_depth,
+                                 pdl=not a.no_pdl), rank, 2, control_group=ctrl)
     if ch.role == "prefill":
         kv = torch.randn((L, 2, T, H, D), device=dev).half()
         planes = KVPlanes.dense(kv)
@@ -61,8 +66,9 @@ def main():
     tr = read_trace(0 if ch.role == "prefill" else 1)
     allt = exchange(tr.tolist(), ctrl)
     if rank == 0:
-        k1 = np.array(allt[0], np.int64)  # start, free seen, rung, out    (P clock)
-        k3 = np.array(allt[1], np.int64)  # start, ready seen, release, released (D clock)
+        # rows are indexed by the hand-off's epoch (1..steps; row 0 unused)
+        k1 = np.array(allt[0], np.int64)[1:]  # start, free seen, rung, out    (P clock)
+        k3 = np.array(allt[1], np.int64)[1:]  # start, ready seen, release, released (D clock)
         n = min(len(k1), len(k3))
         k1, k3 = k1[:n], k3[:n]
         s = slice(n // 2, n)  # steady state
@@ -83,7 +89,16 @@ def main():
             "k3_release_store_us": med(k3[s, 3] - k3[s, 2]),
             "k3_gap_prev_out_to_start_us": med(k3[n // 2 + 1:, 0] - k3[n // 2:-1, 3]),
             "k3_start_minus_k1_rung_us": med(k3[s, 0] - d - k1[s, 2]),
+            "queue_depth": a.queue_depth, "pdl": not a.no_pdl, "layers": L, "heads": H,
         }
+        # three consecutive steady-state hand-offs on one (prefill) clock, us
+        # relative to the first K1's start
+        i0 = n // 2
+        t0 = k1[i0, 0]
+        out["timeline_us"] = [
+            {"epoch": int(i0 + 1 + j),
+             "k1": [round((x - t0) / 1e3, 2) for x in k1[i0 + j]],
+             "k3": [round((x - d - t0) / 1e3, 2) for x in k3[i0 + j]]} for j in range(3)]
         print(json.dumps(out), flush=True)
     dist.barrier()
     ch.close()
