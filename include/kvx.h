@@ -203,15 +203,40 @@ int kvx_dequant_scatter_paged_kivi(const void* payload, int64_t payload_layer_st
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
                                    int group, int bits, void* k_cache, void* v_cache,
                                    int64_t dst_layer_stride, void* stream);
-/* Same contract, for a payload read over NVLink: the per-channel K groups and
+/*
+ * Fused kivi prefill side: kvx_quant_pack_kivi over a whole hand-off with
+ * device doorbells (no per-chunk launches or stream memops).  The K
+ * (per-channel) quantiser sets peer_ready_flags[c] = ready_value as soon as
+ * chunk c (layers_per_chunk layers; at most KVX_KIVI_V_FLAGS chunks) of K
+ * is in the payload; the residual rows follow; the V quantiser then sets
+ * peer_ready_flags[KVX_KIVI_V_FLAGS + c] per chunk -- a V doorbell publishes
+ * the whole chunk (K, residual and V).  peer_ready_flags may be IPC/peer
+ * mapped (st.release.sys).  counters: 2*64 u32 of scratch on this GPU, zero
+ * before the first call (left zero).  free_flag (nullable): the launches are
+ * held in the GPU front-end (stream memop) until *free_flag >= free_value
+ * (the queue slot's previous use consumed).  ctl as for kvx_quant_pack_signal.
+ */
+#define KVX_KIVI_V_FLAGS 32
+int kvx_quant_pack_kivi_signal(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                               int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                               int group, int bits, const int64_t* group_starts, int64_t n_groups,
+                               const int64_t* residual_tokens, int64_t n_residual, void* payload,
+                               int64_t payload_layer_stride, const int64_t* seg_offsets,
+                               void* counters, void* peer_ready_flags, int layers_per_chunk,
+                               uint32_t ready_value, const void* free_flag, uint32_t free_value,
+                               void* ctl, void* stream);
+/* Same contract as kvx_dequant_scatter_paged_kivi, for a payload read over
+ * NVLink: the per-channel K groups and
  * the per-token V rows are staged into shared memory with cp.async.bulk
  * (TMA) before they are dequantised -- the kivi format's pull transport.
  * Shapes that cannot be bulk-staged fall back to the per-lane kernels.
  * ready_flags (nullable, this GPU's memory): the kernels wait in-kernel, per
- * chunk of layers_per_chunk layers, until ready_flags[chunk] >= ready_value,
- * so ONE call consumes a whole hand-off while the prefill side is still
- * publishing it; the caller releases the queue slot after the call (stream
- * order).  With flags, shapes that cannot be bulk-staged return
+ * chunk of layers_per_chunk layers, until the chunk's doorbell is >=
+ * ready_value -- K groups on ready_flags[chunk], V rows (and, after them,
+ * the residual rows) on ready_flags[KVX_KIVI_V_FLAGS + chunk], the layout
+ * kvx_quant_pack_kivi_signal rings -- so ONE call consumes a whole hand-off
+ * while the prefill side is still publishing it; the caller releases the
+ * queue slot after the call (stream order).  With flags, shapes that cannot be bulk-staged return
  * KVX_ERR_UNSUPPORTED.  ctl as for kvx_quant_pack_signal.
  * 8-bit: seg_offsets[4] (V codes) and payload_layer_stride must be 32-byte
  * multiples (32-byte vector accesses). */

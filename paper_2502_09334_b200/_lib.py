@@ -42,6 +42,8 @@ SIGNATURES = {
     "kvx_pull_supported": [_I64, _I, _I, _I, _I],
     "kvx_quant_pack_kivi": [_P, _P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _I64, _P,
                             _I64, _P, _P],
+    "kvx_quant_pack_kivi_signal": [_P, _P, _I64, _I64, _I64, _I, _I, _I, _I, _P, _I64, _P, _I64,
+                                   _P, _I64, _P, _P, _P, _I, _U32, _P, _U32, _P, _P],
     "kvx_dequant_scatter_paged_kivi": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _I, _I,
                                        _I, _I, _P, _P, _I64, _P],
     "kvx_pull_dequant_scatter_paged_kivi": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _I,
@@ -73,6 +75,7 @@ SIGNATURES = {
 }
 
 # constants of include/kvx.h
+KVX_KIVI_V_FLAGS = 32
 KVX_PULL_PDL = 1
 KVX_ROLE_PREFILL, KVX_ROLE_DECODE = 0, 1
 KVX_PAIR_GATE, KVX_PAIR_PDL = 1, 2

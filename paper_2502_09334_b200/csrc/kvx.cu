@@ -432,13 +432,20 @@ int kivi_check(int head_dim, int group, int bits) {
 }
 
 template <int BITS, int G>
-cudaError_t launch_kchan_quant(const kvx::KchanGeo& kg, cudaStream_t s) {
+cudaError_t launch_kchan_quant(const kvx::KchanGeo& kg, cudaStream_t s, uint32_t* counters = nullptr,
+                               uint32_t* peer_flags = nullptr, int layers_per_chunk = 1,
+                               uint32_t ready_value = 0) {
   constexpr int cta_ch = 4 * (32 / (G / 16)) * 8;  // matches quant_pack_kchan_kernel
   const int cblocks = (kg.row_elems + cta_ch - 1) / cta_ch;
   const int64_t items = kg.n_layers * kg.n_groups * cblocks;
   int64_t grid = int64_t(sm_count(current_device())) * 8;
   if (grid > items) grid = items;
-  kvx::quant_pack_kchan_kernel<BITS, G><<<unsigned(grid), 128, 0, s>>>(kg);
+  kvx::KchanSignal sig;
+  sig.counters = counters;
+  sig.peer_flags = peer_flags;
+  sig.items_per_chunk = kg.n_groups * cblocks * int64_t(layers_per_chunk > 0 ? layers_per_chunk : 1);
+  sig.ready_value = ready_value;
+  kvx::quant_pack_kchan_kernel<BITS, G><<<unsigned(grid), 128, 0, s>>>(kg, sig);
   return cudaGetLastError();
 }
 
@@ -700,11 +707,20 @@ int kvx_pull_supported(int64_t n_tokens, int n_heads, int head_dim, int group, i
 
 // ---- "kivi" format: per-channel K groups + fp16 residual window, V per token --
 
-int kvx_quant_pack_kivi(const void* k_src, const void* v_src, int64_t src_layer_stride,
-                        int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim, int group,
-                        int bits, const int64_t* group_starts, int64_t n_groups,
-                        const int64_t* residual_tokens, int64_t n_residual, void* payload,
-                        int64_t payload_layer_stride, const int64_t* seg_offsets, void* stream) {
+struct KiviSignal {  // fused kivi prefill: device doorbells per layer chunk
+  uint32_t* counters = nullptr;    // [2][kMaxSignalChunks] (K, V)
+  uint32_t* peer_flags = nullptr;  // ready row: K chunks at [c], V chunks at [KVX_KIVI_V_FLAGS + c]
+  int layers_per_chunk = 1;
+  uint32_t ready_value = 0;
+  kvx::Ctl* ctl = nullptr;
+};
+
+static int kivi_quant(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                      int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim, int group,
+                      int bits, const int64_t* group_starts, int64_t n_groups,
+                      const int64_t* residual_tokens, int64_t n_residual, void* payload,
+                      int64_t payload_layer_stride, const int64_t* seg_offsets, void* stream,
+                      const KiviSignal& ks = KiviSignal()) {
   int rc = kivi_check(head_dim, group, bits);
   if (rc) return rc;
   if (n_layers < 0 || n_tokens < 0 || n_heads <= 0 || n_groups < 0 || n_residual < 0 ||
@@ -718,7 +734,7 @@ int kvx_quant_pack_kivi(const void* k_src, const void* v_src, int64_t src_layer_
   char* base = static_cast<char*>(payload);
   const int row_elems = n_heads * head_dim;
   cudaError_t e = cudaSuccess;
-  if (n_groups) {
+  if (n_groups) {  // K per channel first: the decode side starts pulling it first
     kvx::KchanGeo kg;
     kg.k_plane = static_cast<const char*>(k_src);
     kg.layer_stride_b = src_layer_stride * 2;
@@ -730,9 +746,25 @@ int kvx_quant_pack_kivi(const void* k_src, const void* v_src, int64_t src_layer_
     kg.scale = base + seg_offsets[1];
     kg.zero = base + seg_offsets[2];
     kg.payload_ls = payload_layer_stride;
-    if (bits == 4) e = group == 32 ? launch_kchan_quant<4, 32>(kg, s) : launch_kchan_quant<4, 64>(kg, s);
-    else e = group == 32 ? launch_kchan_quant<8, 32>(kg, s) : launch_kchan_quant<8, 64>(kg, s);
+    uint32_t* cnt = ks.counters;
+    uint32_t* fl = ks.peer_flags;
+    const int lpc = ks.layers_per_chunk;
+    const uint32_t rv = ks.ready_value;
+    if (bits == 4)
+      e = group == 32 ? launch_kchan_quant<4, 32>(kg, s, cnt, fl, lpc, rv)
+                      : launch_kchan_quant<4, 64>(kg, s, cnt, fl, lpc, rv);
+    else
+      e = group == 32 ? launch_kchan_quant<8, 32>(kg, s, cnt, fl, lpc, rv)
+                      : launch_kchan_quant<8, 64>(kg, s, cnt, fl, lpc, rv);
     if (e != cudaSuccess) return e;
+  } else if (ks.peer_flags) {
+    // no per-channel groups (every request shorter than a group): the K
+    // doorbells carry nothing, ring them in stream order
+    const int nc = int((n_layers + ks.layers_per_chunk - 1) / ks.layers_per_chunk);
+    for (int c = 0; c < nc; ++c) {
+      rc = kvx_stream_signal(ks.peer_flags + c, ks.ready_value, stream);
+      if (rc) return rc;
+    }
   }
   if (n_residual) {  // residual window: fp16 rows gathered into the payload
     kvx::Geo g;
@@ -743,17 +775,65 @@ int kvx_quant_pack_kivi(const void* k_src, const void* v_src, int64_t src_layer_
     k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(g, reinterpret_cast<uint8_t*>(base + seg_offsets[3]));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  {  // V per token
+  {  // V per token (its doorbells, rung after the K and residual kernels in
+     // stream order, publish the whole chunk)
     kvx::Geo g;
     rc = make_geo(g, v_src, v_src, src_layer_stride, nullptr, n_layers, n_tokens, n_heads, head_dim,
                   group, bits, payload_layer_stride, 1, 1);
     if (rc) return rc;
+    SignalReq rq;
+    if (ks.peer_flags) {
+      rq.counters = ks.counters + kvx::kMaxSignalChunks;
+      rq.peer_flags = ks.peer_flags + KVX_KIVI_V_FLAGS;
+      rq.ready_value = ks.ready_value;
+      rq.ctl = ks.ctl;
+      rq.layers_per_chunk = ks.layers_per_chunk;
+      rq.n_layers = n_layers;
+    }
     e = bits == 4 ? dispatch_quant<4>(group, g, base + seg_offsets[4], base + seg_offsets[5],
-                                      base + seg_offsets[6], s)
+                                      base + seg_offsets[6], s, rq)
                   : dispatch_quant<8>(group, g, base + seg_offsets[4], base + seg_offsets[5],
-                                      base + seg_offsets[6], s);
+                                      base + seg_offsets[6], s, rq);
   }
   return e;
+}
+
+int kvx_quant_pack_kivi(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                        int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim, int group,
+                        int bits, const int64_t* group_starts, int64_t n_groups,
+                        const int64_t* residual_tokens, int64_t n_residual, void* payload,
+                        int64_t payload_layer_stride, const int64_t* seg_offsets, void* stream) {
+  return kivi_quant(k_src, v_src, src_layer_stride, n_layers, n_tokens, n_heads, head_dim, group,
+                    bits, group_starts, n_groups, residual_tokens, n_residual, payload,
+                    payload_layer_stride, seg_offsets, stream);
+}
+
+int kvx_quant_pack_kivi_signal(const void* k_src, const void* v_src, int64_t src_layer_stride,
+                               int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
+                               int group, int bits, const int64_t* group_starts, int64_t n_groups,
+                               const int64_t* residual_tokens, int64_t n_residual, void* payload,
+                               int64_t payload_layer_stride, const int64_t* seg_offsets,
+                               void* counters, void* peer_ready_flags, int layers_per_chunk,
+                               uint32_t ready_value, const void* free_flag, uint32_t free_value,
+                               void* ctl, void* stream) {
+  if (!counters || !peer_ready_flags || layers_per_chunk < 1 || !aligned(counters, 4) ||
+      !aligned(peer_ready_flags, 4) || !aligned(free_flag, 4) || !aligned(ctl, 8))
+    return KVX_ERR_INVALID_ARG;
+  if (n_layers > 0 && (n_layers + layers_per_chunk - 1) / layers_per_chunk > KVX_KIVI_V_FLAGS)
+    return KVX_ERR_INVALID_ARG;
+  if (free_flag) {  // hold the launch in the GPU front-end until the queue slot is free
+    int rc = kvx_stream_wait(free_flag, free_value, stream);
+    if (rc) return rc;
+  }
+  KiviSignal ks;
+  ks.counters = static_cast<uint32_t*>(counters);
+  ks.peer_flags = static_cast<uint32_t*>(peer_ready_flags);
+  ks.layers_per_chunk = layers_per_chunk;
+  ks.ready_value = ready_value;
+  ks.ctl = static_cast<kvx::Ctl*>(ctl);
+  return kivi_quant(k_src, v_src, src_layer_stride, n_layers, n_tokens, n_heads, head_dim, group,
+                    bits, group_starts, n_groups, residual_tokens, n_residual, payload,
+                    payload_layer_stride, seg_offsets, stream, ks);
 }
 
 static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
@@ -824,9 +904,10 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
     bool ok = false;
     if (bulk && aligned(v_cache, 32) && g.plane_row_b % 32 == 0) {
       PullDone pd;  // no in-kernel completion: the caller releases the slot after this call
-      e = bits == 4 ? dispatch_pull<4>(group, g, vc, vs, vz, s, &ok, ready, ready_value,
+      const uint32_t* vready = ready ? ready + KVX_KIVI_V_FLAGS : nullptr;
+      e = bits == 4 ? dispatch_pull<4>(group, g, vc, vs, vz, s, &ok, vready, ready_value,
                                        layers_per_chunk, pd, ctl, false)
-                    : dispatch_pull<8>(group, g, vc, vs, vz, s, &ok, ready, ready_value,
+                    : dispatch_pull<8>(group, g, vc, vs, vz, s, &ok, vready, ready_value,
                                        layers_per_chunk, pd, ctl, false);
       if (e != cudaSuccess) return e;
     }

@@ -945,12 +945,6 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // PDL: the stream's next kernel (the next hand-off's pull) may be scheduled
-  // now; its producer starts streaming its own queue slot while this grid
-  // drains, and its consumers wait (pdl_wait) until this grid has completed
-#ifndef KVX_PDL_LATE
-  pdl_launch_dependents();
-#endif
   const int64_t two_t = int64_t(g.planes) * g.n_tokens;  // payload rows per layer
 #ifdef KVX_TRACE
   const uint32_t trace_id = bg.trace_id;
@@ -997,10 +991,14 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
         bulk_g2s(mbuf + bg.rows_per_span * bg.meta_row_bytes, zbase + r0 * bg.meta_row_bytes, mb,
                  &full[st]);
       }
-#ifdef KVX_PDL_LATE
-      // every span of this CTA is requested: the next pull may be scheduled
+      // PDL: every span of this CTA is requested -- the stream's next kernel
+      // (the next hand-off's pull) may be scheduled now; its producer starts
+      // streaming its own queue slot while this grid's last spans drain, and
+      // its consumers wait (pdl_wait) until this grid has completed.  (At the
+      // top of the kernel instead, every queued pull became resident at once
+      // and hand-offs of 512+ tokens ran 4x slower: 270 vs 68 us at 512
+      // tokens, cfg4 pair 2,637 vs 2,852 GB/s; profiles/r02_pdl_ab.md.)
       pdl_launch_dependents();
-#endif
     }
   } else {
   // ---- consumers: the slot mapping and the cache are stream-ordered inputs

@@ -22,13 +22,24 @@ struct KchanGeo {
   int64_t payload_ls;       // bytes between payload layers
 };
 
+// Per-chunk doorbells of the kchan quantiser (the fused kivi prefill side):
+// items are CTA-strided (item i -> CTA i % gridDim.x) in layer-major order, so
+// the CTAs owning items of chunk c = [a, b) number min(b - a, gridDim.x); the
+// last of them to finish its share rings peer_flags[c] = ready_value.
+struct KchanSignal {
+  uint32_t* counters;       // [kMaxSignalChunks] zero between launches (reset in-kernel)
+  uint32_t* peer_flags;     // decode-side K doorbells (IPC/peer mapped), null = none
+  int64_t items_per_chunk;  // n_groups * cblocks * layers_per_chunk
+  uint32_t ready_value;
+};
+
 // G/16 lanes own 8 adjacent channels x G tokens: each lane loads 16 of the
 // group's tokens with 16-byte loads (a warp reads 256-byte row segments),
 // min/max is reduced over its tokens and then across the lanes with
 // log2(G/16) shuffles, and each lane quantises its own tokens from registers
 // (8 nibbles = one 32-bit store per token at 4-bit).
 template <int BITS, int G>
-__global__ void __launch_bounds__(128) quant_pack_kchan_kernel(KchanGeo g) {
+__global__ void __launch_bounds__(128) quant_pack_kchan_kernel(KchanGeo g, KchanSignal sig) {
   constexpr uint32_t QMAX = (1u << BITS) - 1u;
   constexpr float QMAXF = float(QMAX);
   constexpr int TH = 16;      // tokens per lane (16 x 16 B = 64 registers of data)
@@ -136,6 +147,26 @@ __global__ void __launch_bounds__(128) quant_pack_kchan_kernel(KchanGeo g) {
         } else {
           *reinterpret_cast<uint2*>(dst) =
               make_uint2(bytes4(b[0], b[1], b[2], b[3]), bytes4(b[4], b[5], b[6], b[7]));
+        }
+      }
+    }
+    if (sig.peer_flags) {  // fused kivi prefill: this CTA's share of a chunk is done
+      const int64_t c = item / sig.items_per_chunk;
+      const int64_t nxt = item + gridDim.x;
+      if (nxt >= n_items || nxt / sig.items_per_chunk != c) {
+        __threadfence();  // this thread's payload stores, device-wide
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const int64_t a = c * sig.items_per_chunk;
+          const int64_t b = min(n_items, a + sig.items_per_chunk);
+          const uint32_t owners = uint32_t(min(b - a, int64_t(gridDim.x)));
+          __threadfence();
+          if (atomicAdd(sig.counters + c, 1u) + 1 == owners) {
+            sig.counters[c] = 0u;  // zero again for the next launch
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags + c),
+                         "r"(sig.ready_value)
+                         : "memory");
+          }
         }
       }
     }

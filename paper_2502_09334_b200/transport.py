@@ -767,7 +767,8 @@ class PairChannel:
         if lay.n_tokens != n_tokens:
             raise ValueError("seqlens must sum to n_tokens")
         gs, rt = kivi_groups(seqlens, lay.group)
-        chunks, lpc = pull_chunk_plan(lay.n_layers, lay.fp16_bytes, self.spec.n_chunks,
+        chunks, lpc = pull_chunk_plan(lay.n_layers, lay.fp16_bytes,
+                                      min(self.spec.n_chunks, _lib.KVX_KIVI_V_FLAGS),
                                       self.spec.min_chunk_bytes)
         h, v = self._seq(e)
         return lay, gs, rt, chunks, lpc, h, v
@@ -792,22 +793,28 @@ class PairChannel:
         return hit[0], hit[1]
 
     def _send_kivi(self, src, n_tokens, seqlens, e):
+        """The fused kivi prefill side: K per-channel, residual and V
+        quantisers over the whole hand-off, ringing the K and V chunk
+        doorbells from inside the kernels (kvx_quant_pack_kivi_signal); the
+        launches are held in the GPU front-end until the queue slot is free."""
         lay, gs, rt, chunks, lpc, h, v = self._kivi_common(n_tokens, seqlens, e)
         s, cur = self.stream, torch.cuda.current_stream(self.device)
         s.wait_stream(cur)
         gs_d, rt_d = self._kivi_index(gs, rt, s)
         base = self.k1_target + self._half(e)
         offs = (ctypes.c_int64 * 7)(*lay.offsets)
-        if v > 1:
-            wait(self._pfree(self.flags.ptr, h), v - 1, s)
-        for c, (l0, l1) in enumerate(chunks):
-            k, vv = src.ptrs(l0)
-            _lib.call("kvx_quant_pack_kivi", k, vv, src.layer_stride, l1 - l0, n_tokens,
-                      lay.n_heads, lay.head_dim, lay.group, lay.bits,
-                      gs_d.data_ptr() if len(gs) else None, len(gs),
-                      rt_d.data_ptr() if len(rt) else None, len(rt),
-                      base + l0 * lay.layer_stride, lay.layer_stride, offs, _stream_ptr(s))
-            signal(self._pready(self.peer_flags, h, c), v, s)
+        if getattr(self, "_kivi_cnt", None) is None:  # K and V chunk arrivals per slot
+            self._kivi_cnt = torch.zeros((PULL_MAX_QUEUE, 2 * PULL_MAX_CHUNKS), dtype=torch.int32,
+                                         device=self.device)
+        k, vv = src.ptrs(0)
+        _lib.call("kvx_quant_pack_kivi_signal", k, vv, src.layer_stride, lay.n_layers, n_tokens,
+                  lay.n_heads, lay.head_dim, lay.group, lay.bits,
+                  gs_d.data_ptr() if len(gs) else None, len(gs),
+                  rt_d.data_ptr() if len(rt) else None, len(rt),
+                  base, lay.layer_stride, offs, self._kivi_cnt[h].data_ptr(),
+                  self._pready(self.peer_flags, h, 0), lpc, v,
+                  self._pfree(self.flags.ptr, h) if v > 1 else None, v - 1, self.ctl.ptr,
+                  _stream_ptr(s))
         cur.wait_stream(s)
 
     def _recv_kivi(self, dst, n_tokens, seqlens, e):
@@ -835,7 +842,8 @@ class PairChannel:
                       self._pready(self.flags.ptr, h, 0), v, lpc, self.ctl.ptr, _stream_ptr(s))
         else:  # "pull_ldg": per-chunk stream waits, per-lane peer loads
             for c, (l0, l1) in enumerate(chunks):
-                wait(self._pready(self.flags.ptr, h, c), v, s)
+                # the chunk's V doorbell publishes all of it (K, residual, V)
+                wait(self._pready(self.flags.ptr, h, _lib.KVX_KIVI_V_FLAGS + c), v, s)
                 _lib.call("kvx_dequant_scatter_paged_kivi", *args(l0, l1), _stream_ptr(s))
         signal(self._pfree(self.peer_flags, h), v, s)
         rdst.record_stream(s)
