@@ -456,7 +456,8 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
     spec = ChannelSpec(L, T, H, D, args.bits, args.group, n_chunks, mode,
                        format=getattr(args, "format", "default"),
                        queue_depth=getattr(args, "queue_depth", 2),
-                       pdl=not args.no_pdl, gate_recv=args.gate_recv)
+                       pdl=not args.no_pdl, gate_recv=args.gate_recv,
+                       gate_send=not args.no_gate_send)
     ch = PairChannel(spec, rank, world, control_group=ctrl)
     lay = spec.layout(T)
     # per step token counts (fixed workload, or the trace's batches)
@@ -667,7 +668,7 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                    "pairs": pairs,
                    "format": spec.format,
                    "native_pair": ch._pair is not None,
-                   "pdl": spec.pdl, "gate_recv": spec.gate_recv,
+                   "pdl": spec.pdl, "gate_recv": spec.gate_recv, "gate_send": spec.gate_send,
                    "queue_depth": ch.Q,
                    **({"trace_batches_timed": tok[args.warmup:args.warmup + args.steps],
                        "trace": "lengths log-uniform [128, 8192], 1-16 req/batch, <=16384 "
@@ -711,6 +712,8 @@ def main():
                     help="N>1: no programmatic dependent launch between consecutive pulls")
     ap.add_argument("--tokens", type=int, default=None,
                     help="override the workload's token count (batch 1 x TOKENS) for sweeps")
+    ap.add_argument("--no-gate-send", action="store_true",
+                    help="N>1: no front-end slot gate before K1 (it waits in-kernel only)")
     ap.add_argument("--gate-recv", action="store_true",
                     help="N>1: hold each pull in the GPU front-end until chunk 0 is published")
     args = ap.parse_args()

@@ -44,6 +44,7 @@ std::mutex g_cache_mu;
 std::map<std::tuple<int, const void*, int, int>, int> g_occupancy;  // (dev, fn, threads, smem)
 std::map<std::pair<int, const void*>, int> g_smem_attr;            // (dev, fn) -> bytes set
 
+
 int current_device() {
   int dev = 0;
   cudaGetDevice(&dev);

@@ -503,14 +503,21 @@ class PairChannel:
         e = self.epoch + 1
         if stage_in is None and self._fused_n(n_tokens):
             # the default path: ONE native launch on the caller's stream
-            cur = torch.cuda.current_stream(self.device)
-            ev = _kernel_events(timing, cur, "k1")
-            k, v = src.ptrs(0)
-            ph, ho = src.window_args
-            rc = self._pair_send(self._pair, e, k, v, src.layer_stride, src.slots_ptr, n_tokens,
-                                 ph, ho, self._send_flags, cur.cuda_stream)
-            _lib.check(rc, "kvx_pair_send")
-            _kernel_events_end(ev, cur)
+            if timing is None:
+                cs = _raw_stream(self.device.index)
+                ev = None
+            else:
+                cur = torch.cuda.current_stream(self.device)
+                cs, ev = cur.cuda_stream, _kernel_events(timing, cur, "k1")
+            sl = src.slots
+            rc = self._pair_send(self._pair, e, src.k.data_ptr(), src.v.data_ptr(),
+                                 src.layer_stride, sl.data_ptr() if sl is not None else None,
+                                 n_tokens, src.plane_heads or src.n_heads, src.head_offset,
+                                 self._send_flags, cs)
+            if rc:
+                _lib.check(rc, "kvx_pair_send")
+            if ev is not None:
+                _kernel_events_end(ev, cur)
             self.epoch = e
             return
         self.epoch = e
@@ -653,14 +660,20 @@ class PairChannel:
         mode = self.spec.mode
         if stage_out is None and self._fused_n(n_tokens):
             # the default path: ONE native K3-bulk launch on the caller's stream
-            cur = torch.cuda.current_stream(self.device)
-            ev = _kernel_events(timing, cur, "k3")
-            k, v = dst.ptrs(0)
-            ph, ho = dst.window_args
-            rc = self._pair_recv(self._pair, e, k, v, dst.layer_stride, dst.slots_ptr, n_tokens,
-                                 ph, ho, self._recv_flags, cur.cuda_stream)
-            _lib.check(rc, "kvx_pair_recv")
-            _kernel_events_end(ev, cur)
+            if timing is None:
+                cs = _raw_stream(self.device.index)
+                ev = None
+            else:
+                cur = torch.cuda.current_stream(self.device)
+                cs, ev = cur.cuda_stream, _kernel_events(timing, cur, "k3")
+            rc = self._pair_recv(self._pair, e, dst.k.data_ptr(), dst.v.data_ptr(),
+                                 dst.layer_stride, dst.slots.data_ptr(), n_tokens,
+                                 dst.plane_heads or dst.n_heads, dst.head_offset,
+                                 self._recv_flags, cs)
+            if rc:
+                _lib.check(rc, "kvx_pair_recv")
+            if ev is not None:
+                _kernel_events_end(ev, cur)
             self.epoch = e
             return
         self.epoch = e
@@ -890,6 +903,18 @@ class PairChannel:
         if self.ctl is not None:
             self.ctl.free()
             self.ctl = None
+
+
+try:  # the caller's current stream as a raw cudaStream_t (no torch.cuda.Stream object)
+    _raw_stream_fn = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover - older torch
+    _raw_stream_fn = None
+
+
+def _raw_stream(device_index: int) -> int:
+    if _raw_stream_fn is not None:
+        return _raw_stream_fn(device_index)
+    return torch.cuda.current_stream(device_index).cuda_stream
 
 
 def _kernel_events(timing, stream, name):
