@@ -461,7 +461,8 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
     ch = PairChannel(spec, rank, world, control_group=ctrl)
     lay = spec.layout(T)
     # per step token counts (fixed workload, or the trace's batches)
-    tok = [T] * (args.warmup + args.steps + 2) if trace is None else [sum(x) for x in trace]
+    tok = [T] * ((args.warmup + args.steps + 2) * args.batch) if trace is None else [
+        sum(x) for x in trace]
     seqs = ([(s,) * b] * len(tok)) if trace is None else [tuple(x) for x in trace]
     it = {"i": 0}
     kivi = spec.format == "kivi"
@@ -475,24 +476,41 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
         kv = B.synthetic_kv_device(torch, L, T, H, D, dev, seed=ch.pair)
         planes = KVPlanes.dense(kv)
         def step(timing=None):
-            i = it["i"] % len(tok)
-            t = next_t()
-            if kivi:
-                ch.send(planes, t, seqlens=seqs[i])
-            else:
-                ch.send(planes, t, timing)
+            for _ in range(args.batch if trace is None else 1):
+                i = it["i"] % len(tok)
+                t = next_t()
+                if kivi:
+                    ch.send(planes, t, timing, seqlens=seqs[i])
+                else:
+                    ch.send(planes, t, timing)
     else:
         slots, nb = B.paged_slots(torch, T, dev, seed=ch.pair)
         kc = torch.zeros((L, nb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
         vc = torch.zeros_like(kc)
-        if trace is None:
+        if trace is None and args.batch > 1:
+            # decode rounds: each step drains `batch` queued hand-offs with
+            # one pull launch (recv_many), each into its own blocks
+            need = (T + B.BLOCK - 1) // B.BLOCK
+            nbb = args.batch * need + 64
+            kc = torch.zeros((L, nbb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
+            vc = torch.zeros_like(kc)
+            perm = torch.randperm(nbb, generator=torch.Generator().manual_seed(ch.pair + 1))
+            tt = torch.arange(T)
+            planes_k = [KVPlanes.paged(kc, vc, (perm[j * need + tt // B.BLOCK] * B.BLOCK +
+                                                tt % B.BLOCK).to(dev))
+                        for j in range(args.batch)]
+            planes = planes_k[0]
+
+            def step(timing=None):
+                ch.recv_many([(pl, next_t()) for pl in planes_k], timing)
+        elif trace is None:
             planes = KVPlanes.paged(kc, vc, slots)
 
             def step(timing=None):
                 i = it["i"] % len(tok)
                 t = next_t()
                 if kivi:
-                    ch.recv(planes, t, seqlens=seqs[i])
+                    ch.recv(planes, t, timing, seqlens=seqs[i])
                 else:
                     ch.recv(planes, t, timing)
         else:
@@ -515,7 +533,7 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
             def step(timing=None):
                 i = it["i"] % len(tok)
                 if kivi:
-                    ch.recv(planes_b[i], next_t(), seqlens=seqs[i])
+                    ch.recv(planes_b[i], next_t(), timing, seqlens=seqs[i])
                 else:
                     ch.recv(planes_b[i], next_t(), timing)
     for _ in range(args.warmup):
@@ -626,15 +644,17 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
             timed = tok[args.warmup:args.warmup + args.steps]
             fp16 = sum(spec.layout(t).fp16_bytes for t in timed) / len(timed)
             wire_mean = sum(spec.layout(t).wire_bytes for t in timed) / len(timed)
-        value = pairs * fp16 / (ms_max * 1e-3) / 1e9
+        per_step = args.batch if trace is None else 1  # hand-offs per pair and step
+        value = pairs * per_step * fp16 / (ms_max * 1e-3) / 1e9
         wire = lay.wire_bytes if (trace is None and not kivi) else wire_mean
-        link_gbs = wire / (ms_max * 1e-3) / 1e9  # per pair
+        link_gbs = per_step * wire / (ms_max * 1e-3) / 1e9  # per pair
         hbm, peak_kind = B.peaks()
-        k3_link = wire / (k3 * 1e-3) / 1e9 if k3 > 0 else None
+        k3_link = per_step * wire / (k3 * 1e-3) / 1e9 if k3 > 0 else None
         sm = [c["sm_mhz"] for c in clocks if c.get("sm_mhz")]
         reasons = sorted({r for c in clocks for r in c.get("reasons", [])})
         r = dict(
-            value=value, ms=ms_max, workload=wl, fp16_bytes=fp16 * pairs, wire_bytes=wire * pairs,
+            value=value, ms=ms_max, workload=wl, fp16_bytes=fp16 * pairs * per_step,
+            wire_bytes=wire * pairs * per_step,
             launches=int(g[:, 6].sum()),  # kvx kernels launched in the timed region
             clocks={"sm_mhz": min(sm) if sm else None,
                     "sm_max_mhz": max((c.get("sm_max_mhz") or 0) for c in clocks) or None,
@@ -673,7 +693,10 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                    **({"trace_batches_timed": tok[args.warmup:args.warmup + args.steps],
                        "trace": "lengths log-uniform [128, 8192], 1-16 req/batch, <=16384 "
                                 "tokens/batch, rng(0)"} if trace is not None else {}),
-                   "pairing": pairing(world), "parallelism": f"{pairs}P{pairs}D"},
+                   "pairing": pairing(world), "parallelism": f"{pairs}P{pairs}D",
+                   "handoffs_per_step": per_step,
+                   **({"decode_pull": f"recv_many: {per_step} queued hand-offs per pull launch"}
+                      if per_step > 1 else {})},
         )
         emit(args, r, world)
     dist.barrier()
@@ -712,6 +735,9 @@ def main():
                     help="N>1: no programmatic dependent launch between consecutive pulls")
     ap.add_argument("--tokens", type=int, default=None,
                     help="override the workload's token count (batch 1 x TOKENS) for sweeps")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="N>1: hand-offs per step; the decode side drains them with ONE pull "
+                         "launch (recv_many, a decode round's pull) -- needs --queue-depth >= it")
     ap.add_argument("--no-gate-send", action="store_true",
                     help="N>1: no front-end slot gate before K1 (it waits in-kernel only)")
     ap.add_argument("--gate-recv", action="store_true",

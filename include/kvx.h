@@ -362,6 +362,18 @@ int kvx_pair_send(void* pair, uint64_t epoch, const void* k_src, const void* v_s
 int kvx_pair_recv(void* pair, uint64_t epoch, void* k_cache, void* v_cache,
                   int64_t dst_layer_stride, const int64_t* dst_slots, int64_t n_tokens,
                   int plane_heads, int head_offset, int flags, void* stream);
+/* Decode end: ONE K3-bulk launch pulling `count` consecutive hand-offs
+ * (epochs first_epoch .. first_epoch + count - 1, count <= queue_depth, <= 8)
+ * into the same paged cache -- the decode side draining everything queued
+ * after a decode round.  dst_slots / n_tokens: HOST arrays of
+ * `count` device slot-mapping pointers and token counts (each >= 1).  Each
+ * part waits on its own chunk doorbells in-kernel; the last CTA frees every
+ * part's queue slot.  flags: KVX_PAIR_PDL only.  KVX_ERR_UNSUPPORTED for a
+ * shape the bulk pull cannot stage (use kvx_pair_recv per hand-off). */
+int kvx_pair_recv_many(void* pair, uint64_t first_epoch, int count, void* k_cache, void* v_cache,
+                       int64_t dst_layer_stride, const int64_t* const* dst_slots,
+                       const int64_t* n_tokens, int plane_heads, int head_offset, int flags,
+                       void* stream);
 int kvx_pair_destroy(void* pair);
 
 #ifdef __cplusplus

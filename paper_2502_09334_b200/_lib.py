@@ -71,6 +71,7 @@ SIGNATURES = {
                         ctypes.POINTER(_P)],
     "kvx_pair_send": [_P, _U64, _P, _P, _I64, _P, _I64, _I, _I, _I, _P],
     "kvx_pair_recv": [_P, _U64, _P, _P, _I64, _P, _I64, _I, _I, _I, _P],
+    "kvx_pair_recv_many": [_P, _U64, _I, _P, _P, _I64, _P, _P, _I, _I, _I, _P],
     "kvx_pair_destroy": [_P],
 }
 

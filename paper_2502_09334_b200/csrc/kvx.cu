@@ -373,6 +373,67 @@ cudaError_t dispatch_pull(int group, const kvx::Geo& g, const void* c, const voi
   }
 }
 
+// K3-bulk over several queued hand-offs (kvx_pair_recv_many).  parts[i]
+// carries the slot payload, doorbells, slot mapping and token count; the
+// span geometry is filled in here.  *ok = false: not bulk-stageable.
+template <int BITS, int G>
+cudaError_t launch_pull_many(const kvx::Geo& g, int64_t n_layers, kvx::PullMany& pm,
+                             cudaStream_t s, bool* ok, bool pdl) {
+  *ok = false;
+  pm.code_row_bytes = int(int64_t(g.row_elems) * BITS / 8);
+  pm.meta_row_bytes = int(int64_t(g.row_elems) / G * 2);
+  pm.cpr = g.row_elems / 32;
+  const int64_t m = bulk_row_multiple(pm.code_row_bytes, pm.meta_row_bytes);
+  int64_t max_two_t = 0;
+  for (int i = 0; i < pm.count; ++i) {
+    const kvx::PullPart& P = pm.part[i];
+    const int64_t two_t = 2 * P.n_tokens;
+    if (two_t < 1 || (two_t * pm.code_row_bytes) % 16 || (two_t * pm.meta_row_bytes) % 16 ||
+        !aligned(P.codes, 16) || !aligned(P.scale, 16) || !aligned(P.zero, 16) ||
+        P.payload_ls % 16)
+      return cudaSuccess;
+    max_two_t = two_t > max_two_t ? two_t : max_two_t;
+  }
+  int64_t r = kBulkStageTarget / pm.code_row_bytes;
+  r = r / m * m;
+  if (r < m) r = m;
+  if (r > max_two_t) r = max_two_t;
+  pm.stage_rows = int(r);
+  pm.stage_bytes = pm.stage_rows * (pm.code_row_bytes + 2 * pm.meta_row_bytes);
+  const int smem = kBulkStages * pm.stage_bytes;
+  if (smem > 200 * 1024) return cudaSuccess;
+  int64_t span0 = 0;
+  for (int i = 0; i < pm.count; ++i) {
+    kvx::PullPart& P = pm.part[i];
+    const int64_t two_t = 2 * P.n_tokens;
+    P.rows_per_span = int(r < two_t ? r : two_t);
+    P.spans_per_layer = int((two_t + P.rows_per_span - 1) / P.rows_per_span);
+    P.span0 = uint32_t(span0);
+    span0 += n_layers * P.spans_per_layer;
+    if (span0 >= (int64_t(1) << 31)) return cudaSuccess;
+  }
+  pm.n_spans = uint32_t(span0);
+  auto k = kvx::pull_many_kernel<BITS, G, kBulkStages>;
+  cudaError_t attr = ensure_smem_attr(k, 200 * 1024);
+  if (attr != cudaSuccess) return attr;
+  int per_sm = blocks_per_sm(k, kBulkThreads, smem);
+  per_sm = per_sm < kPullCtasPerSm ? per_sm : kPullCtasPerSm;
+  int64_t grid = int64_t(sm_count(current_device())) * per_sm;
+  if (grid > pm.n_spans) grid = pm.n_spans;
+  *ok = true;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kBulkThreads);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, g, pm);
+}
+
 template <int BITS>
 cudaError_t dispatch_quant(int group, const kvx::Geo& g, void* c, void* sc, void* z, cudaStream_t s,
                            const SignalReq& rq = SignalReq()) {
@@ -1314,6 +1375,78 @@ int kvx_pair_recv(void* pair, uint64_t epoch, void* k_cache, void* v_cache,
                                         head_offset, ready, v, lpc, p->scratch + h * kPairScratch,
                                         p->peer_flags + kFlagFreeBase + h, p->ctl,
                                         (flags & KVX_PAIR_PDL) ? KVX_PULL_PDL : 0, stream);
+}
+
+int kvx_pair_recv_many(void* pair, uint64_t first_epoch, int count, void* k_cache, void* v_cache,
+                       int64_t dst_layer_stride, const int64_t* const* dst_slots,
+                       const int64_t* n_tokens, int plane_heads, int head_offset, int flags,
+                       void* stream) {
+  auto* p = static_cast<kvx_pair*>(pair);
+  if (!p || p->role != KVX_ROLE_DECODE || count < 1 || !dst_slots || !n_tokens ||
+      (flags & ~KVX_PAIR_PDL))
+    return KVX_ERR_INVALID_ARG;
+  if (count > p->queue_depth || count > kvx::kMaxPullMany) return KVX_ERR_INVALID_ARG;
+  for (int i = 0; i < count; ++i) {
+    int rc = pair_check(p, first_epoch + uint64_t(i), n_tokens[i], plane_heads, head_offset);
+    if (rc) return rc;
+    if (n_tokens[i] < 1 || !dst_slots[i]) return KVX_ERR_INVALID_ARG;
+    if (!kvx_pull_supported(n_tokens[i], p->n_heads, p->head_dim, p->group, p->bits))
+      return KVX_ERR_UNSUPPORTED;
+  }
+  kvx::Geo g;
+  int rc = make_geo(g, k_cache, v_cache, dst_layer_stride, nullptr, p->n_layers, 1, p->n_heads,
+                    p->head_dim, p->group, p->bits, 256, 2, 0, plane_heads, head_offset);
+  if (rc) return rc;
+  if (!aligned(k_cache, 32) || !aligned(v_cache, 32) || (dst_layer_stride * 2) % 32 ||
+      g.plane_row_b % 32 || g.head_off_b % 32)
+    return KVX_ERR_INVALID_ARG;
+  kvx::PullMany pm;
+  std::memset(&pm, 0, sizeof(pm));
+  pm.count = count;
+  pm.ctl = p->ctl;
+  int h0 = 0;
+  for (int i = 0; i < count; ++i) {
+    int h;
+    uint32_t v;
+    seq_of(p, first_epoch + uint64_t(i), &h, &v);
+    if (i == 0) h0 = h;
+    int lpc, nc;
+    rc = kvx_handoff_chunk_plan(p->n_layers, n_tokens[i], p->n_heads, p->head_dim, p->layerwise,
+                                &lpc, &nc);
+    if (rc) return rc;
+    int64_t so, zo;
+    const int64_t ls = pair_layer_stride(p, n_tokens[i], &so, &zo);
+    const char* base = p->payload + int64_t(h) * p->slot_bytes;
+    kvx::PullPart& P = pm.part[i];
+    P.codes = reinterpret_cast<const uint8_t*>(base);
+    P.scale = reinterpret_cast<const __half*>(base + so);
+    P.zero = reinterpret_cast<const __half*>(base + zo);
+    P.payload_ls = ls;
+    P.slots = dst_slots[i];
+    P.n_tokens = n_tokens[i];
+    P.ready = p->local_flags + kFlagReadyBase + h * 64;
+    P.ready_value = v;
+    P.layers_per_chunk = lpc;
+    P.peer_free = p->peer_flags + kFlagFreeBase + h;
+  }
+  pm.done_counter = p->scratch + h0 * kPairScratch;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool pdl = flags & KVX_PAIR_PDL;
+  bool ok = false;
+  cudaError_t e;
+  switch (p->bits) {
+    case 2: e = p->group == 32 ? launch_pull_many<2, 32>(g, p->n_layers, pm, s, &ok, pdl)
+              : p->group == 64 ? launch_pull_many<2, 64>(g, p->n_layers, pm, s, &ok, pdl)
+                               : launch_pull_many<2, 128>(g, p->n_layers, pm, s, &ok, pdl); break;
+    case 8: e = p->group == 32 ? launch_pull_many<8, 32>(g, p->n_layers, pm, s, &ok, pdl)
+              : p->group == 64 ? launch_pull_many<8, 64>(g, p->n_layers, pm, s, &ok, pdl)
+                               : launch_pull_many<8, 128>(g, p->n_layers, pm, s, &ok, pdl); break;
+    default: e = p->group == 32 ? launch_pull_many<4, 32>(g, p->n_layers, pm, s, &ok, pdl)
+               : p->group == 64 ? launch_pull_many<4, 64>(g, p->n_layers, pm, s, &ok, pdl)
+                                : launch_pull_many<4, 128>(g, p->n_layers, pm, s, &ok, pdl); break;
+  }
+  if (e != cudaSuccess) return e;
+  return ok ? KVX_OK : KVX_ERR_UNSUPPORTED;
 }
 
 }  // extern "C"

@@ -925,13 +925,66 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
       : "memory");
 }
 
+// Consumer side of one staged span (R token rows of one layer: codes, then
+// the scales, then the zeros, each a contiguous block of the stage buffer):
+// dequantise and scatter the rows into the paged cache.  Short rows (fewer
+// than 32 chunks, e.g. a TP shard's few KV heads): a warp covers 32 / cpr
+// rows per pass so every lane has a chunk.
+template <int BITS, int G, int CONSUMERS>
+__device__ __forceinline__ void bulk_consume_span(const Geo& g, int code_row_bytes,
+                                                  int meta_row_bytes, int rows_per_span, int cpr,
+                                                  const uint8_t* buf, int rows, int64_t r0,
+                                                  uint32_t layer, int warp, int lane) {
+  constexpr int CB = 32 * BITS / 8;
+  constexpr int LPG = G / 32;
+  const __half* sbuf = reinterpret_cast<const __half*>(buf + rows_per_span * code_row_bytes);
+  const __half* zbuf = sbuf + rows_per_span * meta_row_bytes / 2;
+  const int rpw = (cpr < 32 && (32 % cpr) == 0) ? 32 / cpr : 1;
+  const int sub = rpw > 1 ? lane / cpr : 0;
+  const int cl = rpw > 1 ? lane % cpr : lane;
+  const int gpr = meta_row_bytes / 2;
+  for (int rb = warp * rpw; rb < rows; rb += CONSUMERS * rpw) {
+    const int r = rb + sub;
+    if (r >= rows) continue;
+    const int64_t lrow = r0 + r;
+    const int p = lrow >= g.n_tokens;
+    const int kv = g.plane0 + p;
+    const int64_t t = lrow - p * g.n_tokens;
+    const int64_t pos = pos_of(g, t);
+    if (pos < 0) continue;  // padding token
+    char* dst = const_cast<char*>(row_ptr(g, plane_ptr(g, kv, layer), pos));
+    const uint8_t* crow = buf + r * code_row_bytes;
+    for (int c = cl; c < cpr; c += 32) {
+      K3Data<BITS> d;
+      if constexpr (BITS == 2) {
+        const uint2 v = *reinterpret_cast<const uint2*>(crow + c * CB);
+        d.c.w[0] = v.x;
+        d.c.w[1] = v.y;
+      } else {
+#pragma unroll
+        for (int i = 0; i < Chunk32<BITS>::WORDS / 4; ++i) {
+          const uint4 v = reinterpret_cast<const uint4*>(crow + c * CB)[i];
+          d.c.w[4 * i] = v.x;
+          d.c.w[4 * i + 1] = v.y;
+          d.c.w[4 * i + 2] = v.z;
+          d.c.w[4 * i + 3] = v.w;
+        }
+      }
+      d.s = sbuf[r * gpr + c / LPG];
+      d.z = zbuf[r * gpr + c / LPG];
+      K3Item it;
+      it.active = true;
+      it.dst = dst + int64_t(c) * 64;
+      k3_process<BITS>(it, d);
+    }
+  }
+}
+
 template <int BITS, int G, int STAGES>
 __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     Geo g, BulkGeo bg, const uint8_t* __restrict__ codes, const __half* __restrict__ scale,
     const __half* __restrict__ zero) {
   constexpr int CONSUMERS = 8;
-  constexpr int CB = 32 * BITS / 8;
-  constexpr int LPG = G / 32;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   __shared__ uint32_t s_abort;
@@ -1010,56 +1063,15 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     const int64_t r0 = int64_t(sp - layer * bg.spans_per_layer) * bg.rows_per_span;
     const int rows = int(min(int64_t(bg.rows_per_span), two_t - r0));
     const uint8_t* buf = smem + st * bg.stage_bytes;
-    const __half* sbuf = reinterpret_cast<const __half*>(buf + bg.rows_per_span * bg.code_row_bytes);
-    const __half* zbuf = sbuf + bg.rows_per_span * bg.meta_row_bytes / 2;
     mbar_wait(&full[st], (k / STAGES) & 1);
     if (*reinterpret_cast<volatile uint32_t*>(&s_abort)) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
       continue;
     }
-    // short rows (fewer than 32 chunks, e.g. a TP shard's few KV heads): a
-    // warp covers 32 / cpr rows per pass so every lane has a chunk
-    const int cpr = bg.cpr;
-    const int rpw = (cpr < 32 && (32 % cpr) == 0) ? 32 / cpr : 1;
-    const int sub = rpw > 1 ? lane / cpr : 0;
-    const int cl = rpw > 1 ? lane % cpr : lane;
-    const int gpr = bg.meta_row_bytes / 2;
-    for (int rb = warp * rpw; rb < rows; rb += CONSUMERS * rpw) {
-      const int r = rb + sub;
-      if (r >= rows) continue;
-      const int64_t lrow = r0 + r;
-      const int p = lrow >= g.n_tokens;
-      const int kv = g.plane0 + p;
-      const int64_t t = lrow - p * g.n_tokens;
-      const int64_t pos = pos_of(g, t);
-      if (pos < 0) continue;  // padding token
-      char* dst = const_cast<char*>(row_ptr(g, plane_ptr(g, kv, layer), pos));
-      const uint8_t* crow = buf + r * bg.code_row_bytes;
-      for (int c = cl; c < cpr; c += 32) {
-        K3Data<BITS> d;
-        if constexpr (BITS == 2) {
-          const uint2 v = *reinterpret_cast<const uint2*>(crow + c * CB);
-          d.c.w[0] = v.x;
-          d.c.w[1] = v.y;
-        } else {
-#pragma unroll
-          for (int i = 0; i < Chunk32<BITS>::WORDS / 4; ++i) {
-            const uint4 v = reinterpret_cast<const uint4*>(crow + c * CB)[i];
-            d.c.w[4 * i] = v.x;
-            d.c.w[4 * i + 1] = v.y;
-            d.c.w[4 * i + 2] = v.z;
-            d.c.w[4 * i + 3] = v.w;
-          }
-        }
-        d.s = sbuf[r * gpr + c / LPG];
-        d.z = zbuf[r * gpr + c / LPG];
-        K3Item it;
-        it.active = true;
-        it.dst = dst + int64_t(c) * 64;
-        k3_process<BITS>(it, d);
-      }
-    }
+    bulk_consume_span<BITS, G, CONSUMERS>(g, bg.code_row_bytes, bg.meta_row_bytes,
+                                          bg.rows_per_span, bg.cpr, buf, rows, r0, layer, warp,
+                                          lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
@@ -1090,6 +1102,153 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
         atomicMax(&g_trace_n[1], trace_id + 1);
 #endif
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3-bulk over several queued hand-offs in ONE launch (the decode side's pull
+// of everything queued after a decode round).  The parts are
+// consecutive queue slots of one pair landing in one paged cache; their spans
+// are concatenated (part by part, layer-major within a part) and CTA-strided
+// exactly like the single pull, each part waiting on its own chunk doorbells.
+// The last CTA out frees every part's slot.  Amortises the per-launch ramp,
+// tail and host cost that dominate short hand-offs.
+// ---------------------------------------------------------------------------
+constexpr int kMaxPullMany = 8;  // = the queue depth bound
+
+struct PullPart {
+  const uint8_t* codes;   // the slot's payload: codes / scales / zeros of layer 0
+  const __half* scale;
+  const __half* zero;
+  int64_t payload_ls;     // bytes between payload layers (per-layer segments)
+  const int64_t* slots;   // token -> paged position
+  int64_t n_tokens;
+  const uint32_t* ready;  // this part's chunk doorbells (this GPU), ready[c] >= ready_value
+  uint32_t ready_value;
+  int layers_per_chunk;
+  uint32_t* peer_free;    // the slot's free flag on the prefill GPU
+  uint32_t span0;         // first span of the part in the launch's span space
+  int spans_per_layer;
+  int rows_per_span;      // <= PullMany::stage_rows
+};
+
+struct PullMany {
+  PullPart part[kMaxPullMany];
+  int count;
+  uint32_t n_spans;
+  uint32_t* done_counter;  // as BulkGeo::done_counter
+  Ctl* ctl;
+  int code_row_bytes, meta_row_bytes, stage_bytes, cpr;
+  int stage_rows;          // rows a stage holds (scales start at stage_rows * code_row_bytes)
+};
+
+template <int BITS, int G, int STAGES>
+__global__ void __launch_bounds__(288, 1) pull_many_kernel(Geo g, const __grid_constant__ PullMany pm) {
+  constexpr int CONSUMERS = 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ uint32_t s_abort;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CONSUMERS);
+    }
+    s_abort = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == CONSUMERS) {  // ---- producer: one elected thread
+    if (lane == 0) {
+      uint32_t k = 0;
+      int i = 0, ready_chunk = -1;
+      bool ok = true;
+      for (uint32_t sp = blockIdx.x; sp < pm.n_spans; sp += gridDim.x, ++k) {
+        const int st = k % STAGES;
+        if (k >= STAGES) mbar_wait(&empty[st], ((k / STAGES) & 1) ^ 1);
+        while (i + 1 < pm.count && sp >= pm.part[i + 1].span0) {
+          ++i;
+          ready_chunk = -1;
+        }
+        const PullPart& P = pm.part[i];
+        const uint32_t local = sp - P.span0;
+        const uint32_t layer = local / P.spans_per_layer;
+        if (ok) {
+          const int c = int(layer) / P.layers_per_chunk;
+          if (c > ready_chunk) {
+            ok = wait_ready(P.ready + c, P.ready_value, pm.ctl);
+            if (!ok) *reinterpret_cast<volatile uint32_t*>(&s_abort) = 1u;
+            ready_chunk = c;
+          }
+        }
+        if (!ok) {
+          mbar_arrive_empty_phase(&full[st]);
+          continue;
+        }
+        const int64_t two_t = 2 * P.n_tokens;
+        const int64_t r0 = int64_t(local - layer * P.spans_per_layer) * P.rows_per_span;
+        const int rows = int(min(int64_t(P.rows_per_span), two_t - r0));
+        uint8_t* buf = smem + st * pm.stage_bytes;
+        const uint32_t cb = rows * pm.code_row_bytes, mb = rows * pm.meta_row_bytes;
+        mbar_expect_tx(&full[st], cb + 2 * mb);
+        const char* seg = reinterpret_cast<const char*>(P.codes) + int64_t(layer) * P.payload_ls;
+        bulk_g2s(buf, seg + r0 * pm.code_row_bytes, cb, &full[st]);
+        const char* sbase = reinterpret_cast<const char*>(P.scale) + int64_t(layer) * P.payload_ls;
+        const char* zbase = reinterpret_cast<const char*>(P.zero) + int64_t(layer) * P.payload_ls;
+        uint8_t* mbuf = buf + pm.stage_rows * pm.code_row_bytes;
+        bulk_g2s(mbuf, sbase + r0 * pm.meta_row_bytes, mb, &full[st]);
+        bulk_g2s(mbuf + pm.stage_rows * pm.meta_row_bytes, zbase + r0 * pm.meta_row_bytes, mb,
+                 &full[st]);
+      }
+      pdl_launch_dependents();  // as in pull_dequant_scatter_kernel
+    }
+  } else {
+    pdl_wait();  // the slot mappings and the cache are stream-ordered inputs
+    uint32_t k = 0;
+    int i = 0;
+    Geo gp = g;
+    gp.slots = pm.part[0].slots;
+    gp.n_tokens = pm.part[0].n_tokens;
+    for (uint32_t sp = blockIdx.x; sp < pm.n_spans; sp += gridDim.x, ++k) {
+      const int st = k % STAGES;
+      while (i + 1 < pm.count && sp >= pm.part[i + 1].span0) {
+        ++i;
+        gp.slots = pm.part[i].slots;
+        gp.n_tokens = pm.part[i].n_tokens;
+      }
+      const PullPart& P = pm.part[i];
+      const uint32_t local = sp - P.span0;
+      const uint32_t layer = local / P.spans_per_layer;
+      const int64_t r0 = int64_t(local - layer * P.spans_per_layer) * P.rows_per_span;
+      const int rows = int(min(int64_t(P.rows_per_span), 2 * P.n_tokens - r0));
+      const uint8_t* buf = smem + st * pm.stage_bytes;
+      mbar_wait(&full[st], (k / STAGES) & 1);
+      if (*reinterpret_cast<volatile uint32_t*>(&s_abort)) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        continue;
+      }
+      bulk_consume_span<BITS, G, CONSUMERS>(gp, pm.code_row_bytes, pm.meta_row_bytes,
+                                            pm.stage_rows, pm.cpr, buf, rows, r0, layer, warp,
+                                            lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  // completion: every part's slot is freed by the last CTA out (see the
+  // single pull for why no fence is needed)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t inc = s_abort ? 0x10001u : 1u;
+    const uint32_t total = atomicAdd(pm.done_counter, inc) + inc;
+    if ((total & 0xFFFFu) == gridDim.x) {
+      pm.done_counter[0] = 0u;
+      if ((total >> 16) == 0u)
+        for (int j = 0; j < pm.count; ++j)
+          asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(pm.part[j].peer_free),
+                       "r"(pm.part[j].ready_value)
+                       : "memory");
     }
   }
 }

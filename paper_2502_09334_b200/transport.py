@@ -499,7 +499,7 @@ class PairChannel:
             return  # nothing to hand off (both ends skip it: no epoch consumed)
         if self.spec.format == "kivi":
             self.epoch += 1
-            return self._send_kivi(src, n_tokens, seqlens, self.epoch)
+            return self._send_kivi(src, n_tokens, seqlens, self.epoch, timing)
         e = self.epoch + 1
         if stage_in is None and self._fused_n(n_tokens):
             # the default path: ONE native launch on the caller's stream
@@ -655,7 +655,7 @@ class PairChannel:
             return
         if self.spec.format == "kivi":
             self.epoch += 1
-            return self._recv_kivi(dst, n_tokens, seqlens, self.epoch)
+            return self._recv_kivi(dst, n_tokens, seqlens, self.epoch, timing)
         e = self.epoch + 1
         mode = self.spec.mode
         if stage_out is None and self._fused_n(n_tokens):
@@ -724,6 +724,56 @@ class PairChannel:
         cur.wait_stream(cs)
         if stage_out is not None:
             cur.wait_stream(self.xfer)
+
+    def recv_many(self, items, timing: list | None = None) -> None:
+        """Decode end, fused pull: receive the next ``len(items)`` hand-offs
+        with ONE K3-bulk launch (``kvx_pair_recv_many``) -- the decode side
+        draining everything queued after a decode round.
+        ``items``: [(dst_planes, n_tokens), ...] in hand-off order, at most the
+        queue depth; every destination is the same paged cache (only the slot
+        mappings differ).  Hand-offs the bulk pull cannot stage (or any other
+        transport) are received one by one instead."""
+        if self.role != "decode":
+            raise RuntimeError("recv_many() on the prefill end of the channel")
+        items = [(d, int(n)) for d, n in items]
+        if not items:
+            return
+        if len(items) > self.Q:
+            raise ValueError(f"recv_many: {len(items)} hand-offs > queue depth {self.Q}")
+        self.check()
+        d0 = items[0][0]
+        key = (d0.k.data_ptr(), d0.v.data_ptr(), d0.layer_stride, d0.plane_heads or d0.n_heads,
+               d0.head_offset)
+        batch = True
+        for d, n in items:
+            self.spec.check_planes(d, n, "destination")
+            if d.slots is None:
+                raise ValueError("the decode side needs a slot mapping (paged destination)")
+            if (d.k.data_ptr(), d.v.data_ptr(), d.layer_stride, d.plane_heads or d.n_heads,
+                    d.head_offset) != key:
+                raise ValueError("recv_many: every hand-off must land in the same cache")
+            batch = batch and n > 0 and self._fused_n(n)
+        if not batch:
+            for d, n in items:
+                self.recv(d, n, timing)
+            return
+        k = len(items)
+        slots = (ctypes.c_void_p * k)(*[d.slots.data_ptr() for d, _ in items])
+        ns = (ctypes.c_int64 * k)(*[n for _, n in items])
+        if timing is None:
+            cs, ev = _raw_stream(self.device.index), None
+        else:
+            cur = torch.cuda.current_stream(self.device)
+            cs, ev = cur.cuda_stream, _kernel_events(timing, cur, "k3")
+        e0 = self.epoch + 1
+        rc = _lib.load().kvx_pair_recv_many(self._pair, e0, k, d0.k.data_ptr(), d0.v.data_ptr(),
+                                            d0.layer_stride, slots, ns, key[3], key[4],
+                                            self._recv_flags & _lib.KVX_PAIR_PDL, cs)
+        if rc:
+            _lib.check(rc, "kvx_pair_recv_many")
+        if ev is not None:
+            _kernel_events_end(ev, cur)
+        self.epoch = e0 + k - 1
 
     def _recv_pull(self, dst, lay, e, s, cur, timing, stage_out):
         """Pull receive on the channel stream: the bulk kernel with in-kernel
@@ -805,7 +855,7 @@ class PairChannel:
         cache[key] = hit  # most recently used last
         return hit[0], hit[1]
 
-    def _send_kivi(self, src, n_tokens, seqlens, e):
+    def _send_kivi(self, src, n_tokens, seqlens, e, timing=None):
         """The fused kivi prefill side: K per-channel, residual and V
         quantisers over the whole hand-off, ringing the K and V chunk
         doorbells from inside the kernels (kvx_quant_pack_kivi_signal); the
@@ -820,6 +870,7 @@ class PairChannel:
             self._kivi_cnt = torch.zeros((PULL_MAX_QUEUE, 2 * PULL_MAX_CHUNKS), dtype=torch.int32,
                                          device=self.device)
         k, vv = src.ptrs(0)
+        ev = _kernel_events(timing, s, "k1")
         _lib.call("kvx_quant_pack_kivi_signal", k, vv, src.layer_stride, lay.n_layers, n_tokens,
                   lay.n_heads, lay.head_dim, lay.group, lay.bits,
                   gs_d.data_ptr() if len(gs) else None, len(gs),
@@ -828,9 +879,10 @@ class PairChannel:
                   self._pready(self.peer_flags, h, 0), lpc, v,
                   self._pfree(self.flags.ptr, h) if v > 1 else None, v - 1, self.ctl.ptr,
                   _stream_ptr(s))
+        _kernel_events_end(ev, s)
         cur.wait_stream(s)
 
-    def _recv_kivi(self, dst, n_tokens, seqlens, e):
+    def _recv_kivi(self, dst, n_tokens, seqlens, e, timing=None):
         lay, gs, rt, chunks, lpc, h, v = self._kivi_common(n_tokens, seqlens, e)
         s, cur = self.stream, torch.cuda.current_stream(self.device)
         s.wait_stream(cur)
@@ -851,8 +903,10 @@ class PairChannel:
         if self.spec.mode == "pull":
             # TMA bulk-staged kernels over the whole hand-off, waiting in-kernel
             # for each chunk's doorbell (a handful of launches per hand-off)
+            ev = _kernel_events(timing, s, "k3")
             _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args(0, lay.n_layers),
                       self._pready(self.flags.ptr, h, 0), v, lpc, self.ctl.ptr, _stream_ptr(s))
+            _kernel_events_end(ev, s)
         else:  # "pull_ldg": per-chunk stream waits, per-lane peer loads
             for c, (l0, l1) in enumerate(chunks):
                 # the chunk's V doorbell publishes all of it (K, residual, V)

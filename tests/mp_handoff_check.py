@@ -315,6 +315,50 @@ def main():
         print(f"queue_depth={Q}: prefill ran {Q} hand-offs ahead", flush=True)
     dist.barrier()
     ch.close()
+
+    # recv_many: the decode side drains several queued hand-offs (ragged
+    # lengths, each into its own blocks of one cache) with ONE pull launch,
+    # over 3 rounds so every slot is reused; bit-exact vs the oracle
+    Q = 4
+    spec = ChannelSpec(L, Tmax, H, D, 4, 128, 3, "pull", queue_depth=Q)
+    ch = PairChannel(spec, rank, world, control_group=ctrl)
+    for rnd in range(3):
+        Ts = [Tmax, 16, 77, 130][: 2 + rnd]
+        seeds = [7000 + 100 * rnd + 10 * i + ch.pair for i in range(len(Ts))]
+        if ch.role == "prefill":
+            for T, sd in zip(Ts, seeds):
+                ch.send(KVPlanes.dense(torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=sd)).to(dev)), T)
+            torch.cuda.synchronize()
+        else:
+            nbm = sum(-(-T // bs) for T in Ts) + 4
+            kcm = torch.zeros((L, nbm, bs, H, D), dtype=torch.float16, device=dev)
+            vcm = torch.zeros_like(kcm)
+            perm = np.random.default_rng(rnd).permutation(nbm)
+            items, slots_l, b0 = [], [], 0
+            for T in Ts:
+                nbt = -(-T // bs)
+                t = np.arange(T)
+                sl = (perm[b0 + t // bs] * bs + t % bs).astype(np.int64)
+                b0 += nbt
+                slots_l.append(sl)
+                items.append((KVPlanes.paged(kcm, vcm, torch.from_numpy(sl).to(dev)), T))
+            ch.recv_many(items)
+            torch.cuda.synchronize()
+            ch.check()
+            okc = np.zeros((L, nbm, bs, H, D), np.float16); ovc = okc.copy()
+            for T, sd, sl in zip(Ts, seeds, slots_l):
+                c, s_, z = O.quant_pack(O.synthetic_kv(L, T, H, D, seed=sd).reshape(-1, D), 4, 128)
+                O.scatter_paged(O.unpack_dequant(c, s_, z, 4, 128, D).reshape(L, 2, T, H, D),
+                                sl, okc, ovc)
+            if not (np.array_equal(kcm.cpu().numpy().view(np.uint16), okc.view(np.uint16)) and
+                    np.array_equal(vcm.cpu().numpy().view(np.uint16), ovc.view(np.uint16))):
+                failures += 1
+                print(f"MISMATCH recv_many rank={rank} round={rnd} Ts={Ts}", flush=True)
+        dist.barrier(ctrl)
+    if rank == 0:
+        print("recv_many: ok", flush=True)
+    dist.barrier()
+    ch.close()
     f = _mp.total(failures, ctrl)
     if rank == 0:
         print(f"mp_handoff_check modes={modes} world={world} failures={f}", flush=True)
