@@ -340,7 +340,10 @@ int kvx_handoff_chunk_plan(int64_t n_layers, int64_t n_tokens, int n_heads, int 
  * ONE kernel launch per end:
  *   kvx_pair_send: K1 with device doorbells into slot e % Q (KVX_PAIR_GATE:
  *     first a stream memop holding the launch in the GPU front-end until the
- *     decode side has freed the slot -- a lagging partner holds no SMs);
+ *     decode side has freed the slot -- a lagging partner holds no SMs;
+ *     KVX_PAIR_PDL instead: latency mode, the K1 is launched with
+ *     programmatic dependent launch behind the stream's previous kernel and
+ *     waits for the slot in-kernel only);
  *   kvx_pair_recv: K3-bulk pulling the slot over NVLink as chunks are
  *     published, freeing it in-kernel (KVX_PAIR_GATE: launch once chunk 0 is
  *     published; KVX_PAIR_PDL: programmatic dependent launch, so a pull

@@ -206,6 +206,7 @@ struct SignalReq {
   kvx::Ctl* ctl = nullptr;
   int layers_per_chunk = 1;
   int64_t n_layers = 0;
+  bool pdl = false;  // programmatic dependent launch behind the stream's previous kernel
 };
 
 template <int BITS, int G>
@@ -237,10 +238,23 @@ cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero
     // (the counters are zero between launches: each chunk's last arrival resets its own)
   }
   auto k = kvx::quant_pack_kernel<BITS, G>;
-  k<<<grid_for(k, ig.n_items), kThreads, 0, s>>>(g, ig, static_cast<uint8_t*>(codes),
-                                                 static_cast<__half*>(scale),
-                                                 static_cast<__half*>(zero), sig);
-  return cudaGetLastError();
+  if (!rq.pdl) {
+    k<<<grid_for(k, ig.n_items), kThreads, 0, s>>>(g, ig, static_cast<uint8_t*>(codes),
+                                                   static_cast<__half*>(scale),
+                                                   static_cast<__half*>(zero), sig);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid_for(k, ig.n_items);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, g, ig, static_cast<uint8_t*>(codes),
+                            static_cast<__half*>(scale), static_cast<__half*>(zero), sig);
 }
 
 template <int BITS, int G>
@@ -1308,7 +1322,8 @@ int kvx_pair_send(void* pair, uint64_t epoch, const void* k_src, const void* v_s
   auto* p = static_cast<kvx_pair*>(pair);
   int rc = pair_check(p, epoch, n_tokens, plane_heads, head_offset);
   if (rc) return rc;
-  if (p->role != KVX_ROLE_PREFILL || (flags & ~KVX_PAIR_GATE)) return KVX_ERR_INVALID_ARG;
+  if (p->role != KVX_ROLE_PREFILL || (flags & ~(KVX_PAIR_GATE | KVX_PAIR_PDL)))
+    return KVX_ERR_INVALID_ARG;
   if (n_tokens == 0) return KVX_OK;
   int h;
   uint32_t v;
@@ -1331,11 +1346,39 @@ int kvx_pair_send(void* pair, uint64_t epoch, const void* k_src, const void* v_s
     rc = kvx_stream_wait(free_flag, v - 1, stream);
     if (rc) return rc;
   }
-  return kvx_quant_pack_signal(k_src, v_src, src_layer_stride, src_slots, p->n_layers, n_tokens,
-                               p->n_heads, p->head_dim, p->group, p->bits, base, base + so,
-                               base + zo, ls, plane_heads, head_offset,
-                               p->scratch + h * kPairScratch, p->peer_flags + kFlagReadyBase + h * 64,
-                               lpc, v, free_flag, v - 1, p->ctl, s);
+  if (!(flags & KVX_PAIR_PDL))
+    return kvx_quant_pack_signal(k_src, v_src, src_layer_stride, src_slots, p->n_layers, n_tokens,
+                                 p->n_heads, p->head_dim, p->group, p->bits, base, base + so,
+                                 base + zo, ls, plane_heads, head_offset,
+                                 p->scratch + h * kPairScratch,
+                                 p->peer_flags + kFlagReadyBase + h * 64, lpc, v, free_flag, v - 1,
+                                 p->ctl, s);
+  // PDL: K1 launched behind the stream's previous kernel (typically the
+  // previous hand-off's K1, which signals once its items are done); its CTAs
+  // wait (griddepcontrol.wait) for that grid before reading anything
+  kvx::Geo g;
+  rc = make_geo(g, k_src, v_src, src_layer_stride, src_slots, p->n_layers, n_tokens, p->n_heads,
+                p->head_dim, p->group, p->bits, ls, 2, 0, plane_heads, head_offset);
+  if (rc) return rc;
+  if (!aligned(k_src, 32) || !aligned(v_src, 32) || (src_layer_stride * 2) % 32 ||
+      g.plane_row_b % 32 || g.head_off_b % 32)
+    return KVX_ERR_INVALID_ARG;
+  SignalReq rq;
+  rq.counters = p->scratch + h * kPairScratch;
+  rq.peer_flags = p->peer_flags + kFlagReadyBase + h * 64;
+  rq.ready_value = v;
+  rq.free_flag = free_flag;
+  rq.free_value = v - 1;
+  rq.ctl = p->ctl;
+  rq.layers_per_chunk = lpc;
+  rq.n_layers = p->n_layers;
+  rq.pdl = true;
+  char* codes = base;
+  switch (p->bits) {
+    case 2: return dispatch_quant<2>(p->group, g, codes, base + so, base + zo, s, rq);
+    case 8: return dispatch_quant<8>(p->group, g, codes, base + so, base + zo, s, rq);
+    default: return dispatch_quant<4>(p->group, g, codes, base + so, base + zo, s, rq);
+  }
 }
 
 int kvx_pair_recv(void* pair, uint64_t epoch, void* k_cache, void* v_cache,

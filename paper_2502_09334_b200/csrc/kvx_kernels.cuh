@@ -579,6 +579,9 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
   const uint32_t trace_id = sig.trace_id;
   if (sig.peer_flags && blockIdx.x == 0 && threadIdx.x == 0) KVX_TRACE_STAMP(0, trace_id, 0);
 #endif
+  // PDL launches (kvx_pair_send with KVX_PAIR_PDL): wait for the stream's
+  // previous grid and its memory before reading anything (a no-op otherwise)
+  pdl_wait();
   if (sig.peer_flags) {
     for (int i = threadIdx.x; i < kMaxSignalChunks; i += blockDim.x) cta_cnt[i] = 0u;
     if (threadIdx.x == 0) {
@@ -627,6 +630,9 @@ __global__ void __launch_bounds__(256, KVX_K1_MIN_BLOCKS) quant_pack_kernel(Geo 
     }
   }
 k1_done:
+  // this warp's items are done: the stream's next kernel may be scheduled
+  // (it waits for this grid's completion before it reads anything)
+  pdl_launch_dependents();
 #ifdef KVX_TRACE
   if (sig.peer_flags) {  // trace builds: stamp the last CTA's exit
     __syncthreads();

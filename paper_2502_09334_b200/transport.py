@@ -410,7 +410,10 @@ class PairChannel:
             self._pair = h.value
             L = _lib.load()
             self._pair_send, self._pair_recv = L.kvx_pair_send, L.kvx_pair_recv
-            self._send_flags = _lib.KVX_PAIR_GATE if spec.gate_send else 0
+            # the front-end slot gate, or (latency mode) K1s chained with PDL
+            # that wait for the slot in-kernel
+            self._send_flags = (_lib.KVX_PAIR_GATE if spec.gate_send else
+                                _lib.KVX_PAIR_PDL if spec.pdl else 0)
             self._recv_flags = ((_lib.KVX_PAIR_GATE if spec.gate_recv else 0) |
                                 (_lib.KVX_PAIR_PDL if spec.pdl else 0))
 

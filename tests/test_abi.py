@@ -201,6 +201,9 @@ def test_pair_entry_points_validate(lib):
     assert lib.kvx_pair_create(*good[:13], 12, ctypes.byref(out)) == E   # ctl alignment
     assert lib.kvx_pair_send(None, 1, 256, 256, 0, None, 1, 0, 0, 0, None) == E
     assert lib.kvx_pair_recv(None, 1, 256, 256, 0, 256, 1, 0, 0, 0, None) == E
+    slots = (ctypes.c_void_p * 1)(256)
+    ns = (ctypes.c_int64 * 1)(16)
+    assert lib.kvx_pair_recv_many(None, 1, 1, 256, 256, 0, slots, ns, 0, 0, 0, None) == E
     assert lib.kvx_pair_destroy(None) == 0
     lpc, nc = ctypes.c_int(), ctypes.c_int()
     # a 16-token 70B GQA hand-off is one chunk; config 3 is layer-granular

@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--queue-depth", type=int, default=2)
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--no-gate-send", action="store_true")
     ap.add_argument("--layers", type=int, default=80)
     ap.add_argument("--heads", type=int, default=8)
     a = ap.parse_args()
@@ -50,7 +51,8 @@ def main():
     ctrl = dist.new_group(backend="gloo")
     L, H, D, T = a.layers, a.heads, 128, a.tokens
     ch = PairChannel(ChannelSpec(L, T, H, D, 4, 128, 8, "pull", queue_depth=a.queue_depth,
-                                 pdl=not a.no_pdl), rank, 2, control_group=ctrl)
+                                 pdl=not a.no_pdl, gate_send=not a.no_gate_send),
+                     rank, 2, control_group=ctrl)
     if ch.role == "prefill":
         kv = torch.randn((L, 2, T, H, D), device=dev).half()
         planes = KVPlanes.dense(kv)
@@ -90,6 +92,7 @@ def main():
             "k3_gap_prev_out_to_start_us": med(k3[n // 2 + 1:, 0] - k3[n // 2:-1, 3]),
             "k3_start_minus_k1_rung_us": med(k3[s, 0] - d - k1[s, 2]),
             "queue_depth": a.queue_depth, "pdl": not a.no_pdl, "layers": L, "heads": H,
+            "gate_send": not a.no_gate_send,
         }
         # three consecutive steady-state hand-offs on one (prefill) clock, us
         # relative to the first K1's start
