@@ -457,7 +457,7 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                        format=getattr(args, "format", "default"),
                        queue_depth=getattr(args, "queue_depth", 2),
                        pdl=not args.no_pdl, gate_recv=args.gate_recv,
-                       gate_send=not args.no_gate_send)
+                       gate_send=args.gate_send and not args.no_gate_send)
     ch = PairChannel(spec, rank, world, control_group=ctrl)
     lay = spec.layout(T)
     # per step token counts (fixed workload, or the trace's batches)
@@ -729,7 +729,7 @@ def main():
                     help="reference arm: layers per step (default: ~1 GB of fp16 KV)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--queue-depth", type=int, default=2,
+    ap.add_argument("--queue-depth", type=int, default=4,
                     help="pull: queue slots per pair in the prefill GPU's HBM")
     ap.add_argument("--no-pdl", action="store_true",
                     help="N>1: no programmatic dependent launch between consecutive pulls")
@@ -738,8 +738,11 @@ def main():
     ap.add_argument("--batch", type=int, default=1,
                     help="N>1: hand-offs per step; the decode side drains them with ONE pull "
                          "launch (recv_many, a decode round's pull) -- needs --queue-depth >= it")
-    ap.add_argument("--no-gate-send", action="store_true",
-                    help="N>1: no front-end slot gate before K1 (it waits in-kernel only)")
+    ap.add_argument("--gate-send", action="store_true",
+                    help="N>1: hold each K1 in the GPU front-end until its queue slot is free "
+                         "(ChannelSpec.gate_send; default here: latency mode -- K1s chained with "
+                         "PDL, waiting for the slot in-kernel)")
+    ap.add_argument("--no-gate-send", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--gate-recv", action="store_true",
                     help="N>1: hold each pull in the GPU front-end until chunk 0 is published")
     args = ap.parse_args()
