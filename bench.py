@@ -340,10 +340,13 @@ def run_local(args, torch):
     if not args.no_e2e and args.format == "default":
         kv_h = torch.empty(kv.shape, dtype=torch.float16, pin_memory=True)
         kv_h.copy_(kv)
-        kc_h = torch.empty(kc.shape, dtype=torch.float16, pin_memory=True)
-        vc_h = torch.empty(vc.shape, dtype=torch.float16, pin_memory=True)
+        # the host cache holds exactly the blocks this hand-off fills (a random
+        # permutation of them): the D2H moves the hand-off's result, no slack
+        e_slots, e_nb = paged_slots(torch, T, dev, slack_blocks=0)
+        kc_h = torch.empty((L, e_nb, BLOCK, H, D), dtype=torch.float16, pin_memory=True)
+        vc_h = torch.empty((L, e_nb, BLOCK, H, D), dtype=torch.float16, pin_memory=True)
         del plan
-        host = HostHandoff(kv_h, kc_h, vc_h, slots, dev, KvPrecision(args.bits), args.group,
+        host = HostHandoff(kv_h, kc_h, vc_h, e_slots, dev, KvPrecision(args.bits), args.group,
                            n_chunks=args.e2e_chunks)
         for _ in range(max(1, min(args.warmup, 3))):
             host.run()
@@ -359,8 +362,9 @@ def run_local(args, torch):
         e2e = {"value": round(fp16_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
                "h2d_bytes_per_step": host.h2d_bytes, "d2h_bytes_per_step": host.d2h_bytes,
                "ms_per_step": round(e2e_ms, 3), "steps": n_e2e,
-               "path": "pinned host KV -> H2D -> K1 -> K3 -> D2H of the paged cache, "
-                       f"{len(host.chunks)} layer chunks on 3 streams"}
+               "path": "pinned host KV -> H2D -> K1 -> K3 -> D2H of the paged cache (exactly "
+                       f"the blocks the hand-off fills), {len(host.chunks)} layer chunks on 3 "
+                       "streams"}
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_reference(wl, args.bits, args.group, budget_s=args.cpu_budget)
