@@ -55,6 +55,29 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
     return out
 
 
+FAST_SRC = os.path.join(HERE, "csrc", "kvx_fast.c")
+
+
+def fast_path() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_kvx_fast" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_fast(force: bool = False) -> str:
+    """The CPython fast-call shims for kvx_pair_send/recv (csrc/kvx_fast.c)."""
+    import sysconfig
+    out = fast_path()
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(FAST_SRC):
+        return out
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-Wall",
+           f"-I{sysconfig.get_paths()['include']}", "-o", out, FAST_SRC]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"cc failed ({r.returncode}): {' '.join(cmd)}")
+    return out
+
+
 if __name__ == "__main__":
     if "--variant" in sys.argv:
         i = sys.argv.index("--variant")
@@ -62,3 +85,4 @@ if __name__ == "__main__":
         print(build(variant=name, defines=defs))
     else:
         print(build(force="--force" in sys.argv, verbose=True))
+        print(build_fast(force="--force" in sys.argv))

@@ -408,8 +408,7 @@ class PairChannel:
                       spec.group, self.Q, int(spec.layerwise), self.flags.ptr, self.peer_flags,
                       queue, self.slot_bytes, self.ctl.ptr, ctypes.byref(h))
             self._pair = h.value
-            L = _lib.load()
-            self._pair_send, self._pair_recv = L.kvx_pair_send, L.kvx_pair_recv
+            self._pair_send, self._pair_recv = _pair_calls()
             # the front-end slot gate, or (latency mode) K1s chained with PDL
             # that wait for the slot in-kernel
             self._send_flags = (_lib.KVX_PAIR_GATE if spec.gate_send else
@@ -960,6 +959,20 @@ class PairChannel:
         if self.ctl is not None:
             self.ctl.free()
             self.ctl = None
+
+
+def _pair_calls():
+    """(send, recv) callables for kvx_pair_send / kvx_pair_recv: the CPython
+    fast-call shims (csrc/kvx_fast.c) bound to the loaded library, or its
+    ctypes functions when the shim is not built.  Same library, same calls."""
+    L = _lib.load()
+    try:
+        from . import _kvx_fast
+    except ImportError:
+        return L.kvx_pair_send, L.kvx_pair_recv
+    _kvx_fast.bind(ctypes.cast(L.kvx_pair_send, ctypes.c_void_p).value,
+                   ctypes.cast(L.kvx_pair_recv, ctypes.c_void_p).value)
+    return _kvx_fast.pair_send, _kvx_fast.pair_recv
 
 
 try:  # the caller's current stream as a raw cudaStream_t (no torch.cuda.Stream object)
