@@ -235,8 +235,13 @@ int kvx_quant_pack_kivi_signal(const void* k_src, const void* v_src, int64_t src
  * ready_value -- K groups on ready_flags[chunk], V rows (and, after them,
  * the residual rows) on ready_flags[KVX_KIVI_V_FLAGS + chunk], the layout
  * kvx_quant_pack_kivi_signal rings -- so ONE call consumes a whole hand-off
- * while the prefill side is still publishing it; the caller releases the
- * queue slot after the call (stream order).  With flags, shapes that cannot be bulk-staged return
+ * while the prefill side is still publishing it.  done_counter /
+ * peer_free_flag (nullable, together; only with ready_flags and no residual
+ * rows): the V kernel's last CTA frees the queue slot in-kernel as in
+ * kvx_pull_dequant_scatter_paged; otherwise the caller releases the slot
+ * after the call (stream order).  flags: KVX_PULL_PDL launches both pulls
+ * with programmatic dependent launch (each one's producer streams while the
+ * stream's previous kernel drains).  With flags, shapes that cannot be bulk-staged return
  * KVX_ERR_UNSUPPORTED.  ctl as for kvx_quant_pack_signal.
  * 8-bit: seg_offsets[4] (V codes) and payload_layer_stride must be 32-byte
  * multiples (32-byte vector accesses). */
@@ -248,7 +253,9 @@ int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_lay
                                         int head_dim, int group, int bits, void* k_cache,
                                         void* v_cache, int64_t dst_layer_stride,
                                         const void* ready_flags, uint32_t ready_value,
-                                        int layers_per_chunk, void* ctl, void* stream);
+                                        int layers_per_chunk, void* done_counter,
+                                        void* peer_free_flag, void* ctl, int flags,
+                                        void* stream);
 
 /* Packed payload sizes in bytes for n_rows rows (codes, scale, zero). */
 int kvx_packed_sizes(int64_t n_rows, int head_dim, int group, int bits, int64_t* codes_bytes,

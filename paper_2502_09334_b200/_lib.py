@@ -47,7 +47,8 @@ SIGNATURES = {
     "kvx_dequant_scatter_paged_kivi": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _I, _I,
                                        _I, _I, _P, _P, _I64, _P],
     "kvx_pull_dequant_scatter_paged_kivi": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _I,
-                                            _I, _I, _I, _P, _P, _I64, _P, _U32, _I, _P, _P],
+                                            _I, _I, _I, _P, _P, _I64, _P, _U32, _I, _P, _P, _P,
+                                            _I, _P],
     "kvx_packed_sizes": [_I64, _I, _I, _I, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                          ctypes.POINTER(_I64)],
     "kvx_enable_peer": [_I, _I],

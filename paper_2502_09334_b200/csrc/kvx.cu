@@ -546,7 +546,8 @@ template <int BITS, int G>
 cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, void* kc,
                               int64_t dst_ls_b, cudaStream_t s, bool* ok,
                               const uint32_t* ready = nullptr, uint32_t ready_value = 0,
-                              int layers_per_chunk = 1, kvx::Ctl* ctl = nullptr) {
+                              int layers_per_chunk = 1, kvx::Ctl* ctl = nullptr,
+                              bool pdl = false) {
   *ok = false;
   constexpr int kStages = 4;
   kvx::KchanBulk kb;
@@ -579,8 +580,17 @@ cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, voi
   if (grid > kb.n_spans) grid = kb.n_spans;
   if (grid < 1) return cudaSuccess;
   *ok = true;
-  k<<<unsigned(grid), kBulkThreads, smem, s>>>(kg, kb, slots, static_cast<char*>(kc), dst_ls_b);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kBulkThreads);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, kg, kb, slots, static_cast<char*>(kc), dst_ls_b);
 }
 
 }  // namespace
@@ -919,7 +929,8 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
                         int64_t n_tokens, int n_heads, int head_dim, int group, int bits,
                         void* k_cache, void* v_cache, int64_t dst_layer_stride, void* stream,
                         bool bulk, const uint32_t* ready = nullptr, uint32_t ready_value = 0,
-                        int layers_per_chunk = 1, kvx::Ctl* ctl = nullptr) {
+                        int layers_per_chunk = 1, kvx::Ctl* ctl = nullptr,
+                        const PullDone& done = PullDone(), bool pdl = false) {
   int rc = kivi_check(head_dim, group, bits);
   if (rc) return rc;
   if (n_layers < 0 || n_tokens < 0 || n_heads <= 0 || n_groups < 0 || n_residual < 0 ||
@@ -952,12 +963,12 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
       const int lpc = layers_per_chunk;
       if (bits == 4)
         e = group == 32
-                ? launch_kchan_pull<4, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl)
-                : launch_kchan_pull<4, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl);
+                ? launch_kchan_pull<4, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl, pdl)
+                : launch_kchan_pull<4, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl, pdl);
       else
         e = group == 32
-                ? launch_kchan_pull<8, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl)
-                : launch_kchan_pull<8, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl);
+                ? launch_kchan_pull<8, 32>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl, pdl)
+                : launch_kchan_pull<8, 64>(kg, dst_slots, k_cache, dls, s, &ok, ready, ready_value, lpc, ctl, pdl);
       if (e != cudaSuccess) return e;
       if (!ok && ready) return KVX_ERR_UNSUPPORTED;  // per-lane kernels cannot wait in-kernel
     }
@@ -979,12 +990,14 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
     const char *vc = base + seg_offsets[4], *vs = base + seg_offsets[5], *vz = base + seg_offsets[6];
     bool ok = false;
     if (bulk && aligned(v_cache, 32) && g.plane_row_b % 32 == 0) {
-      PullDone pd;  // no in-kernel completion: the caller releases the slot after this call
+      // in-kernel slot release only without residual rows (they are read
+      // after this kernel); otherwise the caller releases the slot after the call
+      PullDone pd = n_residual ? PullDone() : done;
       const uint32_t* vready = ready ? ready + KVX_KIVI_V_FLAGS : nullptr;
       e = bits == 4 ? dispatch_pull<4>(group, g, vc, vs, vz, s, &ok, vready, ready_value,
-                                       layers_per_chunk, pd, ctl, false)
+                                       layers_per_chunk, pd, ctl, pdl)
                     : dispatch_pull<8>(group, g, vc, vs, vz, s, &ok, vready, ready_value,
-                                       layers_per_chunk, pd, ctl, false);
+                                       layers_per_chunk, pd, ctl, pdl);
       if (e != cudaSuccess) return e;
     }
     if (!ok && ready) return KVX_ERR_UNSUPPORTED;  // per-lane kernels cannot wait in-kernel
@@ -1029,14 +1042,24 @@ int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_lay
                                         int head_dim, int group, int bits, void* k_cache,
                                         void* v_cache, int64_t dst_layer_stride,
                                         const void* ready_flags, uint32_t ready_value,
-                                        int layers_per_chunk, void* ctl, void* stream) {
-  if ((ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) || !aligned(ctl, 8))
+                                        int layers_per_chunk, void* done_counter,
+                                        void* peer_free_flag, void* ctl, int flags,
+                                        void* stream) {
+  if ((ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) || !aligned(ctl, 8) ||
+      (flags & ~KVX_PULL_PDL))
     return KVX_ERR_INVALID_ARG;
+  if ((done_counter != nullptr) != (peer_free_flag != nullptr) ||
+      (done_counter && (!ready_flags || n_residual || !aligned(done_counter, 4) ||
+                        !aligned(peer_free_flag, 4))))
+    return KVX_ERR_INVALID_ARG;
+  PullDone done;
+  done.done_counter = static_cast<uint32_t*>(done_counter);
+  done.peer_free = static_cast<uint32_t*>(peer_free_flag);
   return kivi_dequant(payload, payload_layer_stride, seg_offsets, dst_slots, group_starts,
                       n_groups, residual_dst_slots, n_residual, n_layers, n_tokens, n_heads,
                       head_dim, group, bits, k_cache, v_cache, dst_layer_stride, stream, true,
                       static_cast<const uint32_t*>(ready_flags), ready_value, layers_per_chunk,
-                      static_cast<kvx::Ctl*>(ctl));
+                      static_cast<kvx::Ctl*>(ctl), done, (flags & KVX_PULL_PDL) != 0);
 }
 
 // ---- transport -------------------------------------------------------------

@@ -358,8 +358,12 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
         bulk_g2s(buf + G * code_slice + 2 * S, g.zero + layer * g.payload_ls + meta, mb,
                  &full[st]);
       }
+      // PDL (launched behind the previous hand-off's pull): every span of this
+      // CTA is requested, the stream's next kernel may be scheduled
+      pdl_launch_dependents();
     }
   } else {  // ---- consumers
+    pdl_wait();  // the slot mapping, group starts and the cache are stream-ordered
     const int nck = S / 32;           // 32-channel chunks per full slab
     const int c = threadIdx.x % nck;  // this thread's chunk (fixed across spans)
     const int jstep = (CONSUMERS * 32) / nck;

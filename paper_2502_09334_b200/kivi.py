@@ -165,8 +165,8 @@ def decompress_kivi_into_paged(packed: PackedKiviKV, k_cache: torch.Tensor, v_ca
             lay.n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, v,
             dst.layer_stride)
     if bulk:
-        _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args, None, 0, 1, None,
-                  _stream_ptr(stream))
+        _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args, None, 0, 1, None, None, None,
+                  0, _stream_ptr(stream))
     else:
         _lib.call("kvx_dequant_scatter_paged_kivi", *args, _stream_ptr(stream))
     if stream is not None:  # temporaries were allocated on the current stream

@@ -852,8 +852,8 @@ class PairChannel:
             host = torch.from_numpy(np.concatenate([gs, rt]).astype(np.int64)).pin_memory()
             with torch.cuda.stream(stream):
                 dev = host.to(self.device, non_blocking=True)
-            dev.record_stream(stream)
-            hit = (dev[:len(gs)], dev[len(gs):], host)
+            hit = (dev[:len(gs)], dev[len(gs):], host, dev)
+        hit[3].record_stream(stream)  # (re)used on this stream: not freed under it
         cache[key] = hit  # most recently used last
         return hit[0], hit[1]
 
@@ -863,8 +863,7 @@ class PairChannel:
         doorbells from inside the kernels (kvx_quant_pack_kivi_signal); the
         launches are held in the GPU front-end until the queue slot is free."""
         lay, gs, rt, chunks, lpc, h, v = self._kivi_common(n_tokens, seqlens, e)
-        s, cur = self.stream, torch.cuda.current_stream(self.device)
-        s.wait_stream(cur)
+        s = torch.cuda.current_stream(self.device)
         gs_d, rt_d = self._kivi_index(gs, rt, s)
         base = self.k1_target + self._half(e)
         offs = (ctypes.c_int64 * 7)(*lay.offsets)
@@ -880,43 +879,50 @@ class PairChannel:
                   base, lay.layer_stride, offs, self._kivi_cnt[h].data_ptr(),
                   self._pready(self.peer_flags, h, 0), lpc, v,
                   self._pfree(self.flags.ptr, h) if v > 1 else None, v - 1, self.ctl.ptr,
-                  _stream_ptr(s))
+                  s.cuda_stream)
         _kernel_events_end(ev, s)
-        cur.wait_stream(s)
 
     def _recv_kivi(self, dst, n_tokens, seqlens, e, timing=None):
+        """Kivi decode side on the caller's stream: the K (per-channel) and V
+        bulk pulls, chained with programmatic dependent launch behind the
+        previous hand-off's pull, each waiting in-kernel for its doorbells;
+        without residual rows the V pull's last CTA frees the queue slot
+        (no stream memop between hand-offs)."""
         lay, gs, rt, chunks, lpc, h, v = self._kivi_common(n_tokens, seqlens, e)
-        s, cur = self.stream, torch.cuda.current_stream(self.device)
-        s.wait_stream(cur)
-        gs_d, rt_d = self._kivi_index(gs, rt, s)
-        with torch.cuda.stream(s):
-            rdst = dst.slots[rt_d].contiguous()
+        cur = torch.cuda.current_stream(self.device)
+        gs_d, rt_d = self._kivi_index(gs, rt, cur)
+        rdst = dst.slots[rt_d].contiguous() if len(rt) else None
         base = self.k3_source + self._half(e)
         offs = (ctypes.c_int64 * 7)(*lay.offsets)
+        cs = cur.cuda_stream
 
         def args(l0, l1):
             k, vv = dst.ptrs(l0)
             return (base + l0 * lay.layer_stride, lay.layer_stride, offs, dst.slots_ptr,
                     gs_d.data_ptr() if len(gs) else None, len(gs),
-                    rdst.data_ptr() if rdst.numel() else None, rdst.numel(), l1 - l0,
+                    rdst.data_ptr() if rdst is not None else None, len(rt), l1 - l0,
                     n_tokens, lay.n_heads, lay.head_dim, lay.group, lay.bits, k, vv,
                     dst.layer_stride)
 
         if self.spec.mode == "pull":
             # TMA bulk-staged kernels over the whole hand-off, waiting in-kernel
-            # for each chunk's doorbell (a handful of launches per hand-off)
-            ev = _kernel_events(timing, s, "k3")
+            # for each chunk's doorbell
+            ev = _kernel_events(timing, cur, "k3")
+            release = not len(rt)
             _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args(0, lay.n_layers),
-                      self._pready(self.flags.ptr, h, 0), v, lpc, self.ctl.ptr, _stream_ptr(s))
-            _kernel_events_end(ev, s)
+                      self._pready(self.flags.ptr, h, 0), v, lpc,
+                      self._done_counter(h) if release else None,
+                      self._pfree(self.peer_flags, h) if release else None, self.ctl.ptr,
+                      _lib.KVX_PULL_PDL if self.spec.pdl else 0, cs)
+            _kernel_events_end(ev, cur)
+            if not release:
+                signal(self._pfree(self.peer_flags, h), v, cur)
         else:  # "pull_ldg": per-chunk stream waits, per-lane peer loads
             for c, (l0, l1) in enumerate(chunks):
                 # the chunk's V doorbell publishes all of it (K, residual, V)
-                wait(self._pready(self.flags.ptr, h, _lib.KVX_KIVI_V_FLAGS + c), v, s)
-                _lib.call("kvx_dequant_scatter_paged_kivi", *args(l0, l1), _stream_ptr(s))
-        signal(self._pfree(self.peer_flags, h), v, s)
-        rdst.record_stream(s)
-        cur.wait_stream(s)
+                wait(self._pready(self.flags.ptr, h, _lib.KVX_KIVI_V_FLAGS + c), v, cur)
+                _lib.call("kvx_dequant_scatter_paged_kivi", *args(l0, l1), cs)
+            signal(self._pfree(self.peer_flags, h), v, cur)
 
     # flags of the push / copy / nccl modes: slot c = "chunk c of epoch e
     # ready" (written by P into D's flags); slot FLAG_SLOTS//2 + c = "chunk c

@@ -150,7 +150,8 @@ def test_fused_and_kivi_entry_points_validate(lib):
     offs = (ctypes.c_int64 * 7)(*([0] * 7))
     for fn in ("kvx_dequant_scatter_paged_kivi", "kvx_pull_dequant_scatter_paged_kivi"):
         f = getattr(lib, fn)
-        tail = (None,) if fn.startswith("kvx_dequant") else (None, 0, 1, None, None)
+        tail = ((None,) if fn.startswith("kvx_dequant") else
+                (None, 0, 1, None, None, None, 0, None))
         # kivi: bits 2 and group 128 are not kivi formats
         assert f(256, 256, offs, 256, None, 0, None, 0, 1, 1, 1, 128, 32, 2, 256, 256, 0,
                  *tail) == E
@@ -162,7 +163,17 @@ def test_fused_and_kivi_entry_points_validate(lib):
     # the pull variant's doorbells must be aligned
     assert lib.kvx_pull_dequant_scatter_paged_kivi(256, 256, offs, 256, None, 0, None, 0, 1, 32,
                                                    1, 128, 32, 4, 256, 256, 0, 258, 1, 1, None,
-                                                   None) == E
+                                                   None, None, 0, None) == E
+    # in-kernel slot release needs doorbells, both pointers, and no residual rows
+    assert lib.kvx_pull_dequant_scatter_paged_kivi(256, 256, offs, 256, None, 0, None, 0, 1, 32,
+                                                   1, 128, 32, 4, 256, 256, 0, None, 1, 1, 256,
+                                                   256, None, 0, None) == E
+    assert lib.kvx_pull_dequant_scatter_paged_kivi(256, 256, offs, 256, None, 0, 256, 1, 1, 32,
+                                                   1, 128, 32, 4, 256, 256, 0, 256, 1, 1, 256,
+                                                   256, None, 0, None) == E
+    assert lib.kvx_pull_dequant_scatter_paged_kivi(256, 256, offs, 256, None, 0, None, 0, 1, 32,
+                                                   1, 128, 32, 4, 256, 256, 0, 256, 1, 1, None,
+                                                   None, None, 4, None) == E  # flags
 
 
 def test_8bit_payload_stride_must_keep_32_byte_alignment(lib):
