@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <map>
@@ -209,9 +210,83 @@ struct SignalReq {
   bool pdl = false;  // programmatic dependent launch behind the stream's previous kernel
 };
 
+#ifndef KVX_K1_BULK
+#define KVX_K1_BULK 0  // K1 with TMA-staged source rows (A/B: -DKVX_K1_BULK=1)
+#endif
+#ifndef KVX_K1B_STAGES
+#define KVX_K1B_STAGES 4
+#endif
+#ifndef KVX_K1B_STAGE_BYTES
+#define KVX_K1B_STAGE_BYTES 16384
+#endif
+
+// K1-bulk launch (see quant_pack_bulk_kernel); *ok = false: shape not staged.
+template <int BITS, int G>
+cudaError_t launch_quant_bulk(const kvx::Geo& g, void* codes, void* scale, void* zero,
+                              cudaStream_t s, const SignalReq& rq, bool* ok) {
+  *ok = false;
+  constexpr int kStages = KVX_K1B_STAGES;
+  const int row_bytes = g.row_elems * 2;
+  if (g.n_tokens < 1 || g.row_elems % 32 || row_bytes > KVX_K1B_STAGE_BYTES) return cudaSuccess;
+  kvx::K1BulkGeo kb;
+  int64_t r = KVX_K1B_STAGE_BYTES / row_bytes;
+  if (r > g.n_tokens) r = g.n_tokens;
+  kb.rows_per_span = int(r);
+  kb.spans_per_plane = int((g.n_tokens + r - 1) / r);
+  const int64_t n_layers = g.n_token_rows / (int64_t(g.planes) * g.n_tokens);
+  const int64_t n_spans = n_layers * g.planes * kb.spans_per_plane;
+  if (n_spans >= (int64_t(1) << 31)) return cudaSuccess;
+  kb.n_spans = uint32_t(n_spans);
+  kb.row_bytes = row_bytes;
+  kb.stage_bytes = kb.rows_per_span * row_bytes;
+  kb.cpr = g.row_elems / 32;
+  kb.contiguous = (g.slots == nullptr && g.plane_row_b == row_bytes) ? 1 : 0;
+  kb.spans_per_chunk = uint32_t(int64_t(rq.layers_per_chunk > 0 ? rq.layers_per_chunk : 1) *
+                                g.planes * kb.spans_per_plane);
+  kvx::SignalGeo sig = {};
+  sig.counters = rq.counters;
+  sig.peer_flags = rq.peer_flags;
+  sig.ready_value = rq.ready_value;
+  sig.free_flag = rq.free_flag;
+  sig.free_value = rq.free_value;
+  sig.ctl = rq.ctl;
+#ifdef KVX_TRACE
+  sig.trace_id = g_trace_epoch;
+#endif
+  if (rq.peer_flags && (n_spans + kb.spans_per_chunk - 1) / kb.spans_per_chunk > kvx::kMaxSignalChunks)
+    return cudaErrorInvalidValue;
+  const int smem = kStages * kb.stage_bytes;
+  auto k = kvx::quant_pack_bulk_kernel<BITS, G, kStages>;
+  cudaError_t attr = ensure_smem_attr(k, kStages * KVX_K1B_STAGE_BYTES);
+  if (attr != cudaSuccess) return attr;
+  constexpr int kThreadsB = 288;  // 8 consumer warps + the producer warp
+  int per_sm = blocks_per_sm(k, kThreadsB, smem);
+  int64_t grid = int64_t(sm_count(current_device())) * (per_sm > 0 ? per_sm : 1);
+  if (grid > n_spans) grid = n_spans;
+  *ok = true;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kThreadsB);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = rq.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, g, kb, static_cast<uint8_t*>(codes),
+                            static_cast<__half*>(scale), static_cast<__half*>(zero), sig);
+}
+
 template <int BITS, int G>
 cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero, cudaStream_t s,
                          const SignalReq& rq = SignalReq()) {
+  static const bool bulk = KVX_K1_BULK || std::getenv("KVX_K1_BULK") != nullptr;
+  if (bulk) {
+    bool ok = false;
+    cudaError_t e = launch_quant_bulk<BITS, G>(g, codes, scale, zero, s, rq, &ok);
+    if (e != cudaSuccess || ok) return e;
+  }
   kvx::ItemGeo ig;
   cudaError_t e = make_items(g, ig);
   if (e != cudaSuccess) return e;

@@ -328,8 +328,48 @@ __device__ __forceinline__ K1Item k1_item(const Geo& g, const ItemGeo& ig, uint3
   return it;
 }
 
-template <int BITS, int G>
-__device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)[16], int lane) {
+// Packed codes of a lane whose four 16-byte source pieces were loaded in the
+// rotated order j -> (j + rot) & 3 (K1-bulk's conflict-free shared-memory
+// reads): min/max and the per-element rounding are order-free, only the code
+// positions are not -- move code piece (m - rot) & 3 to piece m.
+template <int BITS>
+__device__ __forceinline__ void unrotate_codes(Chunk32<BITS>& c, int rot) {
+  if constexpr (BITS == 2) {  // 16 bits of codes per piece, two pieces per word
+    uint64_t v = (uint64_t(c.w[1]) << 32) | c.w[0];
+    const int sh = 16 * rot;
+    v = sh ? (v << sh) | (v >> (64 - sh)) : v;
+    c.w[0] = uint32_t(v);
+    c.w[1] = uint32_t(v >> 32);
+  } else {
+    constexpr int WP = BITS / 4 * 1;  // words per piece: 1 at 4-bit, 2 at 8-bit
+    uint32_t t[4 * WP];
+#pragma unroll
+    for (int i = 0; i < 4 * WP; ++i) t[i] = c.w[i];
+    if (rot & 2) {
+#pragma unroll
+      for (int i = 0; i < 2 * WP; ++i) {
+        const uint32_t a = t[i];
+        t[i] = t[i + 2 * WP];
+        t[i + 2 * WP] = a;
+      }
+    }
+    if (rot & 1) {  // (p0, p1, p2, p3) -> (p3, p0, p1, p2)
+      uint32_t last[WP];
+#pragma unroll
+      for (int i = 0; i < WP; ++i) last[i] = t[3 * WP + i];
+#pragma unroll
+      for (int i = 4 * WP - 1; i >= WP; --i) t[i] = t[i - WP];
+#pragma unroll
+      for (int i = 0; i < WP; ++i) t[i] = last[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 4 * WP; ++i) c.w[i] = t[i];
+  }
+}
+
+template <int BITS, int G, bool ROT = false>
+__device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)[16], int lane,
+                                           int rot = 0) {
   constexpr int LPG = G / 32;
   constexpr float QMAXF = float((1 << BITS) - 1);
   constexpr uint32_t QMAX = (1u << BITS) - 1u;
@@ -369,7 +409,8 @@ __device__ __forceinline__ void k1_process(const K1Item& it, const uint32_t (&w)
 #pragma unroll
     for (int i = 0; i < 32; ++i) b[i] = min(b[i] - 0x4B000000u, QMAX);
   }
-  const Chunk32<BITS> out = pack32<BITS>(b);
+  Chunk32<BITS> out = pack32<BITS>(b);
+  if constexpr (ROT) unrotate_codes<BITS>(out, rot);
   if (it.active) {
     store_chunk<BITS>(it.codes, out);
     if ((lane & (LPG - 1)) == 0) {
@@ -1256,6 +1297,154 @@ __global__ void __launch_bounds__(288, 1) pull_many_kernel(Geo g, const __grid_c
                        "r"(pm.part[j].ready_value)
                        : "memory");
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1-bulk: quantise + pack with the source rows staged by TMA.  One producer
+// thread per CTA streams spans (R consecutive token rows of one (layer,
+// K|V) plane; one cp.async.bulk per row, or one for the span when the rows
+// are contiguous) into a STAGES-deep shared-memory ring; eight consumer
+// warps quantise out of shared memory (each lane's 64-byte chunk read as
+// four 16-byte loads in a bank-conflict-free rotated order) with the same
+// arithmetic as K1 (k1_process).  The bytes in flight per SM are bounded by
+// the ring, not by registers: K1's register prefetch holds ~64 KB per SM at
+// 122 registers; the ring holds 2 CTAs x STAGES x ~16 KB.  Same doorbell
+// contract as K1 (SignalGeo): per-chunk arrivals per CTA (spans are
+// CTA-strided: owners of chunk c's spans = min(#spans, gridDim.x)).
+// ---------------------------------------------------------------------------
+struct K1BulkGeo {
+  int rows_per_span;     // R
+  int spans_per_plane;   // ceil(T / R)
+  uint32_t n_spans;      // n_layers * planes * spans_per_plane
+  int row_bytes;         // source bytes of one token row (n_heads * head_dim * 2)
+  int stage_bytes;       // R * row_bytes
+  int cpr;               // 32-element chunks per row
+  int contiguous;        // 1: a span's rows are one contiguous source range
+  uint32_t spans_per_chunk;  // spans of one doorbell chunk (signal path)
+};
+
+template <int BITS, int G, int STAGES>
+__global__ void __launch_bounds__(288, 2) quant_pack_bulk_kernel(Geo g, K1BulkGeo kb,
+                                                                 uint8_t* __restrict__ codes,
+                                                                 __half* __restrict__ scale,
+                                                                 __half* __restrict__ zero,
+                                                                 SignalGeo sig) {
+  constexpr int CONSUMERS = 8;
+  constexpr int CB = 32 * BITS / 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ uint32_t s_go;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_go = 1u;
+  }
+  pdl_wait();  // PDL launches: the stream's previous grid and its memory first
+  if (sig.peer_flags && threadIdx.x == 0 && sig.free_flag)
+    s_go = spin_until_geq(sig.free_flag, sig.free_value, sig.ctl) ? 1u : 0u;
+  __syncthreads();
+  if (!s_go) return;  // aborted / timed out before anything was stored
+  const int64_t T = g.n_tokens;
+  if (warp == CONSUMERS) {  // ---- producer
+    if (lane == 0) {
+      uint32_t k = 0;
+      for (uint32_t sp = blockIdx.x; sp < kb.n_spans; sp += gridDim.x, ++k) {
+        const int st = k % STAGES;
+        if (k >= STAGES) mbar_wait(&empty[st], ((k / STAGES) & 1) ^ 1);
+        const uint32_t lp = sp / kb.spans_per_plane;  // layer * planes + plane
+        const uint32_t layer = lp / g.planes;
+        const int kv = g.plane0 + int(lp - layer * g.planes);
+        const int64_t t0 = int64_t(sp - lp * kb.spans_per_plane) * kb.rows_per_span;
+        const int rows = int(min(int64_t(kb.rows_per_span), T - t0));
+        uint8_t* buf = smem + st * kb.stage_bytes;
+        mbar_expect_tx(&full[st], uint32_t(rows) * kb.row_bytes);
+        const char* plane = plane_ptr(g, kv, layer);
+        if (kb.contiguous) {
+          bulk_g2s(buf, row_ptr(g, plane, t0), uint32_t(rows) * kb.row_bytes, &full[st]);
+        } else {
+          for (int r = 0; r < rows; ++r)
+            bulk_g2s(buf + r * kb.row_bytes, row_ptr(g, plane, pos_of(g, t0 + r)), kb.row_bytes,
+                     &full[st]);
+        }
+      }
+    }
+  } else {  // ---- consumers
+    const int cpr = kb.cpr;
+    const int rpw = cpr < 32 ? 32 / cpr : 1;  // rows per warp pass (short rows)
+    const int sub = rpw > 1 ? lane / cpr : 0;
+    const int cl = rpw > 1 ? lane % cpr : lane;
+    const int blocks = rpw > 1 ? 1 : (cpr + 31) / 32;
+    const int rot = (lane >> 1) & 3;  // rotated 16-byte order: conflict-free LDS.128
+    uint32_t k = 0;
+    for (uint32_t sp = blockIdx.x; sp < kb.n_spans; sp += gridDim.x, ++k) {
+      const int st = k % STAGES;
+      const uint32_t lp = sp / kb.spans_per_plane;
+      const uint32_t layer = lp / g.planes;
+      const int p = int(lp - layer * g.planes);
+      const int64_t t0 = int64_t(sp - lp * kb.spans_per_plane) * kb.rows_per_span;
+      const int rows = int(min(int64_t(kb.rows_per_span), T - t0));
+      const uint8_t* buf = smem + st * kb.stage_bytes;
+      mbar_wait(&full[st], (k / STAGES) & 1);
+      char* lcodes = reinterpret_cast<char*>(codes) + int64_t(layer) * g.codes_ls;
+      char* lscale = reinterpret_cast<char*>(scale) + int64_t(layer) * g.meta_ls;
+      char* lzero = reinterpret_cast<char*>(zero) + int64_t(layer) * g.meta_ls;
+      const int n_items = ((rows + rpw - 1) / rpw) * blocks;
+      for (int it_i = warp; it_i < n_items; it_i += CONSUMERS) {
+        const int rb = it_i / blocks;
+        const int r = rb * rpw + sub;
+        const int c = (it_i - rb * blocks) * 32 + cl;
+        K1Item it;
+        it.active = r < rows && c < cpr;
+        const int rr = it.active ? r : 0, cc = it.active ? c : 0;
+        const uint8_t* src = buf + rr * kb.row_bytes + cc * 64;
+        uint32_t w[16];  // piece j holds source piece (j + rot) & 3
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint4 v = *reinterpret_cast<const uint4*>(src + ((j + rot) & 3) * 16);
+          w[4 * j] = v.x;
+          w[4 * j + 1] = v.y;
+          w[4 * j + 2] = v.z;
+          w[4 * j + 3] = v.w;
+        }
+        const int64_t lrow = int64_t(p) * T + t0 + rr;
+        it.src = nullptr;
+        it.codes = lcodes + (lrow * cpr + cc) * CB;
+        const int64_t gi = (lrow * cpr + cc) * 32 / G;
+        it.scale = reinterpret_cast<__half*>(lscale) + gi;
+        it.zero = reinterpret_cast<__half*>(lzero) + gi;
+        k1_process<BITS, G, true>(it, w, lane, rot);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (sig.peer_flags) {  // this CTA's share of a doorbell chunk is done
+        const uint32_t c = sp / kb.spans_per_chunk;
+        const uint32_t nxt = sp + gridDim.x;
+        if (nxt >= kb.n_spans || nxt / kb.spans_per_chunk != c) {
+          __threadfence();  // this thread's payload stores, device-wide
+          asm volatile("bar.sync 1, %0;" ::"r"(CONSUMERS * 32) : "memory");
+          if (threadIdx.x == 0) {
+            const uint32_t a = c * kb.spans_per_chunk;
+            const uint32_t b = min(kb.n_spans, a + kb.spans_per_chunk);
+            const uint32_t owners = min(b - a, gridDim.x);
+            __threadfence();
+            if (atomicAdd(sig.counters + c, 1u) + 1 == owners) {
+              sig.counters[c] = 0u;
+              asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags + c),
+                           "r"(sig.ready_value)
+                           : "memory");
+            }
+          }
+        }
+      }
+    }
+    // every consumer of this CTA is done with its spans: the stream's next
+    // kernel may be scheduled (PDL; it waits for this grid before reading)
+    pdl_launch_dependents();
   }
 }
 
