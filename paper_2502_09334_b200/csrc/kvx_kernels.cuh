@@ -1380,6 +1380,12 @@ __global__ void __launch_bounds__(288, 2) quant_pack_bulk_kernel(Geo g, K1BulkGe
     const int cl = rpw > 1 ? lane % cpr : lane;
     const int blocks = rpw > 1 ? 1 : (cpr + 31) / 32;
     const int rot = (lane >> 1) & 3;  // rotated 16-byte order: conflict-free LDS.128
+    // this warp's first (row group, 32-chunk block) inside a span, and the
+    // per-step advance of CONSUMERS items, precomputed once
+    const int rb0 = warp / blocks, blk0 = warp - rb0 * blocks;
+    const int drb = CONSUMERS / blocks, dblk = CONSUMERS - drb * blocks;
+    const uint32_t code_row = uint32_t(cpr) * CB;      // code bytes per payload row
+    const uint32_t meta_row = uint32_t(cpr) * 32 / G;  // groups per payload row
     uint32_t k = 0;
     for (uint32_t sp = blockIdx.x; sp < kb.n_spans; sp += gridDim.x, ++k) {
       const int st = k % STAGES;
@@ -1389,15 +1395,18 @@ __global__ void __launch_bounds__(288, 2) quant_pack_bulk_kernel(Geo g, K1BulkGe
       const int64_t t0 = int64_t(sp - lp * kb.spans_per_plane) * kb.rows_per_span;
       const int rows = int(min(int64_t(kb.rows_per_span), T - t0));
       const uint8_t* buf = smem + st * kb.stage_bytes;
+      // payload row of the span's first token row
+      const int64_t lrow0 = int64_t(p) * T + t0;
+      char* ccodes = reinterpret_cast<char*>(codes) + int64_t(layer) * g.codes_ls +
+                     lrow0 * code_row;
+      __half* cscale = reinterpret_cast<__half*>(reinterpret_cast<char*>(scale) +
+                                                 int64_t(layer) * g.meta_ls) + lrow0 * meta_row;
+      __half* czero = reinterpret_cast<__half*>(reinterpret_cast<char*>(zero) +
+                                                int64_t(layer) * g.meta_ls) + lrow0 * meta_row;
       mbar_wait(&full[st], (k / STAGES) & 1);
-      char* lcodes = reinterpret_cast<char*>(codes) + int64_t(layer) * g.codes_ls;
-      char* lscale = reinterpret_cast<char*>(scale) + int64_t(layer) * g.meta_ls;
-      char* lzero = reinterpret_cast<char*>(zero) + int64_t(layer) * g.meta_ls;
-      const int n_items = ((rows + rpw - 1) / rpw) * blocks;
-      for (int it_i = warp; it_i < n_items; it_i += CONSUMERS) {
-        const int rb = it_i / blocks;
+      for (int rb = rb0, blk = blk0; rb * rpw < rows;) {
         const int r = rb * rpw + sub;
-        const int c = (it_i - rb * blocks) * 32 + cl;
+        const int c = blk * 32 + cl;
         K1Item it;
         it.active = r < rows && c < cpr;
         const int rr = it.active ? r : 0, cc = it.active ? c : 0;
@@ -1411,13 +1420,18 @@ __global__ void __launch_bounds__(288, 2) quant_pack_bulk_kernel(Geo g, K1BulkGe
           w[4 * j + 2] = v.z;
           w[4 * j + 3] = v.w;
         }
-        const int64_t lrow = int64_t(p) * T + t0 + rr;
         it.src = nullptr;
-        it.codes = lcodes + (lrow * cpr + cc) * CB;
-        const int64_t gi = (lrow * cpr + cc) * 32 / G;
-        it.scale = reinterpret_cast<__half*>(lscale) + gi;
-        it.zero = reinterpret_cast<__half*>(lzero) + gi;
+        it.codes = ccodes + uint32_t(rr) * code_row + uint32_t(cc) * CB;
+        const uint32_t gi = uint32_t(rr) * meta_row + uint32_t(cc) * 32 / G;
+        it.scale = cscale + gi;
+        it.zero = czero + gi;
         k1_process<BITS, G, true>(it, w, lane, rot);
+        rb += drb;
+        blk += dblk;
+        if (blk >= blocks) {
+          blk -= blocks;
+          ++rb;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
