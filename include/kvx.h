@@ -69,6 +69,7 @@ extern "C" {
 #define KVX_ERR_INVALID_ARG 10001  /* ValueError on the Python side         */
 #define KVX_ERR_NO_PATH 10002      /* NoPath: no peer access between GPUs    */
 #define KVX_ERR_UNSUPPORTED 10003  /* stream memory ops etc. unavailable     */
+#define KVX_ERR_NCCL 10004         /* an NCCL call failed                    */
 
 /* Library version (major*10000 + minor*100 + patch). */
 int kvx_version(void);
@@ -385,6 +386,26 @@ int kvx_pair_recv_many(void* pair, uint64_t first_epoch, int count, void* k_cach
                        const int64_t* n_tokens, int plane_heads, int head_offset, int flags,
                        void* stream);
 int kvx_pair_destroy(void* pair);
+
+/* ---- NCCL pair pool ---------------------------
+ * The paper pre-builds NCCL groups for its asynchronous SendRecv hand-offs;
+ * these mirror that for engines that pair GPUs through NCCL (TP-sharded
+ * replicas, or pairings without CUDA IPC).  NCCL is resolved at run time
+ * (the process's already-loaded libnccl.so.2, else the system one):
+ * KVX_ERR_UNSUPPORTED without it, KVX_ERR_NCCL when a call fails.
+ *   kvx_nccl_get_unique_id: 128 opaque bytes (rank 0; the caller broadcasts)
+ *   kvx_nccl_pair_init: ncclCommInitRank (collective over the n_ranks)
+ *   kvx_nccl_sendrecv: ONE ncclGroupStart/End holding a send of send_bytes to
+ *     send_peer and a receive of recv_bytes from recv_peer (a peer < 0 or 0
+ *     bytes skips that half), stream-ordered on `stream` -- e.g. a packed
+ *     payload (kvx_quant_pack) on the prefill rank, the landing buffer of
+ *     kvx_dequant_scatter_paged on the decode rank. */
+int kvx_nccl_unique_id_size(void);
+int kvx_nccl_get_unique_id(void* id_out);
+int kvx_nccl_pair_init(const void* unique_id, int n_ranks, int rank, void** comm_out);
+int kvx_nccl_sendrecv(void* comm, const void* send_buf, size_t send_bytes, int send_peer,
+                      void* recv_buf, size_t recv_bytes, int recv_peer, void* stream);
+int kvx_nccl_pair_destroy(void* comm);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,7 @@ KVX_OK = 0
 KVX_ERR_INVALID_ARG = 10001
 KVX_ERR_NO_PATH = 10002
 KVX_ERR_UNSUPPORTED = 10003
+KVX_ERR_NCCL = 10004
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -73,6 +74,11 @@ SIGNATURES = {
     "kvx_pair_send": [_P, _U64, _P, _P, _I64, _P, _I64, _I, _I, _I, _P],
     "kvx_pair_recv": [_P, _U64, _P, _P, _I64, _P, _I64, _I, _I, _I, _P],
     "kvx_pair_recv_many": [_P, _U64, _I, _P, _P, _I64, _P, _P, _I, _I, _I, _P],
+    "kvx_nccl_unique_id_size": [],
+    "kvx_nccl_get_unique_id": [_P],
+    "kvx_nccl_pair_init": [_P, _I, _I, ctypes.POINTER(_P)],
+    "kvx_nccl_sendrecv": [_P, _P, _SZ, _I, _P, _SZ, _I, _P],
+    "kvx_nccl_pair_destroy": [_P],
     "kvx_pair_destroy": [_P],
 }
 

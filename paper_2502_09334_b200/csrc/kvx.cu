@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the entry points are resolved at run time (dlopen)
+
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -680,6 +683,7 @@ const char* kvx_strerror(int code) {
     case KVX_ERR_INVALID_ARG: return "kvx: invalid argument";
     case KVX_ERR_NO_PATH: return "kvx: no peer path between devices";
     case KVX_ERR_UNSUPPORTED: return "kvx: operation unsupported on this device/driver";
+    case KVX_ERR_NCCL: return "kvx: NCCL call failed";
     default: return cudaGetErrorString(static_cast<cudaError_t>(code));
   }
 }
@@ -1588,6 +1592,102 @@ int kvx_pair_recv_many(void* pair, uint64_t first_epoch, int count, void* k_cach
   }
   if (e != cudaSuccess) return e;
   return ok ? KVX_OK : KVX_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"
+
+// ---- NCCL pair pool ------------------------------------------
+// The paper pre-builds NCCL groups for its async SendRecv hand-offs.  These
+// entry points give a serving engine the same thing through the C-ABI.  NCCL
+// is resolved at run time (dlopen of the libnccl.so.2 already loaded by the
+// process -- torch's -- else the system one), so the library has no link-time
+// NCCL dependency and never mixes two NCCL builds in one process.
+namespace {
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return;
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.send = reinterpret_cast<decltype(api.send)>(dlsym(h, "ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(h, "ncclRecv"));
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+    api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.send && api.recv &&
+             api.group_start && api.group_end;
+  });
+  return api;
+}
+
+int nccl_rc(ncclResult_t r) { return r == ncclSuccess ? KVX_OK : KVX_ERR_NCCL; }
+}  // namespace
+
+extern "C" {
+
+int kvx_nccl_unique_id_size(void) { return int(sizeof(ncclUniqueId)); }
+
+int kvx_nccl_get_unique_id(void* id_out) {
+  if (!id_out) return KVX_ERR_INVALID_ARG;
+  const NcclApi& a = nccl_api();
+  if (!a.ok) return KVX_ERR_UNSUPPORTED;
+  ncclUniqueId id;
+  int rc = nccl_rc(a.get_unique_id(&id));
+  if (rc == KVX_OK) std::memcpy(id_out, &id, sizeof(id));
+  return rc;
+}
+
+int kvx_nccl_pair_init(const void* unique_id, int n_ranks, int rank, void** comm_out) {
+  if (!unique_id || !comm_out || n_ranks < 1 || rank < 0 || rank >= n_ranks)
+    return KVX_ERR_INVALID_ARG;
+  const NcclApi& a = nccl_api();
+  if (!a.ok) return KVX_ERR_UNSUPPORTED;
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  int rc = nccl_rc(a.comm_init_rank(&comm, n_ranks, id, rank));
+  if (rc == KVX_OK) *comm_out = comm;
+  return rc;
+}
+
+int kvx_nccl_sendrecv(void* comm, const void* send_buf, size_t send_bytes, int send_peer,
+                      void* recv_buf, size_t recv_bytes, int recv_peer, void* stream) {
+  if (!comm || (send_peer >= 0 && send_bytes && !send_buf) ||
+      (recv_peer >= 0 && recv_bytes && !recv_buf))
+    return KVX_ERR_INVALID_ARG;
+  const NcclApi& a = nccl_api();
+  if (!a.ok) return KVX_ERR_UNSUPPORTED;
+  auto c = static_cast<ncclComm_t>(comm);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc = nccl_rc(a.group_start());
+  if (rc) return rc;
+  if (send_peer >= 0 && send_bytes)
+    rc = nccl_rc(a.send(send_buf, send_bytes, ncclUint8, send_peer, c, s));
+  if (rc == KVX_OK && recv_peer >= 0 && recv_bytes)
+    rc = nccl_rc(a.recv(recv_buf, recv_bytes, ncclUint8, recv_peer, c, s));
+  const int rc2 = nccl_rc(a.group_end());
+  return rc ? rc : rc2;
+}
+
+int kvx_nccl_pair_destroy(void* comm) {
+  if (!comm) return KVX_OK;
+  const NcclApi& a = nccl_api();
+  if (!a.ok) return KVX_ERR_UNSUPPORTED;
+  return nccl_rc(a.comm_destroy(static_cast<ncclComm_t>(comm)));
 }
 
 }  // extern "C"

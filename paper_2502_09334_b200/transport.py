@@ -371,7 +371,7 @@ class PairChannel:
         self.local_payload = None
         self.slot_bytes = _round_up(spec.capacity_bytes)
         if stage_here:
-            if mode == "nccl":  # NCCL needs a torch tensor
+            if mode == "nccl":  # the NCCL staging buffer (no IPC export needed)
                 t = torch.empty(spec.capacity_bytes, dtype=torch.uint8, device=self.device)
                 self.local_payload = (t, _round_up(t.data_ptr()))
             else:
@@ -381,11 +381,24 @@ class PairChannel:
                 b = IpcBuffer(self.slot_bytes * self.Q + 256)
                 self.local_payload = (b, _round_up(b.ptr))
         mine = {"flags": self.flags.handle()}
+        if mode == "nccl" and self.role == "prefill":
+            # a 2-rank NCCL communicator per pair, built through the C-ABI
+            # (kvx_nccl_*: the paper's pre-built NCCL groups)
+            uid = ctypes.create_string_buffer(_lib.load().kvx_nccl_unique_id_size())
+            _lib.call("kvx_nccl_get_unique_id", uid)
+            mine["nccl_id"] = uid.raw
         if self.local_payload is not None and mode != "nccl":
             mine["payload"] = self.local_payload[0].handle()
             mine["payload_off"] = self.local_payload[1] - self.local_payload[0].ptr
         allv = exchange(mine, control_group)
         theirs = allv[self.peer]
+        self._nccl = None
+        if mode == "nccl":
+            uid = mine["nccl_id"] if self.role == "prefill" else theirs["nccl_id"]
+            comm = ctypes.c_void_p()
+            _lib.call("kvx_nccl_pair_init", ctypes.create_string_buffer(uid, len(uid)), 2,
+                      0 if self.role == "prefill" else 1, ctypes.byref(comm))
+            self._nccl = comm.value
         self.peer_flags = ipc_open(theirs["flags"])
         self.peer_payload = None
         self._peer_payload_map = 0
@@ -567,12 +580,9 @@ class PairChannel:
                 _lib.call("kvx_copy_peer", dst, self.device.index, addr, self.device.index,
                           nbytes, _stream_ptr(cs))
                 signal(self._ready(self.peer_flags, c), e, cs)
-            else:  # nccl
-                import torch.distributed as dist
-                t = self.local_payload[0]
-                off = addr - t.data_ptr()
-                with torch.cuda.stream(cs):
-                    dist.send(t[off:off + nbytes], self.peer, group=self.data_group)
+            else:  # nccl: one ncclSend in a group on the copy stream (kvx_nccl_sendrecv)
+                _lib.call("kvx_nccl_sendrecv", self._nccl, addr, nbytes, 1, None, 0, -1,
+                          _stream_ptr(cs))
             self.comm_done[c].record(cs)
         self._prev_ranges = ranges
         cur.wait_stream(s)
@@ -691,15 +701,12 @@ class PairChannel:
         prev = self._prev_ranges
         for c, (l0, l1) in enumerate(self.chunks):
             if mode == "nccl":
-                import torch.distributed as dist
                 g = self._guard(prev, ranges[c])
                 if g is not None:
                     cs.wait_event(self.k_done[g])  # landing bytes consumed by K3
-                t = self.local_payload[0]
                 addr, nbytes = payload.byte_range(l0, l1)
-                off = addr - t.data_ptr()
-                with torch.cuda.stream(cs):
-                    dist.recv(t[off:off + nbytes], self.peer, group=self.data_group)
+                _lib.call("kvx_nccl_sendrecv", self._nccl, None, 0, -1, addr, nbytes, 0,
+                          _stream_ptr(cs))
                 self.comm_done[c].record(cs)
                 s.wait_event(self.comm_done[c])
             else:
@@ -951,6 +958,9 @@ class PairChannel:
         if self._pair is not None:
             _lib.call("kvx_pair_destroy", self._pair)
             self._pair = None
+        if getattr(self, "_nccl", None):
+            _lib.call("kvx_nccl_pair_destroy", self._nccl)
+            self._nccl = None
         if self.peer_flags:
             _lib.call("kvx_ipc_close", self.peer_flags)
             self.peer_flags = 0

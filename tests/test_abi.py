@@ -226,3 +226,22 @@ def test_pair_entry_points_validate(lib):
     assert lib.kvx_handoff_chunk_plan(80, 16, 8, 128, 1, ctypes.byref(lpc), ctypes.byref(nc)) == 0
     assert (lpc.value, nc.value) == (2, 40)  # layer-wise: <= 64 chunks
     assert lib.kvx_handoff_chunk_plan(0, 16, 8, 128, 0, ctypes.byref(lpc), ctypes.byref(nc)) == E
+
+
+def test_nccl_pool_entry_points(lib):
+    """kvx_nccl_*: the paper's pre-built NCCL groups through the
+    C-ABI.  Argument checks need no GPU; the unique id needs only NCCL's
+    bootstrap (it is resolved at run time, no link-time dependency)."""
+    E = _lib.KVX_ERR_INVALID_ARG
+    assert lib.kvx_nccl_unique_id_size() == 128
+    comm = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(128)
+    assert lib.kvx_nccl_pair_init(None, 2, 0, ctypes.byref(comm)) == E
+    assert lib.kvx_nccl_pair_init(uid, 2, 2, ctypes.byref(comm)) == E
+    assert lib.kvx_nccl_sendrecv(None, None, 0, -1, None, 0, -1, None) == E
+    assert lib.kvx_nccl_sendrecv(256, None, 16, 1, None, 0, -1, None) == E
+    assert lib.kvx_nccl_pair_destroy(None) == 0
+    rc = lib.kvx_nccl_get_unique_id(uid)
+    assert rc in (0, _lib.KVX_ERR_UNSUPPORTED, _lib.KVX_ERR_NCCL)
+    if rc == 0:
+        assert any(uid.raw)
