@@ -213,14 +213,21 @@ struct SignalReq {
   bool pdl = false;  // programmatic dependent launch behind the stream's previous kernel
 };
 
+// K1 with TMA-staged source rows (quant_pack_bulk_kernel) is the default; the
+// register-prefetch K1 remains for rows a stage cannot hold and as the A/B
+// baseline (-DKVX_K1_BULK=0, or KVX_K1_REG=1 at run time).  Stage geometry A/B
+// (N=1 config 2, K1 ms; profiles/r02_k1bulk.md): register K1 1.814; bulk
+// 4 x 16 KB 2.20 (before hoisting) / 1.985, 6 x 8 KB 2.91, 4 x 24 KB 1.773,
+// 3 x 32 KB 1.678, 4 x 32 KB (1 CTA/SM) 2.157, 2 x 40 KB 1.607,
+// 2 x 48 KB 1.600 (2 CTAs/SM: 192 KB of source rows in flight per SM).
 #ifndef KVX_K1_BULK
-#define KVX_K1_BULK 0  // K1 with TMA-staged source rows (A/B: -DKVX_K1_BULK=1)
+#define KVX_K1_BULK 1
 #endif
 #ifndef KVX_K1B_STAGES
-#define KVX_K1B_STAGES 4
+#define KVX_K1B_STAGES 2
 #endif
 #ifndef KVX_K1B_STAGE_BYTES
-#define KVX_K1B_STAGE_BYTES 16384
+#define KVX_K1B_STAGE_BYTES 49152
 #endif
 
 // K1-bulk launch (see quant_pack_bulk_kernel); *ok = false: shape not staged.
@@ -284,7 +291,8 @@ cudaError_t launch_quant_bulk(const kvx::Geo& g, void* codes, void* scale, void*
 template <int BITS, int G>
 cudaError_t launch_quant(const kvx::Geo& g, void* codes, void* scale, void* zero, cudaStream_t s,
                          const SignalReq& rq = SignalReq()) {
-  static const bool bulk = KVX_K1_BULK || std::getenv("KVX_K1_BULK") != nullptr;
+  static const bool bulk = KVX_K1_BULK ? std::getenv("KVX_K1_REG") == nullptr
+                                       : std::getenv("KVX_K1_BULK") != nullptr;
   if (bulk) {
     bool ok = false;
     cudaError_t e = launch_quant_bulk<BITS, G>(g, codes, scale, zero, s, rq, &ok);

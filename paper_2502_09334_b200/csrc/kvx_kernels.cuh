@@ -1375,7 +1375,7 @@ __global__ void __launch_bounds__(288, 2) quant_pack_bulk_kernel(Geo g, K1BulkGe
     }
   } else {  // ---- consumers
     const int cpr = kb.cpr;
-    const int rpw = cpr < 32 ? 32 / cpr : 1;  // rows per warp pass (short rows)
+    const int rpw = (cpr < 32 && 32 % cpr == 0) ? 32 / cpr : 1;  // rows per warp pass
     const int sub = rpw > 1 ? lane / cpr : 0;
     const int cl = rpw > 1 ? lane % cpr : lane;
     const int blocks = rpw > 1 ? 1 : (cpr + 31) / 32;
