@@ -891,10 +891,9 @@ class PairChannel:
 
     def _recv_kivi(self, dst, n_tokens, seqlens, e, timing=None):
         """Kivi decode side on the caller's stream: the K (per-channel) and V
-        bulk pulls, chained with programmatic dependent launch behind the
-        previous hand-off's pull, each waiting in-kernel for its doorbells;
-        without residual rows the V pull's last CTA frees the queue slot
-        (no stream memop between hand-offs)."""
+        bulk pulls, each waiting in-kernel for its doorbells; without residual
+        rows the V pull's last CTA frees the queue slot (no stream memop
+        between hand-offs)."""
         lay, gs, rt, chunks, lpc, h, v = self._kivi_common(n_tokens, seqlens, e)
         cur = torch.cuda.current_stream(self.device)
         gs_d, rt_d = self._kivi_index(gs, rt, cur)
@@ -920,7 +919,8 @@ class PairChannel:
                       self._pready(self.flags.ptr, h, 0), v, lpc,
                       self._done_counter(h) if release else None,
                       self._pfree(self.peer_flags, h) if release else None, self.ctl.ptr,
-                      _lib.KVX_PULL_PDL if self.spec.pdl else 0, cs)
+                      0, cs)  # no PDL: measured slower for the two-kernel kivi pull
+                              # (config 3 2,387 vs 2,484 GB/s; profiles/r02_bench/k1default_n2.log)
             _kernel_events_end(ev, cur)
             if not release:
                 signal(self._pfree(self.peer_flags, h), v, cur)
