@@ -18,11 +18,13 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SO = os.path.join(ROOT, "paper_2502_09334_b200", "_kvx.so")
 KERNELS = {  # label -> mangled-name regex
-    "K1 quant_pack<4,128>": r"quant_pack_kernelILi4ELi128E",
+    "K1-bulk quant_pack_bulk<4,128,2> (default)": r"quant_pack_bulk_kernelILi4ELi128ELi2E",
+    "K1 quant_pack<4,128> (register)": r"quant_pack_kernelILi4ELi128E",
     "K3 dequant_scatter<4,128,paged>": r"dequant_scatter_kernelILi4ELi128ELb1E",
     "K3-bulk pull_dequant_scatter<4,128>": r"pull_dequant_scatter_kernelILi4ELi128ELi4E",
     "kivi K1-kchan quant_pack_kchan<4,32>": r"quant_pack_kchan_kernelILi4ELi32E",
     "kivi pull_kchan<4,32>": r"pull_kchan_kernelILi4ELi32ELi4E",
+    "recv_many pull_many<4,128>": r"pull_many_kernelILi4ELi128ELi4E",
 }
 WATCH = ["LDG.256", "STG.256", "LDG.128", "STG.128", "UBLKCP", "SYNCS", "FFMA2", "FFMA", "HFMA2", "FHADD", "FMNMX", "PRMT", "LOP3", "SHFL",
          "BAR", "LDS", "STS", "UTMALDG", "UTCMMA", "UTCHMMA", "HMMA", "MEMBAR", "RED", "ATOM"]
