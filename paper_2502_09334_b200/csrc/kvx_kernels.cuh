@@ -1102,7 +1102,9 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     }
   } else {
   // ---- consumers: the slot mapping and the cache are stream-ordered inputs
+#ifndef KVX_K3_NO_PDL_WAIT  // A/B only: measures what the stream-order wait costs
   pdl_wait();
+#endif
   uint32_t k = 0;
   for (uint32_t sp = blockIdx.x; sp < bg.n_spans; sp += gridDim.x, ++k) {
     const int st = k % STAGES;
@@ -1345,8 +1347,14 @@ __global__ void __launch_bounds__(288, 2) quant_pack_bulk_kernel(Geo g, K1BulkGe
     s_go = 1u;
   }
   pdl_wait();  // PDL launches: the stream's previous grid and its memory first
+#ifdef KVX_TRACE
+  if (sig.peer_flags && blockIdx.x == 0 && threadIdx.x == 0) KVX_TRACE_STAMP(0, sig.trace_id, 0);
+#endif
   if (sig.peer_flags && threadIdx.x == 0 && sig.free_flag)
     s_go = spin_until_geq(sig.free_flag, sig.free_value, sig.ctl) ? 1u : 0u;
+#ifdef KVX_TRACE
+  if (sig.peer_flags && blockIdx.x == 0 && threadIdx.x == 0) KVX_TRACE_STAMP(0, sig.trace_id, 1);
+#endif
   __syncthreads();
   if (!s_go) return;  // aborted / timed out before anything was stored
   const int64_t T = g.n_tokens;
@@ -1451,6 +1459,9 @@ __global__ void __launch_bounds__(288, 2) quant_pack_bulk_kernel(Geo g, K1BulkGe
               asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.peer_flags + c),
                            "r"(sig.ready_value)
                            : "memory");
+#ifdef KVX_TRACE
+              if (nxt >= kb.n_spans || b >= kb.n_spans) KVX_TRACE_STAMP(0, sig.trace_id, 2);
+#endif
             }
           }
         }
@@ -1459,6 +1470,16 @@ __global__ void __launch_bounds__(288, 2) quant_pack_bulk_kernel(Geo g, K1BulkGe
     // every consumer of this CTA is done with its spans: the stream's next
     // kernel may be scheduled (PDL; it waits for this grid before reading)
     pdl_launch_dependents();
+#ifdef KVX_TRACE
+    if (sig.peer_flags) {  // trace builds: stamp the last CTA's exit
+      asm volatile("bar.sync 1, %0;" ::"r"(CONSUMERS * 32) : "memory");
+      if (threadIdx.x == 0 && atomicAdd(sig.counters + kMaxSignalChunks, 1u) == gridDim.x - 1) {
+        sig.counters[kMaxSignalChunks] = 0u;
+        KVX_TRACE_STAMP(0, sig.trace_id, 3);
+        atomicMax(&g_trace_n[0], sig.trace_id + 1);
+      }
+    }
+#endif
   }
 }
 
