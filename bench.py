@@ -488,7 +488,11 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                 else:
                     ch.send(planes, t, timing)
     else:
-        slots, nb = B.paged_slots(torch, T, dev, seed=ch.pair)
+        # fixed workloads: a random permutation of exactly the blocks the
+        # hand-off fills (the e2e download then moves only the result);
+        # traces keep slack blocks for their per-request block rounding
+        slots, nb = B.paged_slots(torch, T, dev, seed=ch.pair,
+                                  slack_blocks=0 if trace is None else 64)
         kc = torch.zeros((L, nb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
         vc = torch.zeros_like(kc)
         if trace is None and args.batch > 1:
