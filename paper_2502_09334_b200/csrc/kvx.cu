@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 #include <nccl.h>  // types only: the entry points are resolved at run time (dlopen)
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -117,6 +118,9 @@ int make_geo(kvx::Geo& g, const void* k, const void* v, int64_t layer_stride, co
   if (head_offset < 0 || head_offset + n_heads > plane_heads) return KVX_ERR_INVALID_ARG;
   g.plane_row_b = int64_t(plane_heads) * head_dim * 2;
   g.head_off_b = int64_t(head_offset) * head_dim * 2;
+#ifdef KVX_DEBUG
+  g.dbg_rows = (layer_stride > 0 && g.plane_row_b > 0) ? layer_stride * 2 / g.plane_row_b : 0;
+#endif
   if (g.head_off_b % 32 || g.plane_row_b % 32) {
     if (n_layers > 0 && n_tokens > 0 && (g.head_off_b % 16 || g.plane_row_b % 16))
       return KVX_ERR_INVALID_ARG;

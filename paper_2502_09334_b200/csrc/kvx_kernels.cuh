@@ -131,6 +131,9 @@ struct Geo {
   int plane0;              // first plane: 0 = K, 1 = V (planes == 1: which one)
   int64_t plane_row_b;     // bytes per token row on the paged side (all its heads)
   int64_t head_off_b;      // byte offset of this launch's head window in that row
+#ifdef KVX_DEBUG
+  int64_t dbg_rows;        // debug builds: token positions one layer plane holds (0 = unknown)
+#endif
 };
 
 // Token row `pos` of a plane, at this launch's head window (TP head shards:
@@ -144,7 +147,17 @@ __device__ __forceinline__ const char* plane_ptr(const Geo& g, int kv, int64_t l
 }
 
 __device__ __forceinline__ int64_t pos_of(const Geo& g, int64_t t) {
-  return g.slots ? __ldg(g.slots + t) : t;
+  const int64_t p = g.slots ? __ldg(g.slots + t) : t;
+#ifdef KVX_DEBUG
+  // debug builds (-DKVX_DEBUG, the sanitizer stand-in): a position past the
+  // plane the caller's layer stride describes is an out-of-bounds access
+  if (g.dbg_rows > 0 && p >= g.dbg_rows) {
+    printf("kvx debug: token %lld -> position %lld outside the plane (%lld rows)\n",
+           (long long)t, (long long)p, (long long)g.dbg_rows);
+    __trap();
+  }
+#endif
+  return p;
 }
 
 // Token row tr = (l*planes + p)*T + t -> (plane kv, layer, row inside the
@@ -487,6 +500,14 @@ __device__ __noinline__ bool spin_until_geq(const uint32_t* flag, uint32_t value
     uint32_t v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
     const int32_t d = int32_t(v - value);
+#ifdef KVX_DEBUG
+    // the sequence protocol: a doorbell is never ahead of the value awaited
+    // (the partner cannot reuse a slot this side has not released)
+    if (d > 0 && d < (1 << 29)) {
+      printf("kvx debug: doorbell %u ahead of the awaited %u\n", v, value);
+      __trap();
+    }
+#endif
     if (d >= 0) {
       // A live doorbell is at most the awaited value (the partner cannot run
       // a slot's use ahead of this side); a jump of >= 2^29 is the host's
