@@ -386,10 +386,28 @@ def enable_peer(dev_a: int, dev_b: int) -> None:
     _lib.call("kvx_enable_peer", int(dev_a), int(dev_b))
 
 
-def transfer(packed: PackedKV, dst_device, *, out: PackedKV | None = None, stream=None,
-             layers: tuple[int, int] | None = None) -> PackedKV:
-    """Copy-engine NVLink transfer of the packed payload to ``dst_device``
-    (cudaMemcpyPeerAsync; the non-fused baseline)."""
+def transfer(packed: PackedKV, dst_device, dst_gpu_ids=None, *, out: PackedKV | None = None,
+             stream=None, layers: tuple[int, int] | None = None) -> PackedKV:
+    """Copy-engine NVLink transfer of the packed payload (cudaMemcpyPeerAsync;
+    the non-fused baseline).
+
+    Two call forms: ``transfer(packed, dst_device)``, or SURVEY 8(b)'s
+    ``transfer(packed, src_gpu_ids, dst_gpu_ids)`` with the reference's
+    stage GPU lists (``kv_comm_cost``'s ``prefill_gpu_ids`` /
+    ``decode_gpu_ids``, costs.py:83): the payload must live on one of the
+    source GPUs and goes to the first destination GPU; ``NoPath`` when the two
+    cannot reach each other (costs.py:63-64)."""
+    if dst_gpu_ids is not None:
+        src_ids = [int(i) for i in dst_device]
+        dst_ids = [int(i) for i in dst_gpu_ids]
+        if not dst_ids:
+            raise ValueError("dst_gpu_ids is empty")
+        if packed.device.index not in src_ids:
+            raise ValueError(f"payload on cuda:{packed.device.index}, not on the source GPUs "
+                             f"{src_ids}")
+        dst_device = torch.device("cuda", dst_ids[0])
+        if dst_device.index != packed.device.index:
+            enable_peer(packed.device.index, dst_device.index)  # NoPath if unreachable
     dst_device = torch.device(dst_device)
     if out is None:
         out = alloc_packed(packed.layout, dst_device)

@@ -138,3 +138,26 @@ def test_cfg2_full_size_properties(cuda):
     plan.run()
     torch.cuda.synchronize()
     assert p.owner.view(torch.int64).sum().item() == digest
+
+
+def test_transfer_with_reference_gpu_lists(cuda):
+    """SURVEY 8(b)'s transfer(packed, src_gpu_ids, dst_gpu_ids): the payload
+    arrives byte-identical (here cuda:0 -> cuda:0; the multi-GPU suite covers
+    real peers through HandoffPlan), and misuse raises like the reference."""
+    torch = cuda
+    from paper_2502_09334_b200 import KvPrecision, compress, decompress_into_paged, transfer
+    kv_np, slots, nb, kv, kc, vc = make_case(torch, "cuda:0", "cuda:0", seed=3)
+    packed = compress(kv, KvPrecision(4), 128)
+    moved = transfer(packed, [0], [0])
+    torch.cuda.synchronize()
+    assert torch.equal(moved.codes(), packed.codes())
+    assert torch.equal(moved.scale().view(torch.int16), packed.scale().view(torch.int16))
+    decompress_into_paged(moved, kc, vc, torch.from_numpy(slots).to("cuda:0"))
+    torch.cuda.synchronize()
+    okc, ovc = expected_cache(kv_np, slots, nb, 16, 4, 128)
+    assert np.array_equal(h16(kc.cpu().numpy()), h16(okc))
+    assert np.array_equal(h16(vc.cpu().numpy()), h16(ovc))
+    with pytest.raises(ValueError):
+        transfer(packed, [1, 2], [0])   # the payload is not on a source GPU
+    with pytest.raises(ValueError):
+        transfer(packed, [0], [])
