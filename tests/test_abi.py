@@ -120,7 +120,7 @@ def test_integration_doc_bindings_match():
     """The ctypes stub INTEGRATION.md shows a maintainer matches the real ABI."""
     src = open(os.path.join(ROOT, "INTEGRATION.md")).read()
     m = {"P": ctypes.c_void_p, "I": ctypes.c_int, "I64": ctypes.c_int64, "U32": ctypes.c_uint32,
-         "U64": ctypes.c_uint64, "PP": ctypes.POINTER(ctypes.c_void_p)}
+         "U64": ctypes.c_uint64, "PP": ctypes.POINTER(ctypes.c_void_p), "SZ": ctypes.c_size_t}
     found = re.findall(r"kvx\.(kvx_\w+)\.argtypes = \[([^\]]*)\]", src)
     assert len(found) >= 4
     for name, body in found:
