@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/matrix")
     a = ap.parse_args()
     plan = [(1, ["--no-cpu-baseline"]), (1, ["--bits", "8", "--no-e2e", "--no-cpu-baseline"]),
+            (1, ["--workload", "cfg4_70b_gqa_pair", "--no-e2e", "--no-cpu-baseline"]),
             (1, ["--bits", "2", "--no-e2e", "--no-cpu-baseline"]),
             (1, ["--bits", "16", "--no-e2e", "--no-cpu-baseline"]),
             (1, ["--format", "kivi", "--group", "32", "--no-e2e", "--no-cpu-baseline"])]
@@ -42,13 +43,21 @@ def main():
         plan += [(2, []), (2, ["--workload", "cfg4_70b_gqa_pair", "--no-e2e"]),
                  (2, ["--workload", "trace_7b", "--no-e2e"]),
                  (2, ["--workload", "small_70b_gqa_128x1", "--no-e2e"]),
+                 (2, ["--workload", "small_70b_gqa_128x1", "--no-e2e", "--batch", "4",
+                      "--queue-depth", "8"]),
+                 (2, ["--workload", "small_70b_gqa_128x1", "--tokens", "16", "--no-e2e"]),
+                 (2, ["--workload", "small_70b_gqa_128x1", "--tokens", "16", "--no-e2e",
+                      "--batch", "4", "--queue-depth", "8"]),
+                 (2, ["--workload", "small_70b_gqa_128x1", "--no-e2e", "--gate-send"]),
                  (2, ["--format", "kivi", "--group", "32", "--no-e2e"]),
                  (2, ["--format", "kivi", "--group", "32", "--workload", "cfg4_70b_gqa_pair",
                       "--no-e2e"]),
                  (2, ["--mode", "pull_ldg", "--no-e2e"]), (2, ["--mode", "push", "--no-e2e"]),
                  (2, ["--mode", "copy", "--no-e2e"]), (2, ["--mode", "nccl", "--no-e2e"]),
                  (2, ["--bits", "8", "--group", "64", "--no-e2e"]),
-                 (2, ["--bits", "16", "--no-e2e"])]
+                 (2, ["--bits", "16", "--no-e2e"]),
+                 (2, ["--bits", "2", "--group", "64", "--workload", "cfg4_70b_gqa_pair",
+                      "--no-e2e"])]
     if a.gpus >= 4:
         plan += [(4, []), (4, ["--workload", "trace_70b_gqa", "--no-e2e"]),
                  (4, ["--workload", "trace_7b", "--no-e2e"])]
@@ -65,17 +74,19 @@ def main():
             f.write(json.dumps(d) + "\n")
             f.flush()
     with open(a.out + ".md", "w") as f:
-        f.write("| N | args | workload | GB/s fp16-eq | ms/step | roofline frac | bound | e2e GB/s |\n")
-        f.write("|---|---|---|---|---|---|---|---|\n")
+        f.write("| N | args | workload | GB/s fp16-eq | ms/step | us/hand-off | roofline frac | "
+                "bound | e2e GB/s |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|\n")
         for d in recs:
             if "error" in d:
                 f.write(f"| ? | {d['_args']} | ERROR | | | | | |\n")
                 continue
             r = d.get("roofline") or {}
             e = d.get("e2e") or {}
+            per = d["ms_per_step"] * 1e3 / (d.get("run") or {}).get("handoffs_per_step", 1)
             f.write(f"| {d['n_gpus']} | {d['_args'] or '(default)'} | {d['config']['workload']} | "
-                    f"{d['value']:.0f} | {d['ms_per_step']:.4f} | {r.get('frac')} | {r.get('bound')} | "
-                    f"{e.get('value', '')} |\n")
+                    f"{d['value']:.0f} | {d['ms_per_step']:.4f} | {per:.1f} | {r.get('frac')} | "
+                    f"{r.get('bound')} | {e.get('value', '')} |\n")
     print(open(a.out + ".md").read())
 
 
