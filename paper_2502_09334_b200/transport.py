@@ -652,6 +652,32 @@ class PairChannel:
         got = int(self._poll_buf[0]) & 0xFFFFFFFF
         return 0 <= ((got - v) & 0xFFFFFFFF) < (1 << 29)
 
+    def poll_count(self) -> int:
+        """Decode end, pull modes: how many of the next hand-offs (at most the
+        queue depth) the prefill side has started publishing -- the count a
+        decode round hands to ``recv_many``.  One device-to-host read of the
+        first-chunk doorbells of every queue slot."""
+        if self.role != "decode" or self.spec.mode not in PULL_MODES:
+            raise RuntimeError("poll_count() needs the decode end of a pull channel")
+        self.check()
+        if getattr(self, "_pollq_buf", None) is None:
+            self._pollq_buf = torch.empty(PULL_MAX_QUEUE * PULL_MAX_CHUNKS, dtype=torch.int32,
+                                          pin_memory=True)
+            self._pollq_stream = torch.cuda.Stream(self.device)
+        n_words = self.Q * PULL_MAX_CHUNKS
+        _lib.call("kvx_memcpy_async", self._pollq_buf.data_ptr(), self._pready(self.flags.ptr, 0, 0),
+                  4 * n_words, _stream_ptr(self._pollq_stream))
+        self._pollq_stream.synchronize()
+        flags = self._pollq_buf[:n_words].tolist()
+        n = 0
+        for k in range(1, self.Q + 1):  # hand-offs epoch+1, epoch+2, ... in order
+            h, v = self._seq(self.epoch + k)
+            got = flags[h * PULL_MAX_CHUNKS] & 0xFFFFFFFF
+            if not 0 <= ((got - v) & 0xFFFFFFFF) < (1 << 29):
+                break
+            n += 1
+        return n
+
     def recv(self, dst: KVPlanes, n_tokens: int, timing: list | None = None,
              stage_out: tuple | None = None, seqlens=None) -> None:
         """Receive into ``dst``.  ``stage_out=((dev_k, dev_v), (host_k, host_v))``:

@@ -329,7 +329,13 @@ def main():
             for T, sd in zip(Ts, seeds):
                 ch.send(KVPlanes.dense(torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=sd)).to(dev)), T)
             torch.cuda.synchronize()
+            dist.barrier(ctrl)  # every hand-off of the round is published
         else:
+            dist.barrier(ctrl)
+            if ch.poll_count() != len(Ts):
+                failures += 1
+                print(f"POLL_COUNT rank={rank} round={rnd}: {ch.poll_count()} != {len(Ts)}",
+                      flush=True)
             nbm = sum(-(-T // bs) for T in Ts) + 4
             kcm = torch.zeros((L, nbm, bs, H, D), dtype=torch.float16, device=dev)
             vcm = torch.zeros_like(kcm)
