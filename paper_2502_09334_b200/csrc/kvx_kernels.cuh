@@ -792,9 +792,15 @@ template <int BITS>
 __device__ __forceinline__ void k3_load(const K3Item& it, K3Data<BITS>& d) {
   if (!it.active) return;
   if constexpr (BITS == 4) {
+#ifdef KVX_K3_LD_PF256  // A/B: ask L2 to fetch 256 B around each code load
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(d.c.w[0]), "=r"(d.c.w[1]), "=r"(d.c.w[2]), "=r"(d.c.w[3])
+                 : "l"(it.codes));
+#else
     asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(d.c.w[0]), "=r"(d.c.w[1]), "=r"(d.c.w[2]), "=r"(d.c.w[3])
                  : "l"(it.codes));
+#endif
   } else if constexpr (BITS == 8) {
     asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(d.c.w[0]), "=r"(d.c.w[1]), "=r"(d.c.w[2]), "=r"(d.c.w[3]),
@@ -810,9 +816,15 @@ __device__ __forceinline__ void k3_load(const K3Item& it, K3Data<BITS>& d) {
 }
 
 __device__ __forceinline__ void st256(void* p, const U4& a, const U4& b) {
+#ifdef KVX_K3_ST_CS  // A/B: streaming (evict-first) stores of the fp16 cache rows
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+               "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+#else
   asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
                "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
                : "memory");
+#endif
 }
 
 template <int BITS>
