@@ -38,6 +38,7 @@ def test_modes_over_ipc_same_gpu(cuda):
     assert "pull bits=4: native pair=True" in out  # the fused one-launch path ran
     assert "long/short alternation Q=2: ok" in out and "queue_depth=3" in out
     assert "recv_many: ok" in out
+    assert "random lengths: 300 hand-offs" in out
 
 
 @pytest.mark.gpu
