@@ -792,7 +792,7 @@ template <int BITS>
 __device__ __forceinline__ void k3_load(const K3Item& it, K3Data<BITS>& d) {
   if (!it.active) return;
   if constexpr (BITS == 4) {
-#ifdef KVX_K3_LD_PF256  // A/B: ask L2 to fetch 256 B around each code load
+#ifndef KVX_K3_PLAIN_HINTS  // L2 fetches 256 B around each code load (A/B: ~0.5 %)
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.b32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(d.c.w[0]), "=r"(d.c.w[1]), "=r"(d.c.w[2]), "=r"(d.c.w[3])
                  : "l"(it.codes));
@@ -816,7 +816,9 @@ __device__ __forceinline__ void k3_load(const K3Item& it, K3Data<BITS>& d) {
 }
 
 __device__ __forceinline__ void st256(void* p, const U4& a, const U4& b) {
-#ifdef KVX_K3_ST_CS  // A/B: streaming (evict-first) stores of the fp16 cache rows
+#ifndef KVX_K3_PLAIN_HINTS  // streaming (evict-first) stores of the fp16 cache rows
+  // (A/B, profiles/r02_bench/k3_hints_n1.log: config 2 K3 1.750 -> 1.743 ms,
+  // config-4 pair shape 0.580 -> 0.570 ms; -DKVX_K3_PLAIN_HINTS restores the plain form)
   asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
                "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
                : "memory");
