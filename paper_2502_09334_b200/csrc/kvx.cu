@@ -377,6 +377,15 @@ constexpr int kBulkStageTarget = KVX_BULK_STAGE_BYTES;
 #define KVX_PULL_PER_SM 1
 #endif
 constexpr int kPullCtasPerSm = KVX_PULL_PER_SM;  // bulk-pull CTAs per SM (A/B: -DKVX_PULL_PER_SM)
+// 2-bit pulls write 8 fp16 bytes per payload byte (4 at 4-bit): at link speed
+// eight consumer warps per SM cannot keep up, so they run 2 CTAs per SM
+// (N=2 config-4 pair: 3,707 -> 4,314 GB/s fp16-eq, config 3 4,102 -> 4,365;
+// 4- and 8-bit lose 3 % and 2 % that way; profiles/r02_bench/pull_2bit_n2.log)
+#ifndef KVX_PULL_PER_SM_2BIT
+#define KVX_PULL_PER_SM_2BIT 2
+#endif
+template <int BITS>
+constexpr int pull_ctas_per_sm() { return BITS == 2 ? KVX_PULL_PER_SM_2BIT : kPullCtasPerSm; }
 
 // Smallest row count whose code and metadata bytes are both 16-byte multiples.
 int64_t bulk_row_multiple(int64_t code_row_bytes, int64_t meta_row_bytes) {
@@ -445,7 +454,7 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   // next hand-off's pull, which PDL schedules next to this one
   // (tools/decode_interference.py: a concurrent HBM-bound round slows 1.96x
   // instead of 2.2x).
-  per_sm = per_sm < kPullCtasPerSm ? per_sm : kPullCtasPerSm;
+  per_sm = per_sm < pull_ctas_per_sm<BITS>() ? per_sm : pull_ctas_per_sm<BITS>();
   int64_t grid = int64_t(sm_count(current_device())) * per_sm;
 #ifdef KVX_PULL_MAX_CTAS
   if (grid > KVX_PULL_MAX_CTAS) grid = KVX_PULL_MAX_CTAS;
@@ -521,7 +530,7 @@ cudaError_t launch_pull_many(const kvx::Geo& g, int64_t n_layers, kvx::PullMany&
   cudaError_t attr = ensure_smem_attr(k, 200 * 1024);
   if (attr != cudaSuccess) return attr;
   int per_sm = blocks_per_sm(k, kBulkThreads, smem);
-  per_sm = per_sm < kPullCtasPerSm ? per_sm : kPullCtasPerSm;
+  per_sm = per_sm < pull_ctas_per_sm<BITS>() ? per_sm : pull_ctas_per_sm<BITS>();
   int64_t grid = int64_t(sm_count(current_device())) * per_sm;
   if (grid > pm.n_spans) grid = pm.n_spans;
   *ok = true;
