@@ -403,13 +403,12 @@ struct PullDone {  // optional in-kernel completion of a pull hand-off
   uint32_t* peer_free = nullptr;
 };
 
+// Span geometry of a K3-bulk pull (false: not bulk-stageable).
 template <int BITS, int G>
-cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale, const void* zero,
-                        cudaStream_t s, bool* ok, const uint32_t* ready, uint32_t ready_value,
-                        int layers_per_chunk, const PullDone& done = PullDone(),
-                        kvx::Ctl* ctl = nullptr, bool pdl = false) {
-  *ok = false;
-  kvx::BulkGeo bg;
+bool plan_pull(const kvx::Geo& g, const void* codes, const void* scale, const void* zero,
+               const uint32_t* ready, uint32_t ready_value, int layers_per_chunk,
+               const PullDone& done, kvx::Ctl* ctl, kvx::BulkGeo& bg) {
+  bg = kvx::BulkGeo{};
   bg.ready = ready;
   bg.ready_value = ready_value;
   bg.done_counter = done.done_counter;
@@ -429,20 +428,34 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   if ((two_t * bg.code_row_bytes) % 16 || (two_t * bg.meta_row_bytes) % 16 ||
       !aligned(codes, 16) || !aligned(scale, 16) || !aligned(zero, 16) || g.codes_ls % 16 ||
       g.meta_ls % 16)
-    return cudaSuccess;  // not bulk-copyable: caller falls back to the LDG kernel
+    return false;  // not bulk-copyable: caller falls back to the LDG kernel
   int64_t r = kBulkStageTarget / bg.code_row_bytes;
   r = r / m * m;
   if (r < m) r = m;
   if (r > two_t) r = two_t;
   bg.rows_per_span = int(r);
   bg.stage_bytes = bg.rows_per_span * (bg.code_row_bytes + 2 * bg.meta_row_bytes);
-  const int smem = kBulkStages * bg.stage_bytes;
-  if (smem > 200 * 1024) return cudaSuccess;
+  if (kBulkStages * bg.stage_bytes > 200 * 1024) return false;
   bg.spans_per_layer = int((two_t + r - 1) / r);
   const int64_t n_layers = g.n_token_rows / two_t;
   const int64_t n_spans = n_layers * bg.spans_per_layer;
-  if (n_spans >= (int64_t(1) << 31)) return cudaSuccess;
+  if (n_spans >= (int64_t(1) << 31)) return false;
   bg.n_spans = uint32_t(n_spans);
+  return true;
+}
+
+template <int BITS, int G>
+cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale, const void* zero,
+                        cudaStream_t s, bool* ok, const uint32_t* ready, uint32_t ready_value,
+                        int layers_per_chunk, const PullDone& done = PullDone(),
+                        kvx::Ctl* ctl = nullptr, bool pdl = false) {
+  *ok = false;
+  kvx::BulkGeo bg;
+  if (!plan_pull<BITS, G>(g, codes, scale, zero, ready, ready_value, layers_per_chunk, done, ctl,
+                          bg))
+    return cudaSuccess;
+  const int smem = kBulkStages * bg.stage_bytes;
+  const int64_t n_spans = bg.n_spans;
   auto k = kvx::pull_dequant_scatter_kernel<BITS, G, kBulkStages>;
   cudaError_t attr = ensure_smem_attr(k, 200 * 1024);
   if (attr != cudaSuccess) return attr;
@@ -639,6 +652,28 @@ cudaError_t launch_kchan_dequant(const kvx::KchanGeo& kg, const int64_t* slots, 
 #endif
 constexpr int kKchanStageCodes = KVX_KCHAN_STAGE_CODES;  // code bytes per kchan span
 
+// Span geometry of a bulk-staged kchan pull (false: not stageable).
+template <int BITS, int G>
+bool plan_kchan_pull(const kvx::KchanGeo& kg, const uint32_t* ready, uint32_t ready_value,
+                     int layers_per_chunk, kvx::Ctl* ctl, kvx::KchanBulk& kb) {
+  kb = kvx::KchanBulk{};
+  kb.ready = ready;
+  kb.ready_value = ready_value;
+  kb.ctl = ctl;
+  kb.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
+  kb.slab = kKchanStageCodes / (G * BITS / 8);  // channels per span (S/32 divides 256)
+  // rows that fit one span whole: the group's code rows are then a single
+  // contiguous range, one bulk copy instead of G (when S/32 still divides 256)
+  if (kg.row_elems <= kb.slab && 256 % (kg.row_elems / 32) == 0) kb.slab = kg.row_elems;
+  if (kg.row_elems % 32 || !aligned(kg.codes, 16) || !aligned(kg.scale, 16) ||
+      !aligned(kg.zero, 16) || kg.payload_ls % 16)
+    return false;
+  kb.slabs = (kg.row_elems + kb.slab - 1) / kb.slab;
+  kb.n_spans = kg.n_layers * kg.n_groups * kb.slabs;
+  kb.stage_bytes = G * kb.slab * BITS / 8 + 4 * kb.slab;
+  return true;
+}
+
 // Bulk-staged kchan dequant (payload read over NVLink).  *ok = false when the
 // shape cannot be staged (caller falls back to the per-lane kernel).
 template <int BITS, int G>
@@ -650,20 +685,8 @@ cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, voi
   *ok = false;
   constexpr int kStages = 4;
   kvx::KchanBulk kb;
-  kb.ready = ready;
-  kb.ready_value = ready_value;
-  kb.ctl = ctl;
-  kb.layers_per_chunk = layers_per_chunk > 0 ? layers_per_chunk : 1;
-  kb.slab = kKchanStageCodes / (G * BITS / 8);  // channels per span (S/32 divides 256)
-  // rows that fit one span whole: the group's code rows are then a single
-  // contiguous range, one bulk copy instead of G (when S/32 still divides 256)
-  if (kg.row_elems <= kb.slab && 256 % (kg.row_elems / 32) == 0) kb.slab = kg.row_elems;
-  if (kg.row_elems % 32 || !aligned(kg.codes, 16) || !aligned(kg.scale, 16) ||
-      !aligned(kg.zero, 16) || kg.payload_ls % 16)
+  if (!plan_kchan_pull<BITS, G>(kg, ready, ready_value, layers_per_chunk, ctl, kb))
     return cudaSuccess;
-  kb.slabs = (kg.row_elems + kb.slab - 1) / kb.slab;
-  kb.n_spans = kg.n_layers * kg.n_groups * kb.slabs;
-  kb.stage_bytes = G * kb.slab * BITS / 8 + 4 * kb.slab;
   const int smem = kStages * kb.stage_bytes;
   auto k = kvx::pull_kchan_kernel<BITS, G, kStages>;
   {
@@ -690,6 +713,41 @@ cudaError_t launch_kchan_pull(const kvx::KchanGeo& kg, const int64_t* slots, voi
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, kg, kb, slots, static_cast<char*>(kc), dst_ls_b);
+}
+
+// The kivi pull as ONE kernel (pull_kivi_kernel): the K groups' spans then
+// the V rows' spans.  *ok = false when either part cannot be bulk-staged.
+template <int BITS, int G>
+cudaError_t launch_kivi_pull(const kvx::KchanGeo& kg, const kvx::Geo& gv, const void* vc,
+                             const void* vs, const void* vz, const int64_t* slots, void* kc,
+                             int64_t dst_ls_b, cudaStream_t s, bool* ok, const uint32_t* ready,
+                             uint32_t ready_value, int layers_per_chunk, kvx::Ctl* ctl,
+                             const PullDone& done) {
+  *ok = false;
+  constexpr int kStages = 4;
+  kvx::KchanBulk kb;
+  kvx::BulkGeo bg;
+  if (!plan_kchan_pull<BITS, G>(kg, ready, ready_value, layers_per_chunk, ctl, kb)) return cudaSuccess;
+  if (!plan_pull<BITS, G>(gv, vc, vs, vz, ready + KVX_KIVI_V_FLAGS, ready_value, layers_per_chunk,
+                          done, ctl, bg))
+    return cudaSuccess;
+  const int stage = kb.stage_bytes > bg.stage_bytes ? kb.stage_bytes : bg.stage_bytes;
+  const int smem = kStages * stage;
+  if (smem > 200 * 1024) return cudaSuccess;
+  auto k = kvx::pull_kivi_kernel<BITS, G, kStages>;
+  cudaError_t attr = ensure_smem_attr(k, 200 * 1024);
+  if (attr != cudaSuccess) return attr;
+  int per_sm = blocks_per_sm(k, kBulkThreads, smem);
+  per_sm = per_sm < kPullCtasPerSm ? per_sm : kPullCtasPerSm;
+  int64_t grid = int64_t(sm_count(current_device())) * per_sm;
+  const int64_t n_all = kb.n_spans + int64_t(bg.n_spans);
+  if (grid > n_all) grid = n_all;
+  if (grid < 1) return cudaSuccess;
+  *ok = true;
+  kvx::pull_kivi_kernel<BITS, G, kStages><<<unsigned(grid), kBulkThreads, smem, s>>>(
+      kg, kb, gv, bg, static_cast<const uint8_t*>(vc), static_cast<const __half*>(vs),
+      static_cast<const __half*>(vz), slots, static_cast<char*>(kc), dst_ls_b, stage);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -1045,7 +1103,39 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const char* base = static_cast<const char*>(payload);
   cudaError_t e = cudaSuccess;
-  if (n_groups) {
+  bool fused = false;  // K groups and V rows in ONE pull kernel (pull_kivi_kernel)
+  static const bool fuse_ok = std::getenv("KVX_KIVI_TWO_KERNELS") == nullptr;
+  if (bulk && ready && n_groups && fuse_ok) {
+    kvx::KchanGeo kg;
+    kg.k_plane = nullptr;
+    kg.layer_stride_b = 0;
+    kg.group_starts = group_starts;
+    kg.n_groups = n_groups;
+    kg.row_elems = n_heads * head_dim;
+    kg.n_layers = n_layers;
+    kg.codes = const_cast<char*>(base + seg_offsets[0]);
+    kg.scale = const_cast<char*>(base + seg_offsets[1]);
+    kg.zero = const_cast<char*>(base + seg_offsets[2]);
+    kg.payload_ls = payload_layer_stride;
+    kvx::Geo gv;
+    rc = make_geo(gv, v_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
+                  head_dim, group, bits, payload_layer_stride, 1, 1);
+    if (rc) return rc;
+    if (gv.plane_row_b % 32 == 0) {
+      const char *vc = base + seg_offsets[4], *vs = base + seg_offsets[5], *vz = base + seg_offsets[6];
+      PullDone pd = n_residual ? PullDone() : done;
+      const int64_t dls = dst_layer_stride * 2;
+      const int lpc = layers_per_chunk;
+      if (bits == 4)
+        e = group == 32 ? launch_kivi_pull<4, 32>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, pd)
+                        : launch_kivi_pull<4, 64>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, pd);
+      else
+        e = group == 32 ? launch_kivi_pull<8, 32>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, pd)
+                        : launch_kivi_pull<8, 64>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, pd);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  if (n_groups && !fused) {
     kvx::KchanGeo kg;
     kg.k_plane = nullptr;
     kg.layer_stride_b = 0;
@@ -1082,7 +1172,7 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
       if (e != cudaSuccess) return e;
     }
   }
-  {
+  if (!fused) {
     kvx::Geo g;
     rc = make_geo(g, v_cache, v_cache, dst_layer_stride, dst_slots, n_layers, n_tokens, n_heads,
                   head_dim, group, bits, payload_layer_stride, 1, 1);

@@ -296,12 +296,76 @@ struct KchanBulk {
   int layers_per_chunk;
 };
 
+// One K span of the kivi pull: (layer, group k, slab of S channels) -- the
+// group's G code-row slices, then its S scales and S zeros, into a stage.
+template <int BITS, int G>
+__device__ __forceinline__ void kchan_issue_span(const KchanGeo& g, const KchanBulk& kb,
+                                                 int64_t sp, uint8_t* buf, uint64_t* bar) {
+  const int S = kb.slab;
+  const int code_slice = S * BITS / 8;
+  const int64_t lg = sp / kb.slabs;
+  const int c0 = int(sp - lg * kb.slabs) * S;
+  const int64_t layer = lg / g.n_groups, grp = lg - layer * g.n_groups;
+  const int ns = min(S, g.row_elems - c0);
+  const uint32_t rb = uint32_t(ns) * BITS / 8, mb = uint32_t(ns) * 2;
+  mbar_expect_tx(bar, G * rb + 2 * mb);
+  const char* lc = g.codes + layer * g.payload_ls + int64_t(c0) * BITS / 8;
+  if (ns == g.row_elems && code_slice == int(rb)) {
+    // the slab is whole rows: the group's G code rows are one range
+    bulk_g2s(buf, lc + grp * G * int64_t(g.row_elems) * BITS / 8, G * rb, bar);
+  } else {
+    for (int j = 0; j < G; ++j)
+      bulk_g2s(buf + j * code_slice, lc + (grp * G + j) * int64_t(g.row_elems) * BITS / 8, rb,
+               bar);
+  }
+  const int64_t meta = (grp * g.row_elems + c0) * 2;
+  bulk_g2s(buf + G * code_slice, g.scale + layer * g.payload_ls + meta, mb, bar);
+  bulk_g2s(buf + G * code_slice + 2 * S, g.zero + layer * g.payload_ls + meta, mb, bar);
+}
+
+// Consumers of one staged K span: each thread keeps one 32-channel chunk's
+// scales and zeros in registers and walks the group's rows.
+template <int BITS, int G, int CONSUMERS>
+__device__ __forceinline__ void kchan_consume_span(const KchanGeo& g, const KchanBulk& kb,
+                                                   int64_t sp, const uint8_t* buf,
+                                                   const int64_t* __restrict__ dst_slots,
+                                                   char* k_cache, int64_t dst_ls_b) {
+  constexpr int CB = 32 * BITS / 8;
+  const int S = kb.slab;
+  const int code_slice = S * BITS / 8;
+  const int nck = S / 32;           // 32-channel chunks per full slab
+  const int c = threadIdx.x % nck;  // this thread's chunk (fixed across spans)
+  const int jstep = (CONSUMERS * 32) / nck;
+  const int64_t lg = sp / kb.slabs;
+  const int c0 = int(sp - lg * kb.slabs) * S;
+  const int64_t layer = lg / g.n_groups, grp = lg - layer * g.n_groups;
+  const int ns = min(S, g.row_elems - c0);
+  if (c * 32 >= ns) return;
+  const uint4* sv = reinterpret_cast<const uint4*>(buf + G * code_slice + c * 64);
+  const uint4* zv = reinterpret_cast<const uint4*>(buf + G * code_slice + 2 * S + c * 64);
+  uint32_t sw[16], zw[16];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint4 a = sv[i], b = zv[i];
+    sw[4 * i] = a.x; sw[4 * i + 1] = a.y; sw[4 * i + 2] = a.z; sw[4 * i + 3] = a.w;
+    zw[4 * i] = b.x; zw[4 * i + 1] = b.y; zw[4 * i + 2] = b.z; zw[4 * i + 3] = b.w;
+  }
+  const int64_t t0 = __ldg(g.group_starts + grp);
+  char* kplane = k_cache + layer * dst_ls_b + int64_t(c0 + c * 32) * 2;
+  for (int j = threadIdx.x / nck; j < G; j += jstep) {
+    const int64_t pos = __ldg(dst_slots + t0 + j);
+    if (pos < 0) continue;
+    uint32_t cw[BITS];
+    kchan_load_codes<BITS>(reinterpret_cast<const char*>(buf + j * code_slice + c * CB), cw);
+    kchan_dequant_store<BITS>(cw, sw, zw, kplane + pos * int64_t(g.row_elems) * 2);
+  }
+}
+
 template <int BITS, int G, int STAGES>
 __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBulk kb,
                                                             const int64_t* __restrict__ dst_slots,
                                                             char* k_cache, int64_t dst_ls_b) {
   constexpr int CONSUMERS = 8;
-  constexpr int CB = 32 * BITS / 8;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   __shared__ uint32_t s_abort;
@@ -315,8 +379,6 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int S = kb.slab;
-  const int code_slice = S * BITS / 8;  // bytes of one row's slab slice in smem
   if (warp == CONSUMERS) {  // ---- producer: one elected thread
     if (lane == 0) {
       int64_t ready_chunk = -1;
@@ -325,9 +387,7 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
       for (int64_t sp = blockIdx.x; sp < kb.n_spans; sp += gridDim.x, ++k) {
         const int st = k % STAGES;
         if (k >= STAGES) mbar_wait(&empty[st], ((k / STAGES) & 1) ^ 1);
-        const int64_t lg = sp / kb.slabs;
-        const int c0 = int(sp - lg * kb.slabs) * S;
-        const int64_t layer = lg / g.n_groups, grp = lg - layer * g.n_groups;
+        const int64_t layer = (sp / kb.slabs) / g.n_groups;
         if (kb.ready && ok) {
           const int64_t c = layer / kb.layers_per_chunk;
           if (c > ready_chunk) {
@@ -340,23 +400,7 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
           mbar_arrive_empty_phase(&full[st]);
           continue;
         }
-        const int ns = min(S, g.row_elems - c0);
-        const uint32_t rb = uint32_t(ns) * BITS / 8, mb = uint32_t(ns) * 2;
-        mbar_expect_tx(&full[st], G * rb + 2 * mb);
-        uint8_t* buf = smem + st * kb.stage_bytes;
-        const char* lc = g.codes + layer * g.payload_ls + int64_t(c0) * BITS / 8;
-        if (ns == g.row_elems && code_slice == int(rb)) {
-          // the slab is whole rows: the group's G code rows are one range
-          bulk_g2s(buf, lc + grp * G * int64_t(g.row_elems) * BITS / 8, G * rb, &full[st]);
-        } else {
-          for (int j = 0; j < G; ++j)
-            bulk_g2s(buf + j * code_slice, lc + (grp * G + j) * int64_t(g.row_elems) * BITS / 8,
-                     rb, &full[st]);
-        }
-        const int64_t meta = (grp * g.row_elems + c0) * 2;
-        bulk_g2s(buf + G * code_slice, g.scale + layer * g.payload_ls + meta, mb, &full[st]);
-        bulk_g2s(buf + G * code_slice + 2 * S, g.zero + layer * g.payload_ls + meta, mb,
-                 &full[st]);
+        kchan_issue_span<BITS, G>(g, kb, sp, smem + st * kb.stage_bytes, &full[st]);
       }
       // PDL (launched behind the previous hand-off's pull): every span of this
       // CTA is requested, the stream's next kernel may be scheduled
@@ -364,40 +408,136 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
     }
   } else {  // ---- consumers
     pdl_wait();  // the slot mapping, group starts and the cache are stream-ordered
-    const int nck = S / 32;           // 32-channel chunks per full slab
-    const int c = threadIdx.x % nck;  // this thread's chunk (fixed across spans)
-    const int jstep = (CONSUMERS * 32) / nck;
     uint32_t k = 0;
     for (int64_t sp = blockIdx.x; sp < kb.n_spans; sp += gridDim.x, ++k) {
       const int st = k % STAGES;
-      const int64_t lg = sp / kb.slabs;
-      const int c0 = int(sp - lg * kb.slabs) * S;
-      const int64_t layer = lg / g.n_groups, grp = lg - layer * g.n_groups;
-      const int ns = min(S, g.row_elems - c0);
-      const uint8_t* buf = smem + st * kb.stage_bytes;
       mbar_wait(&full[st], (k / STAGES) & 1);
-      if (c * 32 < ns && !*reinterpret_cast<volatile uint32_t*>(&s_abort)) {
-        const uint4* sv = reinterpret_cast<const uint4*>(buf + G * code_slice + c * 64);
-        const uint4* zv = reinterpret_cast<const uint4*>(buf + G * code_slice + 2 * S + c * 64);
-        uint32_t sw[16], zw[16];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint4 a = sv[i], b = zv[i];
-          sw[4 * i] = a.x; sw[4 * i + 1] = a.y; sw[4 * i + 2] = a.z; sw[4 * i + 3] = a.w;
-          zw[4 * i] = b.x; zw[4 * i + 1] = b.y; zw[4 * i + 2] = b.z; zw[4 * i + 3] = b.w;
+      if (!*reinterpret_cast<volatile uint32_t*>(&s_abort))
+        kchan_consume_span<BITS, G, CONSUMERS>(g, kb, sp, smem + st * kb.stage_bytes, dst_slots,
+                                               k_cache, dst_ls_b);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+}
+
+// The kivi pull as ONE kernel: the per-channel K spans (kchan_*_span) and the
+// per-token V spans (bulk_consume_span) share one span space -- K first, then
+// V -- and one stage ring sized for the larger kind, so the V rows stream in
+// right behind the K groups with no kernel boundary between them.  K spans
+// wait on ready[c], V spans on ready[KVX_KIVI_V_FLAGS + c] (c = layer chunk).
+// In-kernel completion as in pull_dequant_scatter_kernel (bg.done_counter /
+// peer_free, only without residual rows).
+template <int BITS, int G, int STAGES>
+__global__ void __launch_bounds__(288, 1) pull_kivi_kernel(KchanGeo kg, KchanBulk kb, Geo g,
+                                                           BulkGeo bg,
+                                                           const uint8_t* __restrict__ vcodes,
+                                                           const __half* __restrict__ vscale,
+                                                           const __half* __restrict__ vzero,
+                                                           const int64_t* __restrict__ dst_slots,
+                                                           char* k_cache, int64_t dst_ls_b,
+                                                           int stage_bytes) {
+  constexpr int CONSUMERS = 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ uint32_t s_abort;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CONSUMERS);
+    }
+    s_abort = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t nk = kb.n_spans;
+  const int64_t n_all = nk + int64_t(bg.n_spans);
+  const int64_t two_t = g.n_tokens;  // V only: one plane
+  if (warp == CONSUMERS) {  // ---- producer
+    if (lane == 0) {
+      int64_t ready_k = -1, ready_v = -1;
+      uint32_t k = 0;
+      bool ok = true;
+      for (int64_t sp = blockIdx.x; sp < n_all; sp += gridDim.x, ++k) {
+        const int st = k % STAGES;
+        if (k >= STAGES) mbar_wait(&empty[st], ((k / STAGES) & 1) ^ 1);
+        uint8_t* buf = smem + st * stage_bytes;
+        if (sp < nk) {
+          const int64_t c = ((sp / kb.slabs) / kg.n_groups) / kb.layers_per_chunk;
+          if (ok && c > ready_k) {
+            ok = wait_ready(kb.ready + c, kb.ready_value, kb.ctl);
+            ready_k = c;
+          }
+          if (!ok) {
+            *reinterpret_cast<volatile uint32_t*>(&s_abort) = 1u;
+            mbar_arrive_empty_phase(&full[st]);
+            continue;
+          }
+          kchan_issue_span<BITS, G>(kg, kb, sp, buf, &full[st]);
+        } else {
+          const uint32_t vsp = uint32_t(sp - nk);
+          const uint32_t layer = vsp / bg.spans_per_layer;
+          const int64_t c = int64_t(layer) / bg.layers_per_chunk;
+          if (ok && c > ready_v) {
+            ok = wait_ready(bg.ready + c, bg.ready_value, bg.ctl);
+            ready_v = c;
+          }
+          if (!ok) {
+            *reinterpret_cast<volatile uint32_t*>(&s_abort) = 1u;
+            mbar_arrive_empty_phase(&full[st]);
+            continue;
+          }
+          const int64_t r0 = int64_t(vsp - layer * bg.spans_per_layer) * bg.rows_per_span;
+          const int rows = int(min(int64_t(bg.rows_per_span), two_t - r0));
+          const uint32_t cb = rows * bg.code_row_bytes, mb = rows * bg.meta_row_bytes;
+          mbar_expect_tx(&full[st], cb + 2 * mb);
+          bulk_g2s(buf, vcodes + layer * g.codes_ls + r0 * bg.code_row_bytes, cb, &full[st]);
+          const char* sb = reinterpret_cast<const char*>(vscale) + layer * g.meta_ls;
+          const char* zb = reinterpret_cast<const char*>(vzero) + layer * g.meta_ls;
+          uint8_t* mbuf = buf + bg.rows_per_span * bg.code_row_bytes;
+          bulk_g2s(mbuf, sb + r0 * bg.meta_row_bytes, mb, &full[st]);
+          bulk_g2s(mbuf + bg.rows_per_span * bg.meta_row_bytes, zb + r0 * bg.meta_row_bytes, mb,
+                   &full[st]);
         }
-        const int64_t t0 = __ldg(g.group_starts + grp);
-        char* kplane = k_cache + layer * dst_ls_b + int64_t(c0 + c * 32) * 2;
-        for (int j = threadIdx.x / nck; j < G; j += jstep) {
-          const int64_t pos = __ldg(dst_slots + t0 + j);
-          if (pos < 0) continue;
-          uint32_t cw[BITS];
-          kchan_load_codes<BITS>(reinterpret_cast<const char*>(buf + j * code_slice + c * CB), cw);
-          kchan_dequant_store<BITS>(cw, sw, zw, kplane + pos * int64_t(g.row_elems) * 2);
+      }
+    }
+  } else {  // ---- consumers
+    pdl_wait();
+    uint32_t k = 0;
+    for (int64_t sp = blockIdx.x; sp < n_all; sp += gridDim.x, ++k) {
+      const int st = k % STAGES;
+      const uint8_t* buf = smem + st * stage_bytes;
+      mbar_wait(&full[st], (k / STAGES) & 1);
+      if (!*reinterpret_cast<volatile uint32_t*>(&s_abort)) {
+        if (sp < nk) {
+          kchan_consume_span<BITS, G, CONSUMERS>(kg, kb, sp, buf, dst_slots, k_cache, dst_ls_b);
+        } else {
+          const uint32_t vsp = uint32_t(sp - nk);
+          const uint32_t layer = vsp / bg.spans_per_layer;
+          const int64_t r0 = int64_t(vsp - layer * bg.spans_per_layer) * bg.rows_per_span;
+          const int rows = int(min(int64_t(bg.rows_per_span), two_t - r0));
+          bulk_consume_span<BITS, G, CONSUMERS>(g, bg.code_row_bytes, bg.meta_row_bytes,
+                                                bg.rows_per_span, bg.cpr, buf, rows, r0, layer,
+                                                warp, lane);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  if (bg.done_counter) {  // in-kernel slot release (no residual rows)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t inc = s_abort ? 0x10001u : 1u;
+      const uint32_t total = atomicAdd(bg.done_counter, inc) + inc;
+      if ((total & 0xFFFFu) == gridDim.x) {
+        bg.done_counter[0] = 0u;
+        if ((total >> 16) == 0u)
+          asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(bg.peer_free),
+                       "r"(bg.ready_value)
+                       : "memory");
+      }
     }
   }
 }
