@@ -378,11 +378,12 @@ constexpr int kBulkStageTarget = KVX_BULK_STAGE_BYTES;
 #endif
 constexpr int kPullCtasPerSm = KVX_PULL_PER_SM;  // bulk-pull CTAs per SM (A/B: -DKVX_PULL_PER_SM)
 // 2-bit pulls write 8 fp16 bytes per payload byte (4 at 4-bit): at link speed
-// eight consumer warps per SM cannot keep up, so they run 2 CTAs per SM
-// (N=2 config-4 pair: 3,707 -> 4,314 GB/s fp16-eq, config 3 4,102 -> 4,365;
-// 4- and 8-bit lose 3 % and 2 % that way; profiles/r02_bench/pull_2bit_n2.log)
+// eight consumer warps per SM cannot keep up, so they run 3 CTAs per SM
+// (N=2 config-4 pair, GB/s fp16-eq: 1 CTA 3,707, 2 CTAs 4,101-4,314, 3 CTAs
+// 4,336; config 3: 4,102 / 4,299-4,365 / 4,314.  4- and 8-bit lose 3 % and
+// 2 % with 2 CTAs; profiles/r02_bench/pull_2bit_n2.log, val2_n2.log)
 #ifndef KVX_PULL_PER_SM_2BIT
-#define KVX_PULL_PER_SM_2BIT 2
+#define KVX_PULL_PER_SM_2BIT 3
 #endif
 template <int BITS>
 constexpr int pull_ctas_per_sm() { return BITS == 2 ? KVX_PULL_PER_SM_2BIT : kPullCtasPerSm; }
