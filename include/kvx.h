@@ -237,10 +237,10 @@ int kvx_quant_pack_kivi_signal(const void* k_src, const void* v_src, int64_t src
  * the residual rows) on ready_flags[KVX_KIVI_V_FLAGS + chunk], the layout
  * kvx_quant_pack_kivi_signal rings -- so ONE call consumes a whole hand-off
  * while the prefill side is still publishing it.  done_counter /
- * peer_free_flag (nullable, together; only with ready_flags and no residual
- * rows): the V kernel's last CTA frees the queue slot in-kernel as in
- * kvx_pull_dequant_scatter_paged; otherwise the caller releases the slot
- * after the call (stream order).  flags: KVX_PULL_PDL launches both pulls
+ * peer_free_flag (nullable, together; only with ready_flags): the queue slot
+ * is released once the hand-off's last payload read is done -- by the single
+ * kivi pull kernel's last CTA, or in stream order after the residual rows on
+ * the two-kernel fallback; without them the caller releases it.  flags: KVX_PULL_PDL launches both pulls
  * with programmatic dependent launch (each one's producer streams while the
  * stream's previous kernel drains).  With flags, shapes that cannot be bulk-staged return
  * KVX_ERR_UNSUPPORTED.  ctl as for kvx_quant_pack_signal.

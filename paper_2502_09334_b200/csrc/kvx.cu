@@ -723,7 +723,7 @@ cudaError_t launch_kivi_pull(const kvx::KchanGeo& kg, const kvx::Geo& gv, const 
                              const void* vs, const void* vz, const int64_t* slots, void* kc,
                              int64_t dst_ls_b, cudaStream_t s, bool* ok, const uint32_t* ready,
                              uint32_t ready_value, int layers_per_chunk, kvx::Ctl* ctl,
-                             const PullDone& done) {
+                             const PullDone& done, kvx::KiviResidual kr) {
   *ok = false;
   constexpr int kStages = 4;
   kvx::KchanBulk kb;
@@ -735,19 +735,30 @@ cudaError_t launch_kivi_pull(const kvx::KchanGeo& kg, const kvx::Geo& gv, const 
   const int stage = kb.stage_bytes > bg.stage_bytes ? kb.stage_bytes : bg.stage_bytes;
   const int smem = kStages * stage;
   if (smem > 200 * 1024) return cudaSuccess;
+  if (kr.n_rows > 0) {  // residual spans: as many whole rows as a stage holds
+    if (kr.row_bytes % 16 || kr.row_bytes > stage || !aligned(kr.rows, 16) || kr.payload_ls % 16)
+      return cudaSuccess;
+    kr.rows_per_span = stage / kr.row_bytes;
+    kr.spans_per_layer = int((kr.n_rows + kr.rows_per_span - 1) / kr.rows_per_span);
+    kr.n_spans = kg.n_layers * kr.spans_per_layer;
+  } else {
+    kr.n_spans = 0;
+    kr.rows_per_span = 1;
+    kr.spans_per_layer = 1;
+  }
   auto k = kvx::pull_kivi_kernel<BITS, G, kStages>;
   cudaError_t attr = ensure_smem_attr(k, 200 * 1024);
   if (attr != cudaSuccess) return attr;
   int per_sm = blocks_per_sm(k, kBulkThreads, smem);
   per_sm = per_sm < kPullCtasPerSm ? per_sm : kPullCtasPerSm;
   int64_t grid = int64_t(sm_count(current_device())) * per_sm;
-  const int64_t n_all = kb.n_spans + int64_t(bg.n_spans);
+  const int64_t n_all = kb.n_spans + int64_t(bg.n_spans) + kr.n_spans;
   if (grid > n_all) grid = n_all;
   if (grid < 1) return cudaSuccess;
   *ok = true;
   kvx::pull_kivi_kernel<BITS, G, kStages><<<unsigned(grid), kBulkThreads, smem, s>>>(
       kg, kb, gv, bg, static_cast<const uint8_t*>(vc), static_cast<const __half*>(vs),
-      static_cast<const __half*>(vz), slots, static_cast<char*>(kc), dst_ls_b, stage);
+      static_cast<const __half*>(vz), slots, static_cast<char*>(kc), dst_ls_b, stage, kr);
   return cudaGetLastError();
 }
 
@@ -1124,15 +1135,22 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
     if (rc) return rc;
     if (gv.plane_row_b % 32 == 0) {
       const char *vc = base + seg_offsets[4], *vs = base + seg_offsets[5], *vz = base + seg_offsets[6];
-      PullDone pd = n_residual ? PullDone() : done;
+      // the residual fp16 K rows ride in the same kernel: the slot can be
+      // freed by its last CTA in every case
+      kvx::KiviResidual kr = {};
+      kr.rows = base + seg_offsets[3];
+      kr.payload_ls = payload_layer_stride;
+      kr.dst_slots = residual_dst_slots;
+      kr.n_rows = n_residual;
+      kr.row_bytes = n_heads * head_dim * 2;
       const int64_t dls = dst_layer_stride * 2;
       const int lpc = layers_per_chunk;
       if (bits == 4)
-        e = group == 32 ? launch_kivi_pull<4, 32>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, pd)
-                        : launch_kivi_pull<4, 64>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, pd);
+        e = group == 32 ? launch_kivi_pull<4, 32>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, done, kr)
+                        : launch_kivi_pull<4, 64>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, done, kr);
       else
-        e = group == 32 ? launch_kivi_pull<8, 32>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, pd)
-                        : launch_kivi_pull<8, 64>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, pd);
+        e = group == 32 ? launch_kivi_pull<8, 32>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, done, kr)
+                        : launch_kivi_pull<8, 64>(kg, gv, vc, vs, vz, dst_slots, k_cache, dls, s, &fused, ready, ready_value, lpc, ctl, done, kr);
       if (e != cudaSuccess) return e;
     }
   }
@@ -1200,7 +1218,7 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
   // residual fp16 rows last: once the V kernel has seen every chunk's
   // doorbell, the whole payload is published, so these per-lane reads need
   // no wait of their own
-  if (n_residual) {
+  if (n_residual && !fused) {
     kvx::Geo g;
     rc = make_geo(g, k_cache, k_cache, dst_layer_stride, residual_dst_slots, n_layers, n_residual,
                   n_heads, head_dim, group, 16, payload_layer_stride, 1, 0);
@@ -1209,6 +1227,9 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
     k<<<grid_for(k, g.n_token_rows), kThreads, 0, s>>>(
         g, reinterpret_cast<const uint8_t*>(base + seg_offsets[3]));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // the two-kernel path could not free the slot in-kernel (the residual
+    // rows are read after the V pull): release it in stream order
+    if (done.peer_free) return kvx_stream_signal(done.peer_free, ready_value, stream);
   }
   return e;
 }
@@ -1240,8 +1261,7 @@ int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_lay
       (flags & ~KVX_PULL_PDL))
     return KVX_ERR_INVALID_ARG;
   if ((done_counter != nullptr) != (peer_free_flag != nullptr) ||
-      (done_counter && (!ready_flags || n_residual || !aligned(done_counter, 4) ||
-                        !aligned(peer_free_flag, 4))))
+      (done_counter && (!ready_flags || !aligned(done_counter, 4) || !aligned(peer_free_flag, 4))))
     return KVX_ERR_INVALID_ARG;
   PullDone done;
   done.done_counter = static_cast<uint32_t*>(done_counter);

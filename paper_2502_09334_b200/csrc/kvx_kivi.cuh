@@ -421,6 +421,19 @@ __global__ void __launch_bounds__(288, 1) pull_kchan_kernel(KchanGeo g, KchanBul
   }
 }
 
+// The residual window of a kivi payload (each request's last n mod G tokens,
+// K rows as fp16): rows_per_span rows of one layer per span.
+struct KiviResidual {
+  const char* rows;           // Kr of layer 0 (payload segment)
+  int64_t payload_ls;
+  const int64_t* dst_slots;   // [n_rows] paged positions of the residual tokens
+  int64_t n_rows;             // residual tokens per layer (0 = none)
+  int row_bytes;              // H * D * 2
+  int rows_per_span;
+  int spans_per_layer;
+  int64_t n_spans;            // n_layers * spans_per_layer
+};
+
 // The kivi pull as ONE kernel: the per-channel K spans (kchan_*_span) and the
 // per-token V spans (bulk_consume_span) share one span space -- K first, then
 // V -- and one stage ring sized for the larger kind, so the V rows stream in
@@ -436,7 +449,7 @@ __global__ void __launch_bounds__(288, 1) pull_kivi_kernel(KchanGeo kg, KchanBul
                                                            const __half* __restrict__ vzero,
                                                            const int64_t* __restrict__ dst_slots,
                                                            char* k_cache, int64_t dst_ls_b,
-                                                           int stage_bytes) {
+                                                           int stage_bytes, KiviResidual kr) {
   constexpr int CONSUMERS = 8;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -452,7 +465,8 @@ __global__ void __launch_bounds__(288, 1) pull_kivi_kernel(KchanGeo kg, KchanBul
   }
   __syncthreads();
   const int64_t nk = kb.n_spans;
-  const int64_t n_all = nk + int64_t(bg.n_spans);
+  const int64_t nkv = nk + int64_t(bg.n_spans);  // then the residual spans
+  const int64_t n_all = nkv + kr.n_spans;
   const int64_t two_t = g.n_tokens;  // V only: one plane
   if (warp == CONSUMERS) {  // ---- producer
     if (lane == 0) {
@@ -475,6 +489,24 @@ __global__ void __launch_bounds__(288, 1) pull_kivi_kernel(KchanGeo kg, KchanBul
             continue;
           }
           kchan_issue_span<BITS, G>(kg, kb, sp, buf, &full[st]);
+        } else if (sp >= nkv) {  // residual fp16 K rows: published with V's chunk
+          const int64_t rsp = sp - nkv;
+          const int64_t layer = rsp / kr.spans_per_layer;
+          const int64_t c = layer / bg.layers_per_chunk;
+          if (ok && c > ready_v) {
+            ok = wait_ready(bg.ready + c, bg.ready_value, bg.ctl);
+            ready_v = c;
+          }
+          if (!ok) {
+            *reinterpret_cast<volatile uint32_t*>(&s_abort) = 1u;
+            mbar_arrive_empty_phase(&full[st]);
+            continue;
+          }
+          const int64_t r0 = (rsp - layer * kr.spans_per_layer) * kr.rows_per_span;
+          const int rows = int(min(int64_t(kr.rows_per_span), kr.n_rows - r0));
+          const uint32_t nb = uint32_t(rows) * kr.row_bytes;
+          mbar_expect_tx(&full[st], nb);
+          bulk_g2s(buf, kr.rows + layer * kr.payload_ls + r0 * kr.row_bytes, nb, &full[st]);
         } else {
           const uint32_t vsp = uint32_t(sp - nk);
           const uint32_t layer = vsp / bg.spans_per_layer;
@@ -512,6 +544,19 @@ __global__ void __launch_bounds__(288, 1) pull_kivi_kernel(KchanGeo kg, KchanBul
       if (!*reinterpret_cast<volatile uint32_t*>(&s_abort)) {
         if (sp < nk) {
           kchan_consume_span<BITS, G, CONSUMERS>(kg, kb, sp, buf, dst_slots, k_cache, dst_ls_b);
+        } else if (sp >= nkv) {  // residual rows: 16-byte copies into the K cache
+          const int64_t rsp = sp - nkv;
+          const int64_t layer = rsp / kr.spans_per_layer;
+          const int64_t r0 = (rsp - layer * kr.spans_per_layer) * kr.rows_per_span;
+          const int rows = int(min(int64_t(kr.rows_per_span), kr.n_rows - r0));
+          const int vpr = kr.row_bytes / 16;
+          for (int i = threadIdx.x; i < rows * vpr; i += CONSUMERS * 32) {
+            const int r = i / vpr, v = i - r * vpr;
+            const int64_t pos = __ldg(kr.dst_slots + r0 + r);
+            if (pos < 0) continue;
+            const uint4 x = reinterpret_cast<const uint4*>(buf + int64_t(r) * kr.row_bytes)[v];
+            reinterpret_cast<uint4*>(k_cache + layer * dst_ls_b + pos * int64_t(kr.row_bytes))[v] = x;
+          }
         } else {
           const uint32_t vsp = uint32_t(sp - nk);
           const uint32_t layer = vsp / bg.spans_per_layer;

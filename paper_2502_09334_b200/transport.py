@@ -916,10 +916,10 @@ class PairChannel:
         _kernel_events_end(ev, s)
 
     def _recv_kivi(self, dst, n_tokens, seqlens, e, timing=None):
-        """Kivi decode side on the caller's stream: the K (per-channel) and V
-        bulk pulls, each waiting in-kernel for its doorbells; without residual
-        rows the V pull's last CTA frees the queue slot (no stream memop
-        between hand-offs)."""
+        """Kivi decode side on the caller's stream: ONE bulk pull kernel for the
+        per-channel K groups, the per-token V rows and the fp16 residual rows,
+        waiting in-kernel for the K / V doorbells; its last CTA frees the
+        queue slot (no stream memop between hand-offs)."""
         lay, gs, rt, chunks, lpc, h, v = self._kivi_common(n_tokens, seqlens, e)
         cur = torch.cuda.current_stream(self.device)
         gs_d, rt_d = self._kivi_index(gs, rt, cur)
@@ -940,16 +940,13 @@ class PairChannel:
             # TMA bulk-staged kernels over the whole hand-off, waiting in-kernel
             # for each chunk's doorbell
             ev = _kernel_events(timing, cur, "k3")
-            release = not len(rt)
+            # ONE pull kernel (K groups, V rows, residual rows) that frees the
+            # slot itself; no PDL (measured slower for the kivi pull: config 3
+            # 2,387 vs 2,484 GB/s, profiles/r02_bench/k1default_n2.log)
             _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args(0, lay.n_layers),
-                      self._pready(self.flags.ptr, h, 0), v, lpc,
-                      self._done_counter(h) if release else None,
-                      self._pfree(self.peer_flags, h) if release else None, self.ctl.ptr,
-                      0, cs)  # no PDL: measured slower for the two-kernel kivi pull
-                              # (config 3 2,387 vs 2,484 GB/s; profiles/r02_bench/k1default_n2.log)
+                      self._pready(self.flags.ptr, h, 0), v, lpc, self._done_counter(h),
+                      self._pfree(self.peer_flags, h), self.ctl.ptr, 0, cs)
             _kernel_events_end(ev, cur)
-            if not release:
-                signal(self._pfree(self.peer_flags, h), v, cur)
         else:  # "pull_ldg": per-chunk stream waits, per-lane peer loads
             for c, (l0, l1) in enumerate(chunks):
                 # the chunk's V doorbell publishes all of it (K, residual, V)

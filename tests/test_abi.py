@@ -164,7 +164,8 @@ def test_fused_and_kivi_entry_points_validate(lib):
     assert lib.kvx_pull_dequant_scatter_paged_kivi(256, 256, offs, 256, None, 0, None, 0, 1, 32,
                                                    1, 128, 32, 4, 256, 256, 0, 258, 1, 1, None,
                                                    None, None, 0, None) == E
-    # in-kernel slot release needs doorbells, both pointers, and no residual rows
+    # in-kernel slot release needs doorbells and both pointers (and, as
+    # everywhere, group counts that add up to the token count)
     assert lib.kvx_pull_dequant_scatter_paged_kivi(256, 256, offs, 256, None, 0, None, 0, 1, 32,
                                                    1, 128, 32, 4, 256, 256, 0, None, 1, 1, 256,
                                                    256, None, 0, None) == E
