@@ -105,7 +105,7 @@ def measure(n_gpus: int, bits: int = 4, L: int = 32, H: int = 8, D: int = 128,
 
 def cluster_from_bench_line(line: dict, n_gpus: int, peaks: dict | None = None) -> dict:
     """Uniform NVSwitch cluster from a bench.py N>1 JSON line's live
-    calibration (multi-process, CUDA-graph replayed pull channel): every
+    calibration (multi-process native pull channel, one launch per end): every
     ordered GPU pair gets the measured (alpha, beta)."""
     cal = line["calibration"]
     alpha = cal["alpha_us"] * 1e-6

@@ -24,7 +24,8 @@ prefill replicas' GPU memory (``PAPER.md:859``).  Here:
              NVLink (fused quantise + transfer); K3 on D reads it locally.
     "copy" - K1 local, copy-engine cudaMemcpyAsync into D's landing buffer,
              K3 local (the non-fused baseline).
-    "nccl" - K1 local, torch.distributed (NCCL) send/recv per chunk, K3 local.
+    "nccl" - K1 local, an NCCL send/recv per chunk through the C-ABI's NCCL
+             pair pool (kvx_nccl_*; a 2-rank communicator per pair), K3 local.
 * the default "pull" hand-off is ONE kernel launch per end, issued by the
   native pair object (``kvx_pair_send`` / ``kvx_pair_recv``, include/kvx.h):
   K1 rings per-layer-chunk doorbells in D's memory from the device, D's
@@ -37,9 +38,14 @@ prefill replicas' GPU memory (``PAPER.md:859``).  Here:
   sequence number from its arguments, so any length and any slot tensor is
   one launch -- no per-shape CUDA graphs, no graph caches.  Consecutive
   pulls are chained with programmatic dependent launch: the next pull
-  streams its slot while the previous one drains.
+  streams its slot while the previous one drains.  ``recv_many`` drains
+  several queued hand-offs with one pull launch (a decode round's pull).
+  The prefill end either gates each K1 in the GPU front-end until its slot
+  is free (``gate_send``) or, in latency mode, chains the K1s with PDL.
+* the kivi format: one fused prefill call ringing K and V chunk doorbells
+  in-kernel, one pull kernel for K groups, V rows and residual rows.
 * the other paths (pull_ldg, host doorbells, layer-wise streaming, host
-  staging, kivi) use stream memory operations (cuStreamWriteValue32 /
+  staging) use stream memory operations (cuStreamWriteValue32 /
   cuStreamWaitValue32 GEQ) on the same doorbells, in the GPU front-end.
 * failure: every in-kernel wait is bounded by the channel's timeout and can
   be aborted from the host (``PairChannel.abort``); the kernels then record
