@@ -729,8 +729,8 @@ cudaError_t launch_kivi_pull(const kvx::KchanGeo& kg, const kvx::Geo& gv, const 
   kvx::KchanBulk kb;
   kvx::BulkGeo bg;
   if (!plan_kchan_pull<BITS, G>(kg, ready, ready_value, layers_per_chunk, ctl, kb)) return cudaSuccess;
-  if (!plan_pull<BITS, G>(gv, vc, vs, vz, ready + KVX_KIVI_V_FLAGS, ready_value, layers_per_chunk,
-                          done, ctl, bg))
+  if (!plan_pull<BITS, G>(gv, vc, vs, vz, ready ? ready + KVX_KIVI_V_FLAGS : nullptr, ready_value,
+                          layers_per_chunk, done, ctl, bg))
     return cudaSuccess;
   const int stage = kb.stage_bytes > bg.stage_bytes ? kb.stage_bytes : bg.stage_bytes;
   const int smem = kStages * stage;
@@ -1117,7 +1117,7 @@ static int kivi_dequant(const void* payload, int64_t payload_layer_stride,
   cudaError_t e = cudaSuccess;
   bool fused = false;  // K groups and V rows in ONE pull kernel (pull_kivi_kernel)
   static const bool fuse_ok = std::getenv("KVX_KIVI_TWO_KERNELS") == nullptr;
-  if (bulk && ready && n_groups && fuse_ok) {
+  if (bulk && n_groups && fuse_ok) {
     kvx::KchanGeo kg;
     kg.k_plane = nullptr;
     kg.layer_stride_b = 0;

@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(288, 1) pull_kivi_kernel(KchanGeo kg, KchanBul
         uint8_t* buf = smem + st * stage_bytes;
         if (sp < nk) {
           const int64_t c = ((sp / kb.slabs) / kg.n_groups) / kb.layers_per_chunk;
-          if (ok && c > ready_k) {
+          if (kb.ready && ok && c > ready_k) {
             ok = wait_ready(kb.ready + c, kb.ready_value, kb.ctl);
             ready_k = c;
           }
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(288, 1) pull_kivi_kernel(KchanGeo kg, KchanBul
           const int64_t rsp = sp - nkv;
           const int64_t layer = rsp / kr.spans_per_layer;
           const int64_t c = layer / bg.layers_per_chunk;
-          if (ok && c > ready_v) {
+          if (bg.ready && ok && c > ready_v) {
             ok = wait_ready(bg.ready + c, bg.ready_value, bg.ctl);
             ready_v = c;
           }
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(288, 1) pull_kivi_kernel(KchanGeo kg, KchanBul
           const uint32_t vsp = uint32_t(sp - nk);
           const uint32_t layer = vsp / bg.spans_per_layer;
           const int64_t c = int64_t(layer) / bg.layers_per_chunk;
-          if (ok && c > ready_v) {
+          if (bg.ready && ok && c > ready_v) {
             ok = wait_ready(bg.ready + c, bg.ready_value, bg.ctl);
             ready_v = c;
           }

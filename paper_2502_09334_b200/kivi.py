@@ -11,6 +11,8 @@ lengths of the requests packed back to back in the batch.
 """
 from __future__ import annotations
 
+import os
+
 import ctypes
 from dataclasses import dataclass
 
@@ -196,6 +198,9 @@ class KiviHandoff:
         self.base = _round_up(self.buf.data_ptr())
         self.offs = _offsets_arg(lay)
         self.packed = PackedKiviKV(lay, self.buf, self.base, self.gs, self.rt)
+        # decode side: the per-lane kernels, or (A/B, KVX_KIVI_LOCAL_PULL=1)
+        # the single bulk-staged kivi pull kernel on the local payload
+        self.bulk = os.environ.get("KVX_KIVI_LOCAL_PULL") == "1"
 
     def run(self, timing: list | None = None) -> None:
         lay, s = self.layout, torch.cuda.current_stream()
@@ -212,11 +217,16 @@ class KiviHandoff:
         if ev is not None:
             ev[1].record(s)
         kc, vc = self.dst.ptrs(0)
-        _lib.call("kvx_dequant_scatter_paged_kivi", self.base, lay.layer_stride, self.offs,
-                  self.dst.slots_ptr, self.gs.data_ptr() if self.gs.numel() else None,
-                  self.gs.numel(), self.rdst.data_ptr() if self.rdst.numel() else None,
-                  self.rdst.numel(), lay.n_layers, lay.n_tokens, lay.n_heads, lay.head_dim,
-                  lay.group, lay.bits, kc, vc, self.dst.layer_stride, _stream_ptr(s))
+        args = (self.base, lay.layer_stride, self.offs,
+                self.dst.slots_ptr, self.gs.data_ptr() if self.gs.numel() else None,
+                self.gs.numel(), self.rdst.data_ptr() if self.rdst.numel() else None,
+                self.rdst.numel(), lay.n_layers, lay.n_tokens, lay.n_heads, lay.head_dim,
+                lay.group, lay.bits, kc, vc, self.dst.layer_stride)
+        if self.bulk:  # the single TMA-staged kivi pull kernel, reading local HBM
+            _lib.call("kvx_pull_dequant_scatter_paged_kivi", *args, None, 0, 1, None, None,
+                      None, 0, _stream_ptr(s))
+        else:
+            _lib.call("kvx_dequant_scatter_paged_kivi", *args, _stream_ptr(s))
         if ev is not None:
             ev[2].record(s)
             timing.append({"k1": (ev[0], ev[1]), "k3": (ev[1], ev[2])})
