@@ -855,7 +855,10 @@ __device__ __forceinline__ void k3_process(const K3Item& it, const K3Data<BITS>&
 // PACKED: the short-row item geometry (ItemGeo::rpi_shift > 0), a separate
 // instantiation so the common one keeps its register budget (48 vs 58).
 template <int BITS, int G, bool PACKED = false>
-__global__ void __launch_bounds__(256) dequant_scatter_kernel(Geo g, ItemGeo ig,
+#ifndef KVX_K3_MIN_BLOCKS
+#define KVX_K3_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(256, KVX_K3_MIN_BLOCKS) dequant_scatter_kernel(Geo g, ItemGeo ig,
                                                               const uint8_t* __restrict__ codes,
                                                               const __half* __restrict__ scale,
                                                               const __half* __restrict__ zero) {
