@@ -353,14 +353,6 @@ cudaError_t launch_dequant(const kvx::Geo& g, const void* codes, const void* sca
   kvx::ItemGeo ig;
   cudaError_t e = make_items(g, ig);
   if (e != cudaSuccess) return e;
-  static const bool co = std::getenv("KVX_K3_CO") != nullptr;  // A/B: coalesced stores
-  if (co && ig.rpi_shift == 0 && g.row_elems % 1024 == 0) {
-    auto kc = kvx::dequant_scatter_co_kernel<BITS, G>;
-    kc<<<grid_for(kc, ig.n_items), kThreads, 0, s>>>(g, ig, static_cast<const uint8_t*>(codes),
-                                                     static_cast<const __half*>(scale),
-                                                     static_cast<const __half*>(zero));
-    return cudaGetLastError();
-  }
   auto k = ig.rpi_shift ? kvx::dequant_scatter_kernel<BITS, G, true>
                         : kvx::dequant_scatter_kernel<BITS, G, false>;
   k<<<grid_for(k, ig.n_items), kThreads, 0, s>>>(g, ig, static_cast<const uint8_t*>(codes),

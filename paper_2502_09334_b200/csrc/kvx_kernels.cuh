@@ -892,85 +892,6 @@ __global__ void __launch_bounds__(256, KVX_K3_MIN_BLOCKS) dequant_scatter_kernel
   }
 }
 
-// K3 with coalesced stores (A/B: KVX_K3_CO=1).  Same items as K3 (token row,
-// block of 1024 elements), but lane l owns elements [16l, 16l+16) and
-// [512+16l, 512+16l+16) of the block: its two 32-byte stores land at
-// out + 32l and out + 1024 + 32l, so every warp-wide store instruction
-// writes 1 KB contiguous (eight whole 128-B lines) instead of 32 pieces
-// 64 B apart.  Rows must be whole multiples of 1024 elements.
-template <int BITS>
-struct Half16 {  // codes of 16 elements
-  static constexpr int BYTES = 16 * BITS / 8;
-};
-
-template <int BITS>
-__device__ __forceinline__ void k3co_load16(const char* p, uint32_t (&w)[4]) {
-  if constexpr (BITS == 4) {  // 8 bytes
-    asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];"
-                 : "=r"(w[0]), "=r"(w[1]) : "l"(p));
-  } else if constexpr (BITS == 8) {  // 16 bytes
-    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
-  } else {  // 4 bytes
-    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(w[0]) : "l"(p));
-  }
-}
-
-template <int BITS>
-__device__ __forceinline__ void k3co_store16(char* dst, const uint32_t (&w)[4], __half2 s2,
-                                             __half2 z2) {
-  U4 o[2];
-  if constexpr (BITS == 4) {
-    o[0] = dequant8<4>(w[0], s2, z2);
-    o[1] = dequant8<4>(w[1], s2, z2);
-  } else if constexpr (BITS == 8) {
-    o[0] = dequant8<8>(make_uint2(w[0], w[1]), s2, z2);
-    o[1] = dequant8<8>(make_uint2(w[2], w[3]), s2, z2);
-  } else {
-    o[0] = dequant8<2>(uint16_t(w[0]), s2, z2);
-    o[1] = dequant8<2>(uint16_t(w[0] >> 16), s2, z2);
-  }
-  st256(dst, o[0], o[1]);
-}
-
-template <int BITS, int G>
-__global__ void __launch_bounds__(256) dequant_scatter_co_kernel(Geo g, ItemGeo ig,
-                                                                 const uint8_t* __restrict__ codes,
-                                                                 const __half* __restrict__ scale,
-                                                                 const __half* __restrict__ zero) {
-  constexpr int HB = Half16<BITS>::BYTES;
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
-  const int e0 = lane * 16, e1 = 512 + lane * 16;  // this lane's elements in the block
-  for (uint32_t item = warp; item < ig.n_items; item += n_warps) {
-    const uint32_t tr = fdiv(item, ig.ipr);
-    const int blk = int(item - tr * ig.ipr.d);
-    const uint32_t lk = fdiv(tr, ig.tokens);
-    const uint32_t t = tr - lk * ig.tokens.d;
-    const uint32_t layer = lk >> (g.planes - 1);
-    const int kv = g.plane0 + int(lk - (layer << (g.planes - 1)));
-    const uint32_t lrow = tr - layer * g.planes * ig.tokens.d;
-    const int64_t pos = pos_of(g, t);
-    const int64_t re = int64_t(lrow) * g.row_elems + int64_t(blk) * 1024;  // payload element
-    const char* cb = reinterpret_cast<const char*>(codes) + int64_t(layer) * g.codes_ls;
-    const __half* sb = reinterpret_cast<const __half*>(reinterpret_cast<const char*>(scale) +
-                                                      int64_t(layer) * g.meta_ls);
-    const __half* zb = reinterpret_cast<const __half*>(reinterpret_cast<const char*>(zero) +
-                                                      int64_t(layer) * g.meta_ls);
-    uint32_t w0[4], w1[4];
-    k3co_load16<BITS>(cb + (re + e0) * BITS / 8, w0);
-    k3co_load16<BITS>(cb + (re + e1) * BITS / 8, w1);
-    const __half s0 = __ldg(sb + (re + e0) / G), z0 = __ldg(zb + (re + e0) / G);
-    const __half s1 = __ldg(sb + (re + e1) / G), z1 = __ldg(zb + (re + e1) / G);
-    if (pos < 0) continue;  // padding token (warp-uniform: one row per item)
-    char* out = const_cast<char*>(row_ptr(g, plane_ptr(g, kv, layer), pos)) + int64_t(blk) * 2048;
-    k3co_store16<BITS>(out + lane * 32, w0, __half2half2(s0), __half2half2(z0));
-    k3co_store16<BITS>(out + 1024 + lane * 32, w1, __half2half2(s1), __half2half2(z1));
-    (void)HB;
-  }
-}
-
 // 16-bit passthrough on the decode side: scatter the raw fp16 rows.
 template <int UNROLL>
 __global__ void __launch_bounds__(256) scatter16_kernel(Geo g, const uint8_t* __restrict__ in) {
