@@ -80,15 +80,21 @@ def unpack_dequant_scalar(codes, scale, zero, bits: int, group: int, head_dim: i
     return out
 
 
-def quant_pack(x: np.ndarray, bits: int = 4, group: int = 128):
+def quant_pack(x: np.ndarray, bits: int = 4, group: int = 128, out=None):
+    """``out=(codes, scale, zero)``: preallocated outputs (bench.py reuses them,
+    so the timed loop does not fault fresh pages in on every layer)."""
     x = np.ascontiguousarray(x, dtype=np.float16)
     rows, d = x.shape
     if bits == 16:
         return x.view(np.uint8).reshape(rows, -1).copy(), None, None
     ng = d // group
-    codes = np.empty((rows, d * bits // 8), np.uint8)
-    scale = np.empty((rows, ng), np.float16)
-    zero = np.empty((rows, ng), np.float16)
+    if out is not None:
+        codes, scale, zero = out
+        assert codes.shape == (rows, d * bits // 8) and scale.shape == zero.shape == (rows, ng)
+    else:
+        codes = np.empty((rows, d * bits // 8), np.uint8)
+        scale = np.empty((rows, ng), np.float16)
+        zero = np.empty((rows, ng), np.float16)
     rc = lib().kvq_quant_pack(_p(x), rows, d, group, bits, _p(codes), _p(scale), _p(zero))
     if rc:
         raise ValueError(f"kvq_quant_pack rc={rc}")
