@@ -316,6 +316,36 @@ def main():
     dist.barrier()
     ch.close()
 
+    # latency mode (gate_send=False): consecutive K1s chained with PDL, the
+    # slot waited for in-kernel only; queue depths 2 and 4, bit-exact
+    for Q in (2, 4):
+        spec = ChannelSpec(L, Tmax, H, D, 4, 128, 3, "pull", queue_depth=Q, gate_send=False)
+        ch = PairChannel(spec, rank, world, control_group=ctrl)
+        nbl = Tmax // bs + 4
+        if ch.role == "decode":
+            kcl = torch.zeros((L, nbl, bs, H, D), dtype=torch.float16, device=dev)
+            vcl = torch.zeros_like(kcl)
+        for i, T in enumerate([Tmax, 1, 77, Tmax, 16, 130] * 2):
+            g = torch.Generator(device=dev).manual_seed(4000 + 10 * Q + i + 1000 * ch.pair)
+            kv = torch.randn((L, 2, T, H, D), generator=g, device=dev).half()
+            if ch.role == "prefill":
+                ch.send(KVPlanes.dense(kv), T)
+            else:
+                sl = torch.randperm(nbl * bs, generator=torch.Generator().manual_seed(i))[:T].to(dev)
+                kcl.zero_(); vcl.zero_()
+                ch.recv(KVPlanes.paged(kcl, vcl, sl), T)
+                rk, rv = _mp.local_reference(kv, kcl.shape, sl)
+                torch.cuda.synchronize()
+                if not (torch.equal(kcl, rk) and torch.equal(vcl, rv)):
+                    failures += 1
+                    print(f"MISMATCH latency-mode Q={Q} rank={rank} i={i} T={T}", flush=True)
+        torch.cuda.synchronize()
+        ch.check()
+        dist.barrier()
+        ch.close()
+    if rank == 0:
+        print("latency mode: ok", flush=True)
+
     # shape-agnostic channel (VERDICT weak #4): hundreds of random-length
     # hand-offs, each with a FRESH slot tensor, one native launch per end;
     # no per-shape state grows (no graphs; the fused-plan memo is bounded) and
@@ -347,6 +377,7 @@ def main():
     torch.cuda.synchronize()
     ch.check()
     state = len(getattr(ch, "_fused_memo", {}))
+    ch.check()
     if hasattr(ch, "_graphs") or state > len(set(Ts)):
         failures += 1
         print(f"STATE rank={rank}: per-shape state grew ({state} memo entries)", flush=True)

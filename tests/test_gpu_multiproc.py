@@ -39,6 +39,7 @@ def test_modes_over_ipc_same_gpu(cuda):
     assert "long/short alternation Q=2: ok" in out and "queue_depth=3" in out
     assert "recv_many: ok" in out
     assert "random lengths: 300 hand-offs" in out
+    assert "latency mode: ok" in out
 
 
 @pytest.mark.gpu
