@@ -434,13 +434,6 @@ bool plan_pull(const kvx::Geo& g, const void* codes, const void* scale, const vo
   r = r / m * m;
   if (r < m) r = m;
   if (r > two_t) r = two_t;
-  // short hand-offs: a whole layer per span when it fits in two stage
-  // targets -- no CTA then pulls a second, tiny span of the same layer
-  // after the first (the tail of a 16-token hand-off)
-#ifndef KVX_NO_LAYER_SPANS
-  if (r < two_t && two_t * (bg.code_row_bytes + 2 * bg.meta_row_bytes) <= 2 * kBulkStageTarget)
-    r = two_t;
-#endif
   bg.rows_per_span = int(r);
   bg.stage_bytes = bg.rows_per_span * (bg.code_row_bytes + 2 * bg.meta_row_bytes);
   if (kBulkStages * bg.stage_bytes > 200 * 1024) return false;
