@@ -781,6 +781,9 @@ class PairChannel:
             return
         if len(items) > self.Q:
             raise ValueError(f"recv_many: {len(items)} hand-offs > queue depth {self.Q}")
+        if self.spec.format == "kivi":
+            raise ValueError("recv_many: the kivi format needs each hand-off's seqlens; "
+                             "use recv(..., seqlens=...) per hand-off")
         self.check()
         d0 = items[0][0]
         key = (d0.k.data_ptr(), d0.v.data_ptr(), d0.layer_stride, d0.plane_heads or d0.n_heads,

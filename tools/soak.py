@@ -102,6 +102,55 @@ def run_config(rank, world, dev, ctrl, Q, gate, L, H, D, Tmax, seconds, seed):
             "checks": checks, "mismatches": bad}
 
 
+def run_kivi(rank, world, dev, ctrl, L, H, D, Tmax, seconds, seed):
+    """kivi format: ragged batches of 1-4 requests (residual rows in most),
+    one fused prefill call and one pull kernel per hand-off; every round
+    checked against the local kivi round trip (compress_kivi ->
+    decompress_kivi_into_paged, oracle-pinned in tests/test_gpu_kivi.py)."""
+    from paper_2502_09334_b200.kivi import compress_kivi, decompress_kivi_into_paged
+    spec = ChannelSpec(L, Tmax, H, D, 4, 32, 8, "pull", format="kivi", queue_depth=2)
+    ch = PairChannel(spec, rank, world, control_group=ctrl)
+    bs = 16
+    nb = Tmax // bs + 8
+    rng = np.random.default_rng(seed)
+    if ch.role == "decode":
+        kc = torch.zeros((L, nb, bs, H, D), dtype=torch.float16, device=dev)
+        vc = torch.zeros_like(kc)
+        rk = torch.zeros_like(kc)
+        rv = torch.zeros_like(kc)
+    handoffs = checks = bad = 0
+    t_end = time.time() + seconds
+    stop = False
+    while not stop:
+        n_req = int(rng.integers(1, 5))
+        seq = tuple(int(x) for x in rng.integers(1, Tmax // 4 + 1, size=n_req))
+        T = sum(seq)
+        sd = int(rng.integers(0, 1 << 30))
+        g = torch.Generator(device=dev).manual_seed(sd)
+        kv = torch.randn((L, 2, T, H, D), generator=g, device=dev).half()
+        perm = rng.permutation(nb * bs)[:T]
+        if ch.role == "prefill":
+            ch.send(KVPlanes.dense(kv), T, seqlens=seq)
+        else:
+            sl = torch.from_numpy(perm.astype(np.int64)).to(dev)
+            kc.zero_(); vc.zero_(); rk.zero_(); rv.zero_()
+            ch.recv(KVPlanes.paged(kc, vc, sl), T, seqlens=seq)
+            decompress_kivi_into_paged(compress_kivi(kv, 4, 32, seq), rk, rv, sl)
+            torch.cuda.synchronize()
+            checks += 1
+            if not (torch.equal(kc, rk) and torch.equal(vc, rv)):
+                bad += 1
+                print(f"MISMATCH kivi rank={rank} seq={seq}", flush=True)
+        handoffs += 1
+        if handoffs % 20 == 0:
+            stop = exchange(time.time() > t_end, ctrl)[0]
+    torch.cuda.synchronize()
+    ch.check()
+    dist.barrier(ctrl)
+    ch.close()
+    return {"format": "kivi", "handoffs": handoffs, "checks": checks, "mismatches": bad}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=120.0)
@@ -109,13 +158,17 @@ def main():
     rank, world, dev, ctrl, _ = _mp.init()
     out = []
     configs = [(2, True), (4, False), (8, False), (3, True)]
+    share = a.seconds / (len(configs) + 1)
     for i, (Q, gate) in enumerate(configs):
         out.append(run_config(rank, world, dev, ctrl, Q, gate, L=8, H=8, D=128, Tmax=2048,
-                              seconds=a.seconds / len(configs), seed=1000 + i))
+                              seconds=share, seed=1000 + i))
+    out.append(run_kivi(rank, world, dev, ctrl, L=8, H=8, D=128, Tmax=2048, seconds=share,
+                        seed=99))
     res = exchange(out, ctrl)
     if rank == 0:
         dec = res[1]
         print(json.dumps({"soak": dec, "total_handoffs": sum(r["handoffs"] for r in dec),
+                          "total_checks": sum(r["checks"] for r in dec),
                           "total_mismatches": sum(r["mismatches"] for r in dec)}), flush=True)
     dist.destroy_process_group()
 
