@@ -634,6 +634,9 @@ class PairChannel:
         launch consumes the chunks as their doorbells ring."""
         if self.role != "prefill" or self.spec.mode not in PULL_MODES:
             raise RuntimeError("open_send needs the prefill end of a pull channel")
+        if self.spec.format == "kivi":
+            raise ValueError("layer-wise streaming carries the default format only "
+                             "(the kivi K groups span a request's tokens, not layers)")
         self.check()
         self.spec.check_planes(src, n_tokens, "source")
         return SendSession(self, src, n_tokens)
