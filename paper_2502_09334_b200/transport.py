@@ -335,7 +335,9 @@ class PairChannel:
         """``edge=(prefill_rank, decode_rank)`` overrides the default pairing
         (TP regroups, see TPHandoff).  Construction is collective over the
         control group: ranks outside the edge take part in the handle exchange
-        and get an inert channel (``role is None``)."""
+        and get an inert channel (``role is None``).  ``data_group`` is
+        accepted for round-1 callers and unused: the "nccl" mode builds its
+        own 2-rank communicator through the C-ABI."""
         self.spec = spec
         self.rank, self.world = rank, world
         self._pair = None
@@ -355,7 +357,6 @@ class PairChannel:
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.stream = torch.cuda.Stream(self.device)    # kernels (non-fused paths)
         self.cstream = torch.cuda.Stream(self.device)   # copy engine / NCCL
-        self.data_group = data_group
         self.epoch = 0
         self.Q = spec.queue_depth if spec.mode in PULL_MODES else 1
         self._prev_ranges = None
