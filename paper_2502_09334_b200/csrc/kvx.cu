@@ -368,9 +368,7 @@ cudaError_t launch_dequant(const kvx::Geo& g, const void* codes, const void* sca
 #define KVX_BULK_STAGE_BYTES 12288
 #endif
 constexpr int kBulkStages = KVX_BULK_STAGES;
-#ifndef KVX_BULK_DEEP_STAGES
-#define KVX_BULK_DEEP_STAGES 6  // ring depth for short pulls (0 = always kBulkStages)
-#endif
+
 constexpr int kBulkThreads = 288;
 // code bytes per stage: 4 x 12 KB in flight per SM.  A/B at one CTA per SM
 // (N=2, GB/s fp16-eq, cfg3 / cfg4 pair): 8 KB 2,833 / 2,867; 12 KB 2,945 /
@@ -488,22 +486,6 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
-#if KVX_BULK_DEEP_STAGES > 0
-  // Short pulls (every CTA owns at most KVX_BULK_DEEP_STAGES spans): a
-  // deeper ring lets a PDL-launched pull request ALL of its spans while the
-  // previous pull drains, so the link never waits on the stream-order
-  // handoff between two short hand-offs.  Two such CTAs still fit one SM
-  // (this one and the next pull's).
-  constexpr int kDeep = KVX_BULK_DEEP_STAGES;
-  if (n_spans <= grid * kDeep && kDeep * bg.stage_bytes <= 110 * 1024) {
-    auto kd = kvx::pull_dequant_scatter_kernel<BITS, G, kDeep>;
-    cudaError_t a2 = ensure_smem_attr(kd, 200 * 1024);
-    if (a2 != cudaSuccess) return a2;
-    cfg.dynamicSmemBytes = size_t(kDeep * bg.stage_bytes);
-    return cudaLaunchKernelEx(&cfg, kd, g, bg, static_cast<const uint8_t*>(codes),
-                              static_cast<const __half*>(scale), static_cast<const __half*>(zero));
-  }
-#endif
   return cudaLaunchKernelEx(&cfg, k, g, bg, static_cast<const uint8_t*>(codes),
                             static_cast<const __half*>(scale), static_cast<const __half*>(zero));
 }
