@@ -212,6 +212,41 @@ def cpu_reference(workload: str, bits: int, group: int, budget_s: float | None =
                        f"{C.threads()} OpenMP threads on {cpu_model()}, {elapsed:.2f} s")
 
 
+def cpu_torch_variant(workload: str, bits: int, group: int, budget_s: float = 5.0):
+    """The torch-CPU variant SURVEY.md 8(d) asks for next to the C baseline:
+    oracle/kvq_torch_cpu.py (the same arithmetic in torch ops, bit-identical
+    to the oracle) with torch's intra-op pool on every usable core, layer by
+    layer over the workload until ``budget_s``."""
+    import torch
+    from oracle import kvq_torch_cpu as TC
+    L, H, D, b, s = WORKLOADS[workload]
+    T = b * s
+    nb = (T + BLOCK - 1) // BLOCK
+    threads = len(os.sched_getaffinity(0))
+    prev = torch.get_num_threads()
+    torch.set_num_threads(threads)
+    try:
+        slots = torch.from_numpy(_CPU_LAYERS[("dst", workload)][0]) if ("dst", workload) in \
+            _CPU_LAYERS else torch.randperm(nb * BLOCK)[:T]
+        kc = torch.zeros((nb, BLOCK, H, D), dtype=torch.float16)
+        vc = torch.zeros_like(kc)
+        layers, elapsed = 0, 0.0
+        while elapsed < budget_s and layers < 4 * L:
+            kv = torch.from_numpy(_cpu_layer(workload, layers % L, T, H, D)).reshape(-1, D)
+            t0 = time.perf_counter()
+            c, sc, z = TC.quant_pack(kv, bits, group)
+            TC.dequant_scatter_paged(c, sc, z, slots, T, H, D, group, bits, kc, vc)
+            elapsed += time.perf_counter() - t0
+            layers += 1
+    finally:
+        torch.set_num_threads(prev)
+    fp16_bytes = layers * 2 * T * H * D * 2
+    return {"value": round(fp16_bytes / elapsed / 1e9, 4), "unit": UNIT, "threads": threads,
+            "sample": f"{layers} layers of {workload} ({fp16_bytes / 1e9:.2f} GB fp16), "
+                      f"oracle/kvq_torch_cpu.py (torch {torch.__version__} CPU ops, "
+                      f"{threads} intra-op threads), {elapsed:.2f} s"}
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -380,6 +415,8 @@ def run_local(args, torch):
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_reference(wl, args.bits, args.group, budget_s=args.cpu_budget)
+        if args.bits != 16 and args.format == "default":
+            cpu["torch_cpu"] = cpu_torch_variant(wl, args.bits, args.group)
     traffic = ncu_traffic(wl, args, dom)
     return dict(
         value=value, ms=ms, workload=wl, fp16_bytes=fp16_bytes, wire_bytes=lay.wire_bytes,

@@ -256,3 +256,66 @@ def test_oracle_volume_model_matches_reference_golden():
         O.kv_volume_bytes(1, 1, 1, 1, 3)
     with pytest.raises(ValueError):
         O.kv_volume_bytes(0, 1, 1, 1, 4)
+
+
+# ---------------------------------------------------------------------------
+# The torch-CPU variant of the CPU path equals the oracle
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("patterns", [False, True])
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("group", [32, 64, 128])
+def test_torch_cpu_variant_equals_oracle(bits, group, patterns):
+    import torch
+    from oracle import kvq_torch_cpu as TC
+    x = _random_rows(3000, 500 + bits * 7 + group, patterns)
+    a = O.quant_pack(x, bits, group)
+    b = TC.quant_pack(torch.from_numpy(x), bits, group)
+    for p, q in zip(a, b):
+        assert np.array_equal(np.asarray(p).view(np.uint8), q.numpy().view(np.uint8))
+    da = O.unpack_dequant(*a, bits, group, 128)
+    db = TC.unpack_dequant(*b, bits, group, 128).numpy()
+    assert np.array_equal(h16(da), h16(db))
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_torch_cpu_dequant_arbitrary_scale_zero(bits):
+    """Arbitrary finite scale/zero bit patterns: the float64 -> float16 step
+    (round-to-odd float32, then RN) rounds once, like numpy."""
+    import torch
+    from oracle import kvq_torch_cpu as TC
+    rng = np.random.default_rng(300 + bits)
+    rows, group = 20000, 32
+    codes = rng.integers(0, 256, size=(rows, 128 * bits // 8), dtype=np.uint8)
+
+    def meta():
+        m = rng.integers(0, 0x10000, size=(rows, 128 // group), dtype=np.uint16).view(np.float16)
+        return np.where(np.isfinite(m), m, np.float16(1))
+    s, z = np.abs(meta()), meta()
+    a = O.unpack_dequant(codes, s, z, bits, group, 128)
+    b = TC.unpack_dequant(torch.from_numpy(codes), torch.from_numpy(s), torch.from_numpy(z),
+                          bits, group, 128).numpy()
+    assert np.array_equal(h16(a), h16(b))
+
+
+def test_torch_cpu_golden_groups_and_scatter():
+    import torch
+    from oracle import kvq_torch_cpu as TC
+    g = np.load(os.path.join(GOLD, "groups.npz"))
+    for bits in (2, 4, 8):
+        c, s, z = TC.quant_pack(torch.from_numpy(g["x"]), bits, 128)
+        assert np.array_equal(c.numpy(), g[f"codes{bits}"])
+        assert np.array_equal(h16(s.numpy()), h16(g[f"scale{bits}"]))
+        d = TC.unpack_dequant(c, s, z, bits, 128, 128).numpy()
+        assert np.array_equal(h16(d), h16(g[f"deq{bits}"]))
+    T, H, D, nb, bs = 37, 4, 128, 8, 16
+    kv = O.synthetic_kv(1, T, H, D, seed=4)
+    slots = O.synthetic_slots(T, bs, nb, seed=4)
+    slots[3] = -1
+    c, s, z = O.quant_pack(kv.reshape(-1, D), 4, 64)
+    kc = np.zeros((1, nb, bs, H, D), np.float16); vc = np.zeros_like(kc)
+    C.dequant_scatter_paged(c, s, z, slots, 1, T, H, D, 64, 4, kc, vc)
+    kt = torch.zeros((nb, bs, H, D), dtype=torch.float16); vt = torch.zeros_like(kt)
+    TC.dequant_scatter_paged(torch.from_numpy(c), torch.from_numpy(s), torch.from_numpy(z),
+                             torch.from_numpy(slots), T, H, D, 64, 4, kt, vt)
+    assert np.array_equal(h16(kc[0]), h16(kt.numpy())) and np.array_equal(h16(vc[0]), h16(vt.numpy()))
