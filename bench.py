@@ -312,6 +312,19 @@ def base_config(wl, bits, group, fmt, fp16_bytes):
             "format": fmt, "l2": l2}
 
 
+def _pair_roofline(fp16: float, wire: float, hbm_gbs: float, ms: float) -> dict:
+    """Per pair and step: the link, prefill-HBM and decode-HBM times at the
+    measured peaks, the bound among them and the step's fraction of it."""
+    t = {"link": wire / (NVLINK_GBS * 1e9) * 1e3,
+         "prefill_hbm": (fp16 + 2 * wire) / (hbm_gbs * 1e9) * 1e3,
+         "decode_hbm": fp16 / (hbm_gbs * 1e9) * 1e3}
+    bound = max(t, key=t.get)
+    return {"step_roofline_ms": round(t[bound], 4), "step_bound": bound,
+            "step_frac": round(t[bound] / ms, 4),
+            "link_ms": round(t["link"], 4), "prefill_hbm_ms": round(t["prefill_hbm"], 4),
+            "decode_hbm_ms": round(t["decode_hbm"], 4)}
+
+
 def default_pair_workload(world: int) -> str:
     return "cfg3_13b_2048x8" if world == 2 else "cfg4_70b_gqa_pair"
 
@@ -735,7 +748,11 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                       "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
                       "k3_link_gbs": round(k3_link, 1) if k3_link else None,
                       "frac_of_nominal_900": round(link_gbs / 900.0, 4),
-                      "hbm_peak": hbm},
+                      "hbm_peak": hbm,
+                      # the pair's roofline is max(NVLink time,
+                      # busiest-GPU HBM time).  P's HBM: K1 reads fp16 and
+                      # writes the payload, the pull reads it; D's: fp16 writes
+                      **_pair_roofline(per_step * fp16, per_step * wire, hbm, ms_max)},
             calibration=_calibration(spec, T, ms_max, float(g[:, 7].max()),
                                      host_us=float(g[:, 8].max())) if (
                 trace is None and not kivi) else None,
