@@ -40,3 +40,16 @@ def test_trace_is_deterministic_and_bounded():
     for lens in a:
         assert 1 <= len(lens) <= 16 and sum(lens) <= bench.TRACE_CAP
         assert all(128 <= n <= 8192 for n in lens)
+
+
+def test_pair_roofline_is_max_of_link_and_hbm():
+    """a pair's roofline is max(NVLink time, busiest-GPU HBM time)."""
+    fp16 = 13_421_772_800  # config 3
+    r4 = bench._pair_roofline(fp16, 3_565_158_400, 6538.3, 4.6117)  # 4-bit G=128
+    assert r4["step_bound"] == "link"
+    assert abs(r4["link_ms"] - 3_565_158_400 / 783e9 * 1e3) < 1e-3
+    assert r4["step_frac"] == round(r4["link_ms"] / 4.6117, 4)
+    r2 = bench._pair_roofline(fp16, 2_097_152_000, 6538.3, 3.1243)  # 2-bit G=64
+    assert r2["step_bound"] == "prefill_hbm"
+    assert abs(r2["prefill_hbm_ms"] - (fp16 + 2 * 2_097_152_000) / 6538.3e9 * 1e3) < 1e-3
+    assert r2["step_roofline_ms"] >= max(r2["link_ms"], r2["decode_hbm_ms"])
