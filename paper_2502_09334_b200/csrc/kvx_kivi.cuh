@@ -33,15 +33,135 @@ struct KchanSignal {
   uint32_t ready_value;
 };
 
-// G/16 lanes own 8 adjacent channels x G tokens: each lane loads 16 of the
-// group's tokens with 16-byte loads (a warp reads 256-byte row segments),
-// min/max is reduced over its tokens and then across the lanes with
-// log2(G/16) shuffles, and each lane quantises its own tokens from registers
-// (8 nibbles = one 32-bit store per token at 4-bit).
-template <int BITS, int G>
-__global__ void __launch_bounds__(128) quant_pack_kchan_kernel(KchanGeo g, KchanSignal sig) {
+// One lane's share of a per-channel K group: TH of the group's G tokens x 8
+// adjacent channels (w[j] = token j's 8 fp16), the G / TH lanes of a group
+// adjacent in the warp.  min/max over the lane's tokens, then across the
+// group's lanes with log2(G / TH) shuffles; the group's lanes split the 8
+// channels' IEEE division and reciprocal between them and share the results
+// (K1-kivi 1.99 -> 1.78 ms at N=1 config 2, profiles/r02_bench/kchan_ab_n1.log);
+// the lane with half == 0 stores the 8 scales and zeros (16 B each), every
+// lane quantises its own tokens
+// (8 nibbles = one 32-bit store per token at 4-bit).  Warp-uniform call:
+// inactive lanes (channels past the row) take part in the shuffles.
+template <int BITS, int G, int TH>
+__device__ __forceinline__ void kchan_quant_lanes(const KchanGeo& g, const uint4 (&w)[TH],
+                                                  bool active, int half, int64_t layer, int64_t k,
+                                                  int ch) {
   constexpr uint32_t QMAX = (1u << BITS) - 1u;
   constexpr float QMAXF = float(QMAX);
+  constexpr int LPC = G / TH;
+  __half2 mn[4], mx[4];
+  mn[0] = mx[0] = u32_as_h2(w[0].x);
+  mn[1] = mx[1] = u32_as_h2(w[0].y);
+  mn[2] = mx[2] = u32_as_h2(w[0].z);
+  mn[3] = mx[3] = u32_as_h2(w[0].w);
+#pragma unroll
+  for (int j = 1; j < TH; ++j) {
+    const uint32_t v[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mn[i] = __hmin2(mn[i], u32_as_h2(v[i]));
+      mx[i] = __hmax2(mx[i], u32_as_h2(v[i]));
+    }
+  }
+#pragma unroll
+  for (int off = 1; off < LPC; off <<= 1)  // combine the lanes' token slices
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mn[i] = __hmin2(mn[i], u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(mn[i]), off)));
+      mx[i] = __hmax2(mx[i], u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(mx[i]), off)));
+    }
+  // scale / zero / reciprocal of the 8 channels: the group's LPC lanes hold
+  // the same min/max, so each computes 8 / LPC of the channels (IEEE
+  // division and reciprocal are the costly part) and the results are shared
+  // with one shuffle per channel and value
+  constexpr int PER = 8 / LPC > 0 ? 8 / LPC : 1;
+  float lzf[PER], linv[PER];
+  uint32_t lsz[PER];  // (scale16, zero16) of the lane's channels
+  bool sub = false;
+#pragma unroll
+  for (int m = 0; m < PER; ++m) {
+    const int c = LPC >= 8 ? half : m * LPC + half;  // this lane's m-th channel
+    const __half2 mnp = mn[0], mxp = mx[0];
+    float fmn = __low2float(mnp), fmx = __low2float(mxp);
+#pragma unroll
+    for (int cc = 1; cc < 8; ++cc)  // select channel c without dynamic register indexing
+      if (cc == c) {
+        fmn = (cc & 1) ? __high2float(mn[cc >> 1]) : __low2float(mn[cc >> 1]);
+        fmx = (cc & 1) ? __high2float(mx[cc >> 1]) : __low2float(mx[cc >> 1]);
+      }
+    const __half z16 = __float2half_rn(__fadd_rn(fmn, 0.0f));
+    const __half s16 = __float2half_rn(__fadd_rn(__fdiv_rn(__fsub_rn(fmx, fmn), QMAXF), 0.0f));
+    const float sv = __half2float(s16);
+    linv[m] = (sv != 0.0f) ? __frcp_rn(sv) : 0.0f;
+    lzf[m] = __half2float(z16);
+    lsz[m] = h2_as_u32(__halves2half2(s16, z16));
+    sub |= sv != 0.0f && sv < 6.103515625e-05f;
+  }
+  float zf[8], inv[8];
+  uint32_t sz[8];
+  const int base = (threadIdx.x & 31) & ~(LPC - 1);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int m = LPC >= 8 ? 0 : c / LPC;
+    const int src = base + (LPC >= 8 ? c : c % LPC);
+    zf[c] = __shfl_sync(0xffffffffu, lzf[m], src);
+    inv[c] = __shfl_sync(0xffffffffu, linv[m], src);
+    sz[c] = __shfl_sync(0xffffffffu, lsz[m], src);
+  }
+  const bool clamp = __any_sync(0xffffffffu, active && sub);
+  if (!active) return;
+  char* lc = g.codes + layer * g.payload_ls;
+  if (half == 0) {  // one lane of the group writes the 8 scales / zeros (16 B each)
+    const int64_t meta = (k * g.row_elems + ch) * 2;
+    uint4 sv, zv;  // sz[c] = (scale16, zero16): low halves -> scales, high -> zeros
+    sv.x = prmt(sz[0], sz[1], 0x5410); sv.y = prmt(sz[2], sz[3], 0x5410);
+    sv.z = prmt(sz[4], sz[5], 0x5410); sv.w = prmt(sz[6], sz[7], 0x5410);
+    zv.x = prmt(sz[0], sz[1], 0x7632); zv.y = prmt(sz[2], sz[3], 0x7632);
+    zv.z = prmt(sz[4], sz[5], 0x7632); zv.w = prmt(sz[6], sz[7], 0x7632);
+    *reinterpret_cast<uint4*>(g.scale + layer * g.payload_ls + meta) = sv;
+    *reinterpret_cast<uint4*>(g.zero + layer * g.payload_ls + meta) = zv;
+  }
+  unsigned long long invv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    asm("mov.b64 %0, {%1, %2};" : "=l"(invv[i]) : "f"(inv[2 * i]), "f"(inv[2 * i + 1]));
+#pragma unroll
+  for (int j = 0; j < TH; ++j) {
+    const uint32_t v[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
+    uint32_t b[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      unsigned long long x, r;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(sub_lo(v[i], zf[2 * i])), "f"(sub_hi(v[i], zf[2 * i + 1])));
+      asm("{.reg .b64 mg; mov.b64 mg, {%3, %3}; fma.rn.f32x2 %0, %1, %2, mg;}"
+          : "=l"(r) : "l"(x), "l"(invv[i]), "f"(8388608.0f));
+      b[2 * i] = uint32_t(r);
+      b[2 * i + 1] = uint32_t(r >> 32);
+    }
+    if (clamp) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) b[i] = min(b[i] - 0x4B000000u, QMAX);
+    }
+    const int64_t row = k * G + half * TH + j;  // group-major payload row
+    char* dst = lc + (row * g.row_elems + ch) * BITS / 8;
+    if constexpr (BITS == 4) {
+      *reinterpret_cast<uint32_t*>(dst) =
+          bytes4(lea4(b[1], b[0]), lea4(b[3], b[2]), lea4(b[5], b[4]), lea4(b[7], b[6]));
+    } else {
+      *reinterpret_cast<uint2*>(dst) =
+          make_uint2(bytes4(b[0], b[1], b[2], b[3]), bytes4(b[4], b[5], b[6], b[7]));
+    }
+  }
+}
+
+// G/16 lanes own 8 adjacent channels x G tokens, each lane loading 16 of the
+// group's tokens with 16-byte loads (a warp reads 256-byte row segments).
+// (A TMA-staged variant -- G row copies per (group, channel block) span into
+// a shared-memory ring -- measured 1-21 % slower: the K1 step is bound by
+// issue slots, not by loads in flight; profiles/r02_bench/kchan_ab_n1.log.)
+template <int BITS, int G>
+__global__ void __launch_bounds__(128) quant_pack_kchan_kernel(KchanGeo g, KchanSignal sig) {
   constexpr int TH = 16;      // tokens per lane (16 x 16 B = 64 registers of data)
   constexpr int LPC = G / TH;  // lanes sharing one 8-channel block (2 at G=32, 4 at G=64)
   constexpr int CTA_CH = 4 * (32 / LPC) * 8;  // channels per 128-thread CTA
@@ -70,86 +190,7 @@ __global__ void __launch_bounds__(128) quant_pack_kchan_kernel(KchanGeo g, Kchan
         w[j] = make_uint4(0, 0, 0, 0);
       }
     }
-    __half2 mn[4], mx[4];
-    mn[0] = mx[0] = u32_as_h2(w[0].x);
-    mn[1] = mx[1] = u32_as_h2(w[0].y);
-    mn[2] = mx[2] = u32_as_h2(w[0].z);
-    mn[3] = mx[3] = u32_as_h2(w[0].w);
-#pragma unroll
-    for (int j = 1; j < TH; ++j) {
-      const uint32_t v[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        mn[i] = __hmin2(mn[i], u32_as_h2(v[i]));
-        mx[i] = __hmax2(mx[i], u32_as_h2(v[i]));
-      }
-    }
-#pragma unroll
-    for (int off = 1; off < LPC; off <<= 1)  // combine the lanes' token slices
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        mn[i] = __hmin2(mn[i], u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(mn[i]), off)));
-        mx[i] = __hmax2(mx[i], u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(mx[i]), off)));
-      }
-    float zf[8], inv[8];
-    __half z16[8], s16[8];
-    bool sub = false;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const float fmn = (c & 1) ? __high2float(mn[c >> 1]) : __low2float(mn[c >> 1]);
-      const float fmx = (c & 1) ? __high2float(mx[c >> 1]) : __low2float(mx[c >> 1]);
-      z16[c] = __float2half_rn(__fadd_rn(fmn, 0.0f));
-      s16[c] = __float2half_rn(__fadd_rn(__fdiv_rn(__fsub_rn(fmx, fmn), QMAXF), 0.0f));
-      const float sv = __half2float(s16[c]);
-      inv[c] = (sv != 0.0f) ? __frcp_rn(sv) : 0.0f;
-      zf[c] = __half2float(z16[c]);
-      sub |= sv != 0.0f && sv < 6.103515625e-05f;
-    }
-    const bool clamp = __any_sync(0xffffffffu, active && sub);
-    if (active) {
-      char* lc = g.codes + layer * g.payload_ls;
-      if (half == 0) {  // one lane of the pair writes the 8 scales / zeros (16 B each)
-        const int64_t meta = (k * g.row_elems + ch) * 2;
-        uint4 sv, zv;
-        sv.x = h2_as_u32(__halves2half2(s16[0], s16[1])); sv.y = h2_as_u32(__halves2half2(s16[2], s16[3]));
-        sv.z = h2_as_u32(__halves2half2(s16[4], s16[5])); sv.w = h2_as_u32(__halves2half2(s16[6], s16[7]));
-        zv.x = h2_as_u32(__halves2half2(z16[0], z16[1])); zv.y = h2_as_u32(__halves2half2(z16[2], z16[3]));
-        zv.z = h2_as_u32(__halves2half2(z16[4], z16[5])); zv.w = h2_as_u32(__halves2half2(z16[6], z16[7]));
-        *reinterpret_cast<uint4*>(g.scale + layer * g.payload_ls + meta) = sv;
-        *reinterpret_cast<uint4*>(g.zero + layer * g.payload_ls + meta) = zv;
-      }
-      unsigned long long invv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        asm("mov.b64 %0, {%1, %2};" : "=l"(invv[i]) : "f"(inv[2 * i]), "f"(inv[2 * i + 1]));
-#pragma unroll
-      for (int j = 0; j < TH; ++j) {
-        const uint32_t v[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
-        uint32_t b[8];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          unsigned long long x, r;
-          asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(sub_lo(v[i], zf[2 * i])), "f"(sub_hi(v[i], zf[2 * i + 1])));
-          asm("{.reg .b64 mg; mov.b64 mg, {%3, %3}; fma.rn.f32x2 %0, %1, %2, mg;}"
-              : "=l"(r) : "l"(x), "l"(invv[i]), "f"(8388608.0f));
-          b[2 * i] = uint32_t(r);
-          b[2 * i + 1] = uint32_t(r >> 32);
-        }
-        if (clamp) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) b[i] = min(b[i] - 0x4B000000u, QMAX);
-        }
-        const int64_t row = k * G + half * TH + j;  // group-major payload row
-        char* dst = lc + (row * g.row_elems + ch) * BITS / 8;
-        if constexpr (BITS == 4) {
-          *reinterpret_cast<uint32_t*>(dst) =
-              bytes4(lea4(b[1], b[0]), lea4(b[3], b[2]), lea4(b[5], b[4]), lea4(b[7], b[6]));
-        } else {
-          *reinterpret_cast<uint2*>(dst) =
-              make_uint2(bytes4(b[0], b[1], b[2], b[3]), bytes4(b[4], b[5], b[6], b[7]));
-        }
-      }
-    }
+    kchan_quant_lanes<BITS, G, TH>(g, w, active, half, layer, k, ch);
     if (sig.peer_flags) {  // fused kivi prefill: this CTA's share of a chunk is done
       const int64_t c = item / sig.items_per_chunk;
       const int64_t nxt = item + gridDim.x;
