@@ -389,7 +389,8 @@ def run_local(args, torch):
     k3 = sum(e["k3"][0].elapsed_time(e["k3"][1]) for e in timing) / args.steps
     kernel_bytes = fp16_bytes + lay.wire_bytes  # K1 reads fp16, writes payload; K3 the reverse
     hbm, peak_kind = peaks()
-    dom, dom_ms = ("quant_pack", k1) if k1 >= k3 else ("dequant_scatter_paged", k3)
+    k3_name = "pull_dequant_scatter_paged" if args.k3 == "bulk" else "dequant_scatter_paged"
+    dom, dom_ms = ("quant_pack", k1) if k1 >= k3 else (k3_name, k3)
     achieved = kernel_bytes / (dom_ms * 1e-3) / 1e9
     step_bytes = 2 * kernel_bytes  # algorithmic HBM bytes of the round trip
     roof_ms = step_bytes / (hbm * 1e9) * 1e3
@@ -453,6 +454,8 @@ def ncu_traffic(workload, args, kernel):
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             doc = json.load(f)
         key = f"{workload}/bits{args.bits}/g{args.group}/chunks{args.chunks}"
+        if kernel == "pull_dequant_scatter_paged":  # K3-bulk on the local payload
+            key += "/k3bulk"
         return int(doc["configs"][key][kernel]["traffic_bytes"])
     except Exception:  # noqa: BLE001
         return None
@@ -793,7 +796,7 @@ def main():
                     help="layer chunks per hand-off (default: 1 at N=1; 8 per pair at N>1 for "
                     "the non-fused paths -- the fused pull picks layer-granular chunks itself)")
     ap.add_argument("--mode", default="pull", choices=["pull", "pull_ldg", "push", "copy", "nccl"])
-    ap.add_argument("--k3", default="ldg", choices=["ldg", "bulk"],
+    ap.add_argument("--k3", default="bulk", choices=["ldg", "bulk"],
                     help="N=1: K3 variant (per-lane loads or TMA bulk staging)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=32,
