@@ -796,7 +796,7 @@ def main():
                     help="layer chunks per hand-off (default: 1 at N=1; 8 per pair at N>1 for "
                     "the non-fused paths -- the fused pull picks layer-granular chunks itself)")
     ap.add_argument("--mode", default="pull", choices=["pull", "pull_ldg", "push", "copy", "nccl"])
-    ap.add_argument("--k3", default="bulk", choices=["ldg", "bulk"],
+    ap.add_argument("--k3", default="ldg", choices=["ldg", "bulk"],
                     help="N=1: K3 variant (per-lane loads or TMA bulk staging)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=32,

@@ -449,11 +449,11 @@ class HandoffPlan:
                  group_size: int = DEFAULT_GROUP, mode: str = "pull", n_chunks: int = 8,
                  bulk: bool | None = None, min_chunk_bytes: int = 0):
         self.src, self.dst = src, dst
-        # TMA bulk-staged K3 by default when the payload is read over NVLink
-        # or from this GPU's own HBM (N=1 config 2: 1.765 vs 1.81 ms for the
-        # per-lane K3, profiles/r02_bench/k3_local_ab_n1.log); push / copy
-        # land the payload on D and keep the per-lane K3
-        self.bulk = (mode == "pull" or src.device == dst.device) if bulk is None else bool(bulk)
+        # TMA bulk-staged K3 by default when the payload is read over NVLink;
+        # on a local payload the per-lane K3 (K3-bulk there is 2-3 % faster
+        # for config 2 at 4 bits but 17-30 % slower at 8 bits and for the
+        # 13B / 70B-GQA row shapes: profiles/r02_bench/k3_local_shapes_n1.log)
+        self.bulk = (mode == "pull") if bulk is None else bool(bulk)
         self.bits = _bits_of(prec)
         self.layout = _layout_for(src, n_tokens, self.bits, group_size)
         if (dst.n_layers, dst.n_heads, dst.head_dim) != (src.n_layers, src.n_heads, src.head_dim):
@@ -613,7 +613,7 @@ class HostHandoff:
                     self.up[i].record(self.h2d)
                 self.comp.wait_event(self.up[i])
                 quant_pack_layers(self.src, self.packed, l0, l1, self.comp)
-                dequant_scatter_layers(self.packed, self.dst, l0, l1, self.comp, bulk=True)
+                dequant_scatter_layers(self.packed, self.dst, l0, l1, self.comp)
                 self.done[i].record(self.comp)
                 self.d2h.wait_event(self.done[i])
                 with torch.cuda.stream(self.d2h):
