@@ -266,8 +266,10 @@ def run_reference(args, rank: int, world: int):
     wl = args.workload or ("cfg2_7b_2048x8" if world == 1 else default_pair_workload(world))
     L, H, D, b, s = WORKLOADS[wl]
     if not args.ref_layers:
+        # the whole workload per step when it is at most 16 GB of fp16 KV
+        # (~0.4-0.8 s of AVX2 work on 16 cores), else an 8 GB layer sample
         per_layer = 2 * b * s * H * D * 2
-        args.ref_layers = max(1, min(L, round(1.0e9 / per_layer)))
+        args.ref_layers = L if L * per_layer <= 16e9 else max(1, min(L, round(8e9 / per_layer)))
     for _ in range(args.warmup):  # generates the sampled layers and the cache once
         cpu_reference(wl, bits, group, budget_s=None, max_layers=min(L, 4))
     vals, secs = [], []
@@ -803,7 +805,7 @@ def main():
                     help="N=1 e2e: layer chunks for H2D/compute/D2H overlap")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-layers", type=int, default=None,
-                    help="reference arm: layers per step (default: ~1 GB of fp16 KV)")
+                    help="reference arm: layers per step (default: the whole workload up to 16 GB of fp16 KV)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--queue-depth", type=int, default=4,

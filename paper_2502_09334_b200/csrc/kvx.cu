@@ -389,6 +389,34 @@ constexpr int kPullCtasPerSm = KVX_PULL_PER_SM;  // bulk-pull CTAs per SM (A/B: 
 template <int BITS>
 constexpr int pull_ctas_per_sm() { return BITS == 2 ? KVX_PULL_PER_SM_2BIT : kPullCtasPerSm; }
 
+// K3-bulk on a LOCAL payload (no doorbells: N=1 hand-offs, the decode side of
+// push / copy): HBM feeds the stages, not the link, so the consumers' fp16
+// stores bound it and it wants more CTAs per SM and larger stages than a
+// pull.  Defaults from the N=1 shape sweep (r02_bench/k3_local_geo_n1.log);
+// KVX_LOCAL_PULL_PER_SM / KVX_LOCAL_STAGE_BYTES override them for A/B runs.
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+#ifndef KVX_LOCAL_PULL_PER_SM
+#define KVX_LOCAL_PULL_PER_SM 1
+#endif
+#ifndef KVX_LOCAL_STAGE_BYTES
+#define KVX_LOCAL_STAGE_BYTES KVX_BULK_STAGE_BYTES
+#endif
+int local_pull_ctas_per_sm() {
+  static const int v = env_int("KVX_LOCAL_PULL_PER_SM", KVX_LOCAL_PULL_PER_SM);
+  return v < 1 ? 1 : v;
+}
+int local_row_align() {
+  static const int v = env_int("KVX_LOCAL_ROW_ALIGN", 1);
+  return v;
+}
+int local_stage_target() {
+  static const int v = env_int("KVX_LOCAL_STAGE_BYTES", KVX_LOCAL_STAGE_BYTES);
+  return v < 1024 ? 1024 : v;
+}
+
 // Smallest row count whose code and metadata bytes are both 16-byte multiples.
 int64_t bulk_row_multiple(int64_t code_row_bytes, int64_t meta_row_bytes) {
   auto need = [](int64_t b) {
@@ -431,9 +459,18 @@ bool plan_pull(const kvx::Geo& g, const void* codes, const void* scale, const vo
       !aligned(codes, 16) || !aligned(scale, 16) || !aligned(zero, 16) || g.codes_ls % 16 ||
       g.meta_ls % 16)
     return false;  // not bulk-copyable: caller falls back to the LDG kernel
-  int64_t r = kBulkStageTarget / bg.code_row_bytes;
-  r = r / m * m;
-  if (r < m) r = m;
+  const int target = ready ? kBulkStageTarget : local_stage_target();
+  int64_t unit = m;
+  if (!ready && local_row_align()) {
+    // local payload: the consumers bound the pull, so a span is a whole number
+    // of passes of the 8 consumer warps (rpw rows per warp for short rows)
+    const int64_t rpw = (bg.cpr < 32 && 32 % bg.cpr == 0) ? 32 / bg.cpr : 1;
+    const int64_t w = 8 * rpw;  // powers of two: the max is the lcm
+    unit = w > m ? w : m;
+  }
+  int64_t r = target / bg.code_row_bytes;
+  r = r / unit * unit;
+  if (r < unit) r = unit;
   if (r > two_t) r = two_t;
   bg.rows_per_span = int(r);
   bg.stage_bytes = bg.rows_per_span * (bg.code_row_bytes + 2 * bg.meta_row_bytes);
@@ -469,7 +506,8 @@ cudaError_t launch_pull(const kvx::Geo& g, const void* codes, const void* scale,
   // next hand-off's pull, which PDL schedules next to this one
   // (tools/decode_interference.py: a concurrent HBM-bound round slows 1.96x
   // instead of 2.2x).
-  per_sm = per_sm < pull_ctas_per_sm<BITS>() ? per_sm : pull_ctas_per_sm<BITS>();
+  const int want = ready ? pull_ctas_per_sm<BITS>() : local_pull_ctas_per_sm();
+  per_sm = per_sm < want ? per_sm : want;
   int64_t grid = int64_t(sm_count(current_device())) * per_sm;
 #ifdef KVX_PULL_MAX_CTAS
   if (grid > KVX_PULL_MAX_CTAS) grid = KVX_PULL_MAX_CTAS;
