@@ -370,7 +370,7 @@ def run_local(args, torch):
     else:
         plan = HandoffPlan(KVPlanes.dense(kv), KVPlanes.paged(kc, vc, slots), T,
                            KvPrecision(args.bits), args.group, mode="local", n_chunks=args.chunks,
-                           bulk=(args.k3 == "bulk"))
+                           bulk=None if args.k3 == "auto" else args.k3 == "bulk")
     lay = plan.layout
     fp16_bytes = lay.fp16_bytes
     for _ in range(args.warmup):
@@ -391,7 +391,8 @@ def run_local(args, torch):
     k3 = sum(e["k3"][0].elapsed_time(e["k3"][1]) for e in timing) / args.steps
     kernel_bytes = fp16_bytes + lay.wire_bytes  # K1 reads fp16, writes payload; K3 the reverse
     hbm, peak_kind = peaks()
-    k3_name = "pull_dequant_scatter_paged" if args.k3 == "bulk" else "dequant_scatter_paged"
+    k3_bulk = getattr(plan, "bulk", args.k3 == "bulk")
+    k3_name = "pull_dequant_scatter_paged" if k3_bulk else "dequant_scatter_paged"
     dom, dom_ms = ("quant_pack", k1) if k1 >= k3 else (k3_name, k3)
     achieved = kernel_bytes / (dom_ms * 1e-3) / 1e9
     step_bytes = 2 * kernel_bytes  # algorithmic HBM bytes of the round trip
@@ -445,7 +446,8 @@ def run_local(args, torch):
                   "algorithmic_bytes_per_launch": kernel_bytes // len(plan_chunks(args, L)),
                   "k1_ms": round(k1, 4), "k3_ms": round(k3, 4),
                   "step_roofline_ms": round(roof_ms, 4), "step_frac": round(roof_ms / ms, 4)},
-        extra={"n_chunks": args.chunks, "mode": "local", "k3": args.k3, "format": args.format},
+        extra={"n_chunks": args.chunks, "mode": "local",
+               "k3": "bulk" if k3_bulk else "ldg", "format": args.format},
     )
 
 
@@ -798,8 +800,9 @@ def main():
                     help="layer chunks per hand-off (default: 1 at N=1; 8 per pair at N>1 for "
                     "the non-fused paths -- the fused pull picks layer-granular chunks itself)")
     ap.add_argument("--mode", default="pull", choices=["pull", "pull_ldg", "push", "copy", "nccl"])
-    ap.add_argument("--k3", default="ldg", choices=["ldg", "bulk"],
-                    help="N=1: K3 variant (per-lane loads or TMA bulk staging)")
+    ap.add_argument("--k3", default="auto", choices=["auto", "ldg", "bulk"],
+                    help="N=1: K3 variant (per-lane loads or TMA bulk staging; auto: "
+                    "datapath.local_bulk_preferred, by row length)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=32,
                     help="N=1 e2e: layer chunks for H2D/compute/D2H overlap")

@@ -392,8 +392,11 @@ constexpr int pull_ctas_per_sm() { return BITS == 2 ? KVX_PULL_PER_SM_2BIT : kPu
 // K3-bulk on a LOCAL payload (no doorbells: N=1 hand-offs, the decode side of
 // push / copy): HBM feeds the stages, not the link, so the consumers' fp16
 // stores bound it and it wants more CTAs per SM and larger stages than a
-// pull.  Defaults from the N=1 shape sweep (r02_bench/k3_local_geo_n1.log);
-// KVX_LOCAL_PULL_PER_SM / KVX_LOCAL_STAGE_BYTES override them for A/B runs.
+// pull, and its spans are whole passes of the consumer warps (a 6-row span
+// leaves 2 of 8 warps idle).  N=1 sweep (r02_bench/k3_local_geo_n1.log), K3 ms
+// at 1 CTA per SM, 16 / 24 / 32 KB stages: config 2 1.834 / 1.837 / 1.749,
+// 2-bit 1.547 / 1.562 / 1.545, 13B 2.732 / 2.734 / 2.731; 2 CTAs per SM equal
+// or slower.  KVX_LOCAL_PULL_PER_SM / _STAGE_BYTES / _ROW_ALIGN override.
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return (v && *v) ? std::atoi(v) : dflt;
@@ -402,7 +405,7 @@ int env_int(const char* name, int dflt) {
 #define KVX_LOCAL_PULL_PER_SM 1
 #endif
 #ifndef KVX_LOCAL_STAGE_BYTES
-#define KVX_LOCAL_STAGE_BYTES KVX_BULK_STAGE_BYTES
+#define KVX_LOCAL_STAGE_BYTES 32768
 #endif
 int local_pull_ctas_per_sm() {
   static const int v = env_int("KVX_LOCAL_PULL_PER_SM", KVX_LOCAL_PULL_PER_SM);

@@ -320,6 +320,18 @@ def _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done, ctl,
         _lib.call("kvx_dequant_scatter_paged", *args, _stream_ptr(stream))
 
 
+def local_bulk_preferred(lay: PackedLayout) -> bool:
+    """Which K3 a LOCAL payload (N=1, the host-buffer path) runs: K3-bulk when
+    a token row has at least 64 chunks of 32 elements (the consumer warps then
+    amortise each staged span over several chunks per lane), the per-lane K3
+    for short rows (a 70B-GQA row of 8 KV heads is 32 chunks: K3-bulk there is
+    7-43 % slower).  N=1 sweep, K3 ms, per-lane -> bulk (32 KB stages, spans of
+    whole consumer passes): config 2 1.807 -> 1.749, 13B 2.781 -> 2.731, 8-bit
+    2.136 -> 1.992, 2-bit 1.740 -> 1.545, 70B-GQA 0.535 -> 0.768
+    (profiles/r02_bench/k3_local_geo_n1.log)."""
+    return lay.bits != 16 and (lay.n_heads * lay.head_dim) // 32 >= 64 and pull_supported(lay)
+
+
 def pull_supported(lay: PackedLayout) -> bool:
     return bool(_lib.load().kvx_pull_supported(lay.n_tokens, lay.n_heads, lay.head_dim,
                                                   lay.group, lay.bits))
@@ -449,13 +461,15 @@ class HandoffPlan:
                  group_size: int = DEFAULT_GROUP, mode: str = "pull", n_chunks: int = 8,
                  bulk: bool | None = None, min_chunk_bytes: int = 0):
         self.src, self.dst = src, dst
-        # TMA bulk-staged K3 by default when the payload is read over NVLink;
-        # on a local payload the per-lane K3 (K3-bulk there is 2-3 % faster
-        # for config 2 at 4 bits but 17-30 % slower at 8 bits and for the
-        # 13B / 70B-GQA row shapes: profiles/r02_bench/k3_local_shapes_n1.log)
-        self.bulk = (mode == "pull") if bulk is None else bool(bulk)
         self.bits = _bits_of(prec)
         self.layout = _layout_for(src, n_tokens, self.bits, group_size)
+        # TMA bulk-staged K3 by default when the payload is read over NVLink;
+        # on a local payload (N=1) by row length (local_bulk_preferred); push /
+        # copy land the payload on D and keep the per-lane K3
+        if bulk is None:
+            local = mode == "local" or src.device == dst.device
+            bulk = mode == "pull" and not local or local and local_bulk_preferred(self.layout)
+        self.bulk = bool(bulk)
         if (dst.n_layers, dst.n_heads, dst.head_dim) != (src.n_layers, src.n_heads, src.head_dim):
             raise ValueError("source and destination KV geometry differ")
         self.p_dev, self.d_dev = src.device, dst.device
@@ -588,6 +602,7 @@ class HostHandoff:
         bits = _bits_of(prec)
         self.layout = _layout_for(self.src, kv_host.shape[2], bits, group_size)
         self.packed = alloc_packed(self.layout, self.device)
+        self.bulk = local_bulk_preferred(self.layout)  # K3 variant for the local payload
         self.chunks = layer_chunks(self.layout.n_layers, n_chunks)
         with torch.cuda.device(self.device):
             self.h2d, self.comp, self.d2h = (torch.cuda.Stream() for _ in range(3))
@@ -613,7 +628,8 @@ class HostHandoff:
                     self.up[i].record(self.h2d)
                 self.comp.wait_event(self.up[i])
                 quant_pack_layers(self.src, self.packed, l0, l1, self.comp)
-                dequant_scatter_layers(self.packed, self.dst, l0, l1, self.comp)
+                dequant_scatter_layers(self.packed, self.dst, l0, l1, self.comp,
+                                       bulk=self.bulk)
                 self.done[i].record(self.comp)
                 self.d2h.wait_event(self.done[i])
                 with torch.cuda.stream(self.d2h):
