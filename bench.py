@@ -288,8 +288,10 @@ def run_reference(args, rank: int, world: int):
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": r["cores"],
                          "kind": "port", "cpu_model": r["cpu_model"], "affinity": r["affinity"],
                          "simd": r["simd"],
-                         "sample": f"each step: {args.ref_layers} of the workload's {L} layers "
-                                   f"(bounded sample; GB/s is per fp16 byte processed); "
+                         "sample": (f"each step: the whole workload ({L} layers); "
+                                    if args.ref_layers >= L else
+                                    f"each step: {args.ref_layers} of the workload's {L} layers "
+                                    f"(bounded sample; GB/s is per fp16 byte processed); ")
                                    + r["sample"]},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -415,7 +417,7 @@ def run_local(args, torch):
         for _ in range(max(1, min(args.warmup, 3))):
             host.run()
         torch.cuda.synchronize()
-        n_e2e = max(1, min(args.steps, args.e2e_steps))
+        n_e2e = max(1, min(args.steps, args.e2e_steps or args.steps))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(n_e2e):
@@ -685,7 +687,7 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
             d2h = (hk.numel() + hv.numel()) * 2
             e2e_step = (lambda: ch.recv(planes, next_t(), None, **stage)) if trace is None else (
                 lambda: ch.recv(planes_b[it["i"] % len(tok)], next_t(), None, **stage))
-        n_e2e = max(1, min(args.steps, args.e2e_steps))
+        n_e2e = max(1, min(args.steps, args.e2e_steps or args.steps))
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
@@ -803,7 +805,9 @@ def main():
     ap.add_argument("--k3", default="auto", choices=["auto", "ldg", "bulk"],
                     help="N=1: K3 variant (per-lane loads or TMA bulk staging; auto: "
                     "datapath.local_bulk_preferred, by row length)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="host-buffer e2e steps (default: --steps; consecutive steps "
+                    "pipeline, so few steps under-report the streaming rate)")
     ap.add_argument("--e2e-chunks", type=int, default=32,
                     help="N=1 e2e: layer chunks for H2D/compute/D2H overlap")
     ap.add_argument("--cpu-budget", type=float, default=12.0)

@@ -582,7 +582,12 @@ class HostHandoff:
     paged cache to host memory; this class does the same on one GPU:
     per layer chunk, H2D of the KV (copy engine) -> K1 -> K3 -> D2H of the
     decode cache (second copy engine), three streams overlapping chunk i's
-    compute with chunk i+1's upload and chunk i-1's download.
+    compute with chunk i+1's upload and chunk i-1's download.  Consecutive
+    ``run()`` calls pipeline too: a chunk's upload waits only for the previous
+    run's K1 of that chunk, its K3 only for the previous run's download of it,
+    so run i+1's first uploads overlap run i's last downloads.  Each run ends
+    with the caller's current stream waiting for all of it; the first run also
+    starts after the caller's stream (the slot mapping copied at construction).
     Host tensors must be pinned for the copies to be asynchronous.
     """
 
@@ -608,6 +613,9 @@ class HostHandoff:
             self.h2d, self.comp, self.d2h = (torch.cuda.Stream() for _ in range(3))
             self.up = [torch.cuda.Event() for _ in self.chunks]
             self.done = [torch.cuda.Event() for _ in self.chunks]
+            self.read = [torch.cuda.Event() for _ in self.chunks]  # K1 read kv[chunk]
+            self.down = [torch.cuda.Event() for _ in self.chunks]  # D2H read kc/vc[chunk]
+        self._runs = 0
 
     @property
     def h2d_bytes(self) -> int:
@@ -620,14 +628,21 @@ class HostHandoff:
     def run(self) -> None:
         with torch.cuda.device(self.device):
             cur = torch.cuda.current_stream()
-            for s in (self.h2d, self.comp, self.d2h):
-                s.wait_stream(cur)
+            first = self._runs == 0
+            if first:
+                for s in (self.h2d, self.comp, self.d2h):
+                    s.wait_stream(cur)
             for i, (l0, l1) in enumerate(self.chunks):
+                if not first:
+                    self.h2d.wait_event(self.read[i])  # previous run's K1 read kv[chunk]
                 with torch.cuda.stream(self.h2d):
                     self.kv[l0:l1].copy_(self.kv_host[l0:l1], non_blocking=True)
                     self.up[i].record(self.h2d)
                 self.comp.wait_event(self.up[i])
                 quant_pack_layers(self.src, self.packed, l0, l1, self.comp)
+                self.read[i].record(self.comp)
+                if not first:
+                    self.comp.wait_event(self.down[i])  # previous run's D2H read the cache
                 dequant_scatter_layers(self.packed, self.dst, l0, l1, self.comp,
                                        bulk=self.bulk)
                 self.done[i].record(self.comp)
@@ -635,5 +650,7 @@ class HostHandoff:
                 with torch.cuda.stream(self.d2h):
                     self.kc_host[l0:l1].copy_(self.kc[l0:l1], non_blocking=True)
                     self.vc_host[l0:l1].copy_(self.vc[l0:l1], non_blocking=True)
+                    self.down[i].record(self.d2h)
+            self._runs += 1
             for s in (self.h2d, self.comp, self.d2h):
                 cur.wait_stream(s)

@@ -88,6 +88,37 @@ def test_host_handoff(cuda):
     assert np.array_equal(h16(vc_h.numpy()), h16(ovc))
 
 
+@pytest.mark.parametrize("H", [8, 32])  # per-lane K3 / K3-bulk (local_bulk_preferred)
+def test_host_handoff_pipelined_runs(cuda, H):
+    """Consecutive run()s pipeline per chunk (run i+1's uploads overlap run
+    i's downloads): a new input per synchronised run, then back-to-back runs
+    of one input, each result bit-exact."""
+    from paper_2502_09334_b200 import KvPrecision
+    from paper_2502_09334_b200.datapath import HostHandoff
+    torch = cuda
+    L, T, D, bs = 5, 70, 128, 16
+    nb = (T + bs - 1) // bs + 2
+    slots = O.synthetic_slots(T, bs, nb, seed=3)
+    kv_h = torch.empty((L, 2, T, H, D), dtype=torch.float16).pin_memory()
+    kc_h = torch.zeros((L, nb, bs, H, D), dtype=torch.float16).pin_memory()
+    vc_h = torch.zeros_like(kc_h).pin_memory()
+    host = HostHandoff(kv_h, kc_h, vc_h, torch.from_numpy(slots), "cuda:0", KvPrecision(4), 128,
+                       n_chunks=4)
+    for seed in (11, 12, 13):
+        kv_np = O.synthetic_kv(L, T, H, D, seed=seed)
+        kv_h.copy_(torch.from_numpy(kv_np))
+        host.run()
+        torch.cuda.synchronize()
+        okc, ovc = expected_cache(kv_np, slots, nb, bs, 4, 128)
+        assert np.array_equal(h16(kc_h.numpy()), h16(okc)), seed
+        assert np.array_equal(h16(vc_h.numpy()), h16(ovc)), seed
+    for _ in range(4):
+        host.run()
+    torch.cuda.synchronize()
+    assert np.array_equal(h16(kc_h.numpy()), h16(okc))
+    assert np.array_equal(h16(vc_h.numpy()), h16(ovc))
+
+
 def test_cfg2_full_size_properties(cuda):
     """BASELINE config 2 (7B, 2048 x 8) at full size: every element inside the
     format's error bound, padding never written, and 2,048 sampled token rows
