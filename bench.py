@@ -513,9 +513,18 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
     B = sys.modules[__name__]
 
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # more ranks than GPUs (a dry run of the N=8 rank logic on a smaller box:
+    # pairs i -> i+N/2 then share a GPU over same-device IPC; the numbers mean
+    # nothing): gloo as the default group, since NCCL refuses duplicate GPUs
+    oversub = world > torch.cuda.device_count()
+    if oversub:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if oversub:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     ctrl = dist.new_group(backend="gloo")
     wl = args.workload or B.default_pair_workload(world)
     trace = None
@@ -702,7 +711,8 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
         e2e_ms = e0.elapsed_time(e1) / n_e2e
         dist.barrier()
     stats = torch.tensor([ms, kern.get("k1", 0.0), kern.get("k3", 0.0), e2e_ms, h2d, d2h,
-                          launches, cal_small_ms, host_us], dtype=torch.float64, device=dev)
+                          launches, cal_small_ms, host_us], dtype=torch.float64,
+                         device="cpu" if oversub else dev)
     gathered = [torch.zeros_like(stats) for _ in range(world)]
     dist.all_gather(gathered, stats)
     clocks = exchange(clk.summary(), ctrl)
@@ -778,6 +788,9 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                                 "tokens/batch, rng(0)"} if trace is not None else {}),
                    "pairing": pairing(world), "parallelism": f"{pairs}P{pairs}D",
                    "handoffs_per_step": per_step,
+                   **({"oversubscribed_dry_run": f"{world} ranks on "
+                       f"{torch.cuda.device_count()} GPUs (pairs share a GPU): not a measurement"}
+                      if oversub else {}),
                    **({"decode_pull": f"recv_many: {per_step} queued hand-offs per pull launch"}
                       if per_step > 1 else {})},
         )

@@ -73,7 +73,7 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])  # 8: the 4P4D rank layout (pairs i -> i+4)
 def test_handle_exchange_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
