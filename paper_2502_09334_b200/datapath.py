@@ -468,7 +468,7 @@ class HandoffPlan:
         # copy land the payload on D and keep the per-lane K3
         if bulk is None:
             local = mode == "local" or src.device == dst.device
-            bulk = mode == "pull" and not local or local and local_bulk_preferred(self.layout)
+            bulk = (mode == "pull" and not local) or (local and local_bulk_preferred(self.layout))
         self.bulk = bool(bulk)
         if (dst.n_layers, dst.n_heads, dst.head_dim) != (src.n_layers, src.n_heads, src.head_dim):
             raise ValueError("source and destination KV geometry differ")
