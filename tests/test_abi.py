@@ -246,3 +246,15 @@ def test_nccl_pool_entry_points(lib):
     assert rc in (0, _lib.KVX_ERR_UNSUPPORTED, _lib.KVX_ERR_NCCL)
     if rc == 0:
         assert any(uid.raw)
+
+
+def test_local_k3_choice_by_row_length(lib):
+    """N=1 picks K3-bulk for rows of >= 64 chunks and the per-lane K3 for
+    short rows (datapath.local_bulk_preferred; r02_bench/k3_local_geo_n1.log)."""
+    from paper_2502_09334_b200.datapath import PackedLayout, local_bulk_preferred
+    cfg2 = PackedLayout(32, 16384, 32, 128, 4, 128)    # 128 chunks per row
+    cfg3 = PackedLayout(40, 16384, 40, 128, 8, 128)    # 160
+    gqa = PackedLayout(80, 32768, 8, 128, 4, 128)      # 32: 70B-GQA, 8 KV heads
+    raw = PackedLayout(32, 16384, 32, 128, 16, 128)    # passthrough
+    assert local_bulk_preferred(cfg2) and local_bulk_preferred(cfg3)
+    assert not local_bulk_preferred(gqa) and not local_bulk_preferred(raw)
