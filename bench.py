@@ -591,6 +591,19 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
 
             def step(timing=None):
                 ch.recv_many([(pl, next_t()) for pl in planes_k], timing)
+        elif trace is None and args.chained and not kivi:
+            # chained pulls (kvx.h KVX_PAIR_CHAINED): consecutive hand-offs land
+            # in two alternating block sets, so no pull writes the blocks of
+            # the one before it, and each may write while that one drains
+            kc = torch.zeros((L, 2 * nb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
+            vc = torch.zeros_like(kc)
+            planes_ab = [KVPlanes.paged(kc, vc, slots), KVPlanes.paged(kc, vc, slots + nb * B.BLOCK)]
+            planes = planes_ab[0]
+            torch.cuda.synchronize()  # the caches and slot mappings are ready
+
+            def step(timing=None):
+                i = it["i"]
+                ch.recv(planes_ab[i % 2], next_t(), timing, chained=i > 0 and timing is None)
         elif trace is None:
             planes = KVPlanes.paged(kc, vc, slots)
 
@@ -788,6 +801,8 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                                 "tokens/batch, rng(0)"} if trace is not None else {}),
                    "pairing": pairing(world), "parallelism": f"{pairs}P{pairs}D",
                    "handoffs_per_step": per_step,
+                   **({"chained": "recv(chained=True) into two alternating block sets"}
+                      if args.chained and trace is None and not kivi and args.batch == 1 else {}),
                    **({"oversubscribed_dry_run": f"{world} ranks on "
                        f"{torch.cuda.device_count()} GPUs (pairs share a GPU): not a measurement"}
                       if oversub else {}),
@@ -826,6 +841,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-layers", type=int, default=None,
                     help="reference arm: layers per step (default: the whole workload up to 16 GB of fp16 KV)")
+    ap.add_argument("--chained", action="store_true",
+                    help="N>1 fixed workloads: chained pulls (recv(chained=True)) into two "
+                         "alternating block sets")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--queue-depth", type=int, default=4,
@@ -845,6 +863,8 @@ def main():
     ap.add_argument("--gate-recv", action="store_true",
                     help="N>1: hold each pull in the GPU front-end until chunk 0 is published")
     args = ap.parse_args()
+    if args.chained:
+        args.no_e2e = True  # the alternating block sets would double the e2e download
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
 

@@ -164,8 +164,14 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
  * stream's previous kernel (typically the previous hand-off's pull) is still
  * running; everything that touches stream-ordered memory (the slot mapping,
  * the cache, done_counter) waits for it (griddepcontrol.wait).
+ * KVX_PULL_CHAINED (with KVX_PULL_PDL): the caller promises that the stream's
+ * previous kernel is a pull of the same pair AND that this hand-off's slot
+ * mapping is ready and its destination blocks are not written by that pull;
+ * the consumers then write the cache while the previous pull drains, and
+ * only the completion (done_counter, the free flag) waits for it.
  */
 #define KVX_PULL_PDL 1
+#define KVX_PULL_CHAINED 2
 int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const void* zero,
                                    int64_t payload_layer_stride, const int64_t* dst_slots,
                                    int64_t n_layers, int64_t n_tokens, int n_heads, int head_dim,
@@ -355,7 +361,10 @@ int kvx_handoff_chunk_plan(int64_t n_layers, int64_t n_tokens, int n_heads, int 
  *   kvx_pair_recv: K3-bulk pulling the slot over NVLink as chunks are
  *     published, freeing it in-kernel (KVX_PAIR_GATE: launch once chunk 0 is
  *     published; KVX_PAIR_PDL: programmatic dependent launch, so a pull
- *     streams its slot while the previous hand-off's pull drains).
+ *     streams its slot while the previous hand-off's pull drains;
+ *     KVX_PAIR_CHAINED with KVX_PAIR_PDL: KVX_PULL_CHAINED's promise --
+ *     back-to-back recvs into distinct blocks with ready slot mappings --
+ *     so the pull also writes the cache during the previous pull's drain).
  * Validation: n_tokens <= max_tokens, the head window inside the planes, the
  * current device == the creating device.  Replaces the kv_delay the
  * reference charges per request (simulate.py:221-235). */
@@ -363,6 +372,7 @@ int kvx_handoff_chunk_plan(int64_t n_layers, int64_t n_tokens, int n_heads, int 
 #define KVX_ROLE_DECODE 1
 #define KVX_PAIR_GATE 1
 #define KVX_PAIR_PDL 2
+#define KVX_PAIR_CHAINED 4
 int kvx_pair_create(int role, int64_t n_layers, int64_t max_tokens, int n_heads, int head_dim,
                     int bits, int group, int queue_depth, int layerwise, void* local_flags,
                     void* peer_flags, void* payload, int64_t slot_bytes, void* ctl,

@@ -84,9 +84,9 @@ SIGNATURES = {
 
 # constants of include/kvx.h
 KVX_KIVI_V_FLAGS = 32
-KVX_PULL_PDL = 1
+KVX_PULL_PDL, KVX_PULL_CHAINED = 1, 2
 KVX_ROLE_PREFILL, KVX_ROLE_DECODE = 0, 1
-KVX_PAIR_GATE, KVX_PAIR_PDL = 1, 2
+KVX_PAIR_GATE, KVX_PAIR_PDL, KVX_PAIR_CHAINED = 1, 2, 4
 KVX_STATUS_OK, KVX_STATUS_ABORTED, KVX_STATUS_TIMEOUT = 0, 1, 2
 
 _lib = None

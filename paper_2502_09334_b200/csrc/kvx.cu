@@ -434,6 +434,7 @@ int64_t bulk_row_multiple(int64_t code_row_bytes, int64_t meta_row_bytes) {
 struct PullDone {  // optional in-kernel completion of a pull hand-off
   uint32_t* done_counter = nullptr;
   uint32_t* peer_free = nullptr;
+  bool chained = false;  // KVX_PULL_CHAINED: consumers skip the up-front PDL wait
 };
 
 // Span geometry of a K3-bulk pull (false: not bulk-stageable).
@@ -446,6 +447,7 @@ bool plan_pull(const kvx::Geo& g, const void* codes, const void* scale, const vo
   bg.ready_value = ready_value;
   bg.done_counter = done.done_counter;
   bg.peer_free = done.peer_free;
+  bg.chained = done.chained ? 1 : 0;
   bg.ctl = ctl;
 #ifdef KVX_TRACE
   bg.trace_id = g_trace_epoch;
@@ -963,7 +965,8 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
   if (rc) return rc;
   if (g.n_token_rows == 0) return KVX_OK;
   if ((ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) || !aligned(ctl, 8) ||
-      (flags & ~KVX_PULL_PDL))
+      (flags & ~(KVX_PULL_PDL | KVX_PULL_CHAINED)) ||
+      ((flags & KVX_PULL_CHAINED) && !(flags & KVX_PULL_PDL)))
     return KVX_ERR_INVALID_ARG;
   if ((done_counter != nullptr) != (peer_free_flag != nullptr) ||
       (done_counter && (!ready_flags || !aligned(done_counter, 4) || !aligned(peer_free_flag, 4))))
@@ -978,6 +981,7 @@ int kvx_pull_dequant_scatter_paged(const void* codes, const void* scale, const v
     const uint32_t* rf = static_cast<const uint32_t*>(ready_flags);
     kvx::Ctl* c = static_cast<kvx::Ctl*>(ctl);
     const bool pdl = flags & KVX_PULL_PDL;
+    done.chained = (flags & KVX_PULL_CHAINED) != 0;
     const int lpc = layers_per_chunk;
     bool ok = false;
     cudaError_t e;
@@ -1300,7 +1304,8 @@ int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_lay
                                         void* peer_free_flag, void* ctl, int flags,
                                         void* stream) {
   if ((ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) || !aligned(ctl, 8) ||
-      (flags & ~KVX_PULL_PDL))
+      (flags & ~(KVX_PULL_PDL | KVX_PULL_CHAINED)) ||
+      ((flags & KVX_PULL_CHAINED) && !(flags & KVX_PULL_PDL)))
     return KVX_ERR_INVALID_ARG;
   if ((done_counter != nullptr) != (peer_free_flag != nullptr) ||
       (done_counter && (!ready_flags || !aligned(done_counter, 4) || !aligned(peer_free_flag, 4))))
@@ -1663,7 +1668,8 @@ int kvx_pair_recv(void* pair, uint64_t epoch, void* k_cache, void* v_cache,
   auto* p = static_cast<kvx_pair*>(pair);
   int rc = pair_check(p, epoch, n_tokens, plane_heads, head_offset);
   if (rc) return rc;
-  if (p->role != KVX_ROLE_DECODE || (flags & ~(KVX_PAIR_GATE | KVX_PAIR_PDL)) || !dst_slots)
+  if (p->role != KVX_ROLE_DECODE || (flags & ~(KVX_PAIR_GATE | KVX_PAIR_PDL | KVX_PAIR_CHAINED)) ||
+      ((flags & KVX_PAIR_CHAINED) && !(flags & KVX_PAIR_PDL)) || !dst_slots)
     return KVX_ERR_INVALID_ARG;
   if (n_tokens == 0) return KVX_OK;
   if (!kvx_pull_supported(n_tokens, p->n_heads, p->head_dim, p->group, p->bits))
@@ -1693,7 +1699,9 @@ int kvx_pair_recv(void* pair, uint64_t epoch, void* k_cache, void* v_cache,
                                         k_cache, v_cache, dst_layer_stride, plane_heads,
                                         head_offset, ready, v, lpc, p->scratch + h * kPairScratch,
                                         p->peer_flags + kFlagFreeBase + h, p->ctl,
-                                        (flags & KVX_PAIR_PDL) ? KVX_PULL_PDL : 0, stream);
+                                        ((flags & KVX_PAIR_PDL) ? KVX_PULL_PDL : 0) |
+                                            ((flags & KVX_PAIR_CHAINED) ? KVX_PULL_CHAINED : 0),
+                                        stream);
 }
 
 int kvx_pair_recv_many(void* pair, uint64_t first_epoch, int count, void* k_cache, void* v_cache,

@@ -952,6 +952,7 @@ struct BulkGeo {
   uint32_t trace_id;     // trace builds: the hand-off's epoch
 #endif
   int layers_per_chunk;
+  int chained;           // KVX_PULL_CHAINED: only the completion waits for the previous grid
   int rows_per_span;     // R
   int spans_per_layer;   // ceil(2T / R)
   uint32_t n_spans;      // n_layers * spans_per_layer
@@ -1141,7 +1142,10 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
   } else {
   // ---- consumers: the slot mapping and the cache are stream-ordered inputs
 #ifndef KVX_K3_NO_PDL_WAIT  // A/B only: measures what the stream-order wait costs
-  pdl_wait();
+  // chained pulls (the caller's promise, kvx.h KVX_PULL_CHAINED): this
+  // hand-off's blocks and slot mapping do not depend on the previous pull, so
+  // the cache writes overlap its drain; the completion below still waits
+  if (!bg.chained) pdl_wait();
 #endif
   uint32_t k = 0;
   for (uint32_t sp = blockIdx.x; sp < bg.n_spans; sp += gridDim.x, ++k) {
@@ -1175,6 +1179,10 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
     // passed pdl_wait, so the previous use of these counters has completed.
     __syncthreads();  // this CTA has consumed every span it owned
     if (threadIdx.x == 0) {
+      // chained: the previous pull (same counters' previous user Q hand-offs
+      // back, and the previous slot's free flag) completes before this CTA
+      // counts itself -- completions stay in hand-off order
+      if (bg.chained) pdl_wait();
       // one atomic per CTA: low 16 bits count exits, high bits aborted CTAs
       const uint32_t inc = s_abort ? 0x10001u : 1u;
       const uint32_t total = atomicAdd(bg.done_counter, inc) + inc;
@@ -1190,6 +1198,8 @@ __global__ void __launch_bounds__(288, 1) pull_dequant_scatter_kernel(
 #endif
       }
     }
+  } else if (bg.chained && threadIdx.x == 0) {
+    pdl_wait();  // chained: never complete before the previous grid
   }
 }
 

@@ -689,9 +689,14 @@ class PairChannel:
         return n
 
     def recv(self, dst: KVPlanes, n_tokens: int, timing: list | None = None,
-             stage_out: tuple | None = None, seqlens=None) -> None:
+             stage_out: tuple | None = None, seqlens=None, chained: bool = False) -> None:
         """Receive into ``dst``.  ``stage_out=((dev_k, dev_v), (host_k, host_v))``:
-        download the decode cache to pinned host memory after the hand-off."""
+        download the decode cache to pinned host memory after the hand-off.
+        ``chained`` (fused pull with PDL, default format): the caller promises
+        that the previous operation on the current stream is this channel's
+        previous ``recv`` and that this hand-off's slot mapping is ready and
+        its blocks are not the previous hand-off's -- the pull then writes the
+        cache while the previous pull drains (kvx.h KVX_PAIR_CHAINED)."""
         if self.role != "decode":
             raise RuntimeError("recv() on the prefill end of the channel")
         self.check()
@@ -714,10 +719,13 @@ class PairChannel:
             else:
                 cur = torch.cuda.current_stream(self.device)
                 cs, ev = cur.cuda_stream, _kernel_events(timing, cur, "k3")
+            flags = self._recv_flags
+            if chained and flags & _lib.KVX_PAIR_PDL:
+                flags |= _lib.KVX_PAIR_CHAINED
             rc = self._pair_recv(self._pair, e, dst.k.data_ptr(), dst.v.data_ptr(),
                                  dst.layer_stride, dst.slots.data_ptr(), n_tokens,
                                  dst.plane_heads or dst.n_heads, dst.head_offset,
-                                 self._recv_flags, cs)
+                                 flags, cs)
             if rc:
                 _lib.check(rc, "kvx_pair_recv")
             if ev is not None:

@@ -435,6 +435,55 @@ def main():
         print("recv_many: ok", flush=True)
     dist.barrier()
     ch.close()
+
+    # chained pulls (kvx.h KVX_PAIR_CHAINED): back-to-back recvs, each into its
+    # OWN blocks of one cache with a slot mapping made up front, so every pull
+    # may write while the previous one drains; 3 rounds of 6 ragged hand-offs
+    # over 2 / 4 slots, the whole cache compared with the oracle per round
+    for Q in (2, 4):
+        spec = ChannelSpec(L, Tmax, H, D, 4, 128, 3, "pull", queue_depth=Q, gate_send=False)
+        ch = PairChannel(spec, rank, world, control_group=ctrl)
+        Ts = [Tmax, 16, 77, 1, 130, 64]
+        for rnd in range(3):
+            seeds = [9000 + 100 * rnd + 10 * i + Q + ch.pair for i in range(len(Ts))]
+            if ch.role == "prefill":
+                srcs = [KVPlanes.dense(torch.from_numpy(O.synthetic_kv(L, T, H, D, seed=sd)).to(dev))
+                        for T, sd in zip(Ts, seeds)]
+                torch.cuda.synchronize()
+                for sp, T in zip(srcs, Ts):
+                    ch.send(sp, T)
+            else:
+                nbm = sum(-(-T // bs) for T in Ts) + 3
+                kcm = torch.zeros((L, nbm, bs, H, D), dtype=torch.float16, device=dev)
+                vcm = torch.zeros_like(kcm)
+                perm = np.random.default_rng(50 + rnd).permutation(nbm)
+                planes, slots_l, b0 = [], [], 0
+                for T in Ts:
+                    t = np.arange(T)
+                    sl = (perm[b0 + t // bs] * bs + t % bs).astype(np.int64)
+                    b0 += -(-T // bs)
+                    slots_l.append(sl)
+                    planes.append(KVPlanes.paged(kcm, vcm, torch.from_numpy(sl).to(dev)))
+                torch.cuda.synchronize()  # the cache and slot mappings are ready
+                for i, (pl, T) in enumerate(zip(planes, Ts)):
+                    ch.recv(pl, T, chained=i > 0)
+                torch.cuda.synchronize()
+                ch.check()
+                okc = np.zeros((L, nbm, bs, H, D), np.float16); ovc = okc.copy()
+                for T, sd, sl in zip(Ts, seeds, slots_l):
+                    c, s_, z = O.quant_pack(O.synthetic_kv(L, T, H, D, seed=sd).reshape(-1, D), 4, 128)
+                    O.scatter_paged(O.unpack_dequant(c, s_, z, 4, 128, D).reshape(L, 2, T, H, D),
+                                    sl, okc, ovc)
+                if not (np.array_equal(kcm.cpu().numpy().view(np.uint16), okc.view(np.uint16)) and
+                        np.array_equal(vcm.cpu().numpy().view(np.uint16), ovc.view(np.uint16))):
+                    failures += 1
+                    print(f"MISMATCH chained Q={Q} rank={rank} round={rnd}", flush=True)
+            dist.barrier(ctrl)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ch.close()
+    if rank == 0:
+        print("chained pulls: ok", flush=True)
     f = _mp.total(failures, ctrl)
     if rank == 0:
         print(f"mp_handoff_check modes={modes} world={world} failures={f}", flush=True)
