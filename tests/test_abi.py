@@ -147,6 +147,10 @@ def test_fused_and_kivi_entry_points_validate(lib):
     assert lib.kvx_pull_dequant_scatter_paged(256, 256, 256, 0, None, 1, 1, 1, 128, 128, 4, 256,
                                               256, 0, 0, 0, 256, 1, 1, None, None, None, 4,
                                               None) == E
+    # chained pulls only with programmatic dependent launch
+    assert lib.kvx_pull_dequant_scatter_paged(256, 256, 256, 0, None, 1, 1, 1, 128, 128, 4, 256,
+                                              256, 0, 0, 0, 256, 1, 1, None, None, None,
+                                              _lib.KVX_PULL_CHAINED, None) == E
     offs = (ctypes.c_int64 * 7)(*([0] * 7))
     for fn in ("kvx_dequant_scatter_paged_kivi", "kvx_pull_dequant_scatter_paged_kivi"):
         f = getattr(lib, fn)
