@@ -1,6 +1,6 @@
 """Soak test of the pair protocol (torchrun, 2 ranks): thousands of hand-offs
 with random lengths, fresh slot tensors, random decode-round batching
-(`recv_many` of 1..Q queued hand-offs), both prefill modes (front-end gate /
+(`recv_many` of 1..Q queued hand-offs, or chained recvs), both prefill modes (front-end gate /
 latency mode) and queue depths, for a wall-clock budget.  Every hand-off's
 destination blocks are distinct within a round; every CHECK_EVERY-th round is
 compared on every byte against the local K1 -> K3 on the decode GPU (itself
@@ -65,8 +65,17 @@ def run_config(rank, world, dev, ctrl, Q, gate, L, H, D, Tmax, seconds, seed):
             if check:
                 kc.zero_()
                 vc.zero_()
-            if k > 1 and rng.random() < 0.5:
+            use_many = k > 1 and rng.random() < 0.5
+            chain = rng.random() < 0.5
+            if use_many:
                 ch.recv_many(items)
+            elif chain:
+                # chained pulls (kvx.h KVX_PAIR_CHAINED): the slot mappings are
+                # made and the round's blocks are distinct, so every recv after
+                # the first may write while the previous one drains
+                torch.cuda.current_stream().synchronize()
+                for i, it in enumerate(items):
+                    ch.recv(*it, chained=i > 0)
             else:
                 for it in items:
                     ch.recv(*it)
@@ -90,6 +99,7 @@ def run_config(rank, world, dev, ctrl, Q, gate, L, H, D, Tmax, seconds, seed):
             rng.permutation(nb)
             if k > 1:
                 rng.random()
+            rng.random()
         handoffs += k
         rounds += 1
         if rounds % 50 == 0:
