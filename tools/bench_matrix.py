@@ -38,11 +38,16 @@ def main():
             (1, ["--workload", "cfg4_70b_gqa_pair", "--no-e2e", "--no-cpu-baseline"]),
             (1, ["--bits", "2", "--no-e2e", "--no-cpu-baseline"]),
             (1, ["--bits", "16", "--no-e2e", "--no-cpu-baseline"]),
+            (1, ["--workload", "cfg3_13b_2048x8", "--no-e2e", "--no-cpu-baseline"]),
             (1, ["--format", "kivi", "--group", "32", "--no-e2e", "--no-cpu-baseline"])]
     if a.gpus >= 2:
         plan += [(2, []), (2, ["--workload", "cfg4_70b_gqa_pair", "--no-e2e"]),
                  (2, ["--workload", "trace_7b", "--no-e2e"]),
                  (2, ["--workload", "small_70b_gqa_128x1", "--no-e2e"]),
+                 (2, ["--workload", "small_70b_gqa_128x1", "--no-e2e", "--chained"]),
+                 (2, ["--workload", "small_70b_gqa_128x1", "--tokens", "1024", "--no-e2e"]),
+                 (2, ["--workload", "small_70b_gqa_128x1", "--tokens", "1024", "--no-e2e",
+                      "--chained"]),
                  (2, ["--workload", "small_70b_gqa_128x1", "--no-e2e", "--batch", "4",
                       "--queue-depth", "8"]),
                  (2, ["--workload", "small_70b_gqa_128x1", "--tokens", "16", "--no-e2e"]),
