@@ -592,18 +592,21 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
             def step(timing=None):
                 ch.recv_many([(pl, next_t()) for pl in planes_k], timing)
         elif trace is None and args.chained and not kivi:
-            # chained pulls (kvx.h KVX_PAIR_CHAINED): consecutive hand-offs land
-            # in two alternating block sets, so no pull writes the blocks of
-            # the one before it, and each may write while that one drains
-            kc = torch.zeros((L, 2 * nb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
+            # chained pulls (kvx.h KVX_PAIR_CHAINED): every hand-off of a chain
+            # lands in its own block set (a ring of up to 8 GB of sets); the
+            # chain restarts with an unchained recv whenever the ring wraps,
+            # so no two hand-offs that may be in flight together share blocks
+            set_bytes = L * nb * B.BLOCK * H * D * 2 * 2
+            n_sets = max(2, min(args.warmup + args.steps + 2, int(8e9 // set_bytes)))
+            kc = torch.zeros((L, n_sets * nb, B.BLOCK, H, D), dtype=torch.float16, device=dev)
             vc = torch.zeros_like(kc)
-            planes_ab = [KVPlanes.paged(kc, vc, slots), KVPlanes.paged(kc, vc, slots + nb * B.BLOCK)]
-            planes = planes_ab[0]
+            planes_ring = [KVPlanes.paged(kc, vc, slots + j * nb * B.BLOCK) for j in range(n_sets)]
+            planes = planes_ring[0]
             torch.cuda.synchronize()  # the caches and slot mappings are ready
 
             def step(timing=None):
-                i = it["i"]
-                ch.recv(planes_ab[i % 2], next_t(), timing, chained=i > 0 and timing is None)
+                j = it["i"] % n_sets
+                ch.recv(planes_ring[j], next_t(), timing, chained=j > 0 and timing is None)
         elif trace is None:
             planes = KVPlanes.paged(kc, vc, slots)
 
@@ -801,7 +804,8 @@ def run_pairs(args, torch, rank: int, world: int) -> None:
                                 "tokens/batch, rng(0)"} if trace is not None else {}),
                    "pairing": pairing(world), "parallelism": f"{pairs}P{pairs}D",
                    "handoffs_per_step": per_step,
-                   **({"chained": "recv(chained=True) into two alternating block sets"}
+                   **({"chained": "recv(chained=True), each hand-off of a chain into its own "
+                                  "block set (the chain restarts when the set ring wraps)"}
                       if args.chained and trace is None and not kivi and args.batch == 1 else {}),
                    **({"oversubscribed_dry_run": f"{world} ranks on "
                        f"{torch.cuda.device_count()} GPUs (pairs share a GPU): not a measurement"}
@@ -842,8 +846,8 @@ def main():
     ap.add_argument("--ref-layers", type=int, default=None,
                     help="reference arm: layers per step (default: the whole workload up to 16 GB of fp16 KV)")
     ap.add_argument("--chained", action="store_true",
-                    help="N>1 fixed workloads: chained pulls (recv(chained=True)) into two "
-                         "alternating block sets")
+                    help="N>1 fixed workloads: chained pulls (recv(chained=True)), each "
+                         "hand-off of a chain into its own block set")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--queue-depth", type=int, default=4,
@@ -864,7 +868,7 @@ def main():
                     help="N>1: hold each pull in the GPU front-end until chunk 0 is published")
     args = ap.parse_args()
     if args.chained:
-        args.no_e2e = True  # the alternating block sets would double the e2e download
+        args.no_e2e = True  # the ring of block sets would inflate the e2e download
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
 

@@ -165,10 +165,13 @@ int kvx_dequant_scatter_paged(const void* codes, const void* scale, const void* 
  * running; everything that touches stream-ordered memory (the slot mapping,
  * the cache, done_counter) waits for it (griddepcontrol.wait).
  * KVX_PULL_CHAINED (with KVX_PULL_PDL): the caller promises that the stream's
- * previous kernel is a pull of the same pair AND that this hand-off's slot
- * mapping is ready and its destination blocks are not written by that pull;
- * the consumers then write the cache while the previous pull drains, and
- * only the completion (done_counter, the free flag) waits for it.
+ * previous kernel is a pull of the same pair, and -- for the whole run of
+ * chained pulls since the last unchained one -- that every slot mapping was
+ * ready before the run started and that no two pulls of the run write the
+ * same cache blocks (several of them may be writing at once).  The
+ * consumers then write while the previous pulls drain; only the completion
+ * (done_counter, the free flag) waits, so pulls complete in order and an
+ * unchained pull after the run starts after all of them.
  */
 #define KVX_PULL_PDL 1
 #define KVX_PULL_CHAINED 2
@@ -363,8 +366,9 @@ int kvx_handoff_chunk_plan(int64_t n_layers, int64_t n_tokens, int n_heads, int 
  *     published; KVX_PAIR_PDL: programmatic dependent launch, so a pull
  *     streams its slot while the previous hand-off's pull drains;
  *     KVX_PAIR_CHAINED with KVX_PAIR_PDL: KVX_PULL_CHAINED's promise --
- *     back-to-back recvs into distinct blocks with ready slot mappings --
- *     so the pull also writes the cache during the previous pull's drain).
+ *     a run of back-to-back recvs, each into blocks no other recv of the run
+ *     writes, slot mappings ready before the run -- so the pull also writes
+ *     the cache while earlier pulls drain).
  * Validation: n_tokens <= max_tokens, the head window inside the planes, the
  * current device == the creating device.  Replaces the kv_delay the
  * reference charges per request (simulate.py:221-235). */

@@ -694,9 +694,10 @@ class PairChannel:
         download the decode cache to pinned host memory after the hand-off.
         ``chained`` (fused pull with PDL, default format): the caller promises
         that the previous operation on the current stream is this channel's
-        previous ``recv`` and that this hand-off's slot mapping is ready and
-        its blocks are not the previous hand-off's -- the pull then writes the
-        cache while the previous pull drains (kvx.h KVX_PAIR_CHAINED)."""
+        previous ``recv``, and for the whole run of chained recvs since the
+        last unchained one, that every slot mapping was ready before the run
+        and no two recvs of the run write the same blocks -- the pull then
+        writes the cache while earlier pulls drain (kvx.h KVX_PAIR_CHAINED)."""
         if self.role != "decode":
             raise RuntimeError("recv() on the prefill end of the channel")
         self.check()
