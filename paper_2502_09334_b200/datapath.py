@@ -293,19 +293,22 @@ def _quant_pack_layers(src: KVPlanes, packed: PackedKV, l0: int, l1: int, stream
 def dequant_scatter_layers(packed: PackedKV, dst: KVPlanes, l0: int, l1: int,
                            stream=None, bulk: bool = False, ready: tuple | None = None,
                            done: tuple | None = None, ctl: int | None = None,
-                           pdl: bool = False) -> None:
+                           pdl: bool = False, chained: bool = False) -> None:
     """K3 on layers [l0, l1).  ``bulk``: TMA bulk-staged variant (for payloads
     read over NVLink).  ``ready=(flags_addr, value, layers_per_chunk)``: the
     bulk kernel waits in-kernel until each chunk's doorbell reaches ``value``
     (one launch per hand-off).  ``done=(counter_addr, peer_free_addr)``:
     in-kernel completion (the last CTA sets the prefill side's free flag to
     ``value``; see kvx.h for the sequence protocol).  ``ctl``: control block
-    (abort / timeout of the waits).  ``pdl``: programmatic dependent launch."""
+    (abort / timeout of the waits).  ``pdl``: programmatic dependent launch;
+    ``chained`` (with ``pdl``): kvx.h KVX_PULL_CHAINED."""
     with nvtx_range(f"kvx.K3 layers[{l0},{l1})"):
-        _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done, ctl, pdl)
+        _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done, ctl, pdl,
+                                chained)
 
 
-def _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done, ctl, pdl) -> None:
+def _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done, ctl, pdl,
+                            chained=False) -> None:
     lay = packed.layout
     k, v = dst.ptrs(l0)
     c, s, z = packed.ptrs(l0)
@@ -314,8 +317,9 @@ def _dequant_scatter_layers(packed, dst, l0, l1, stream, bulk, ready, done, ctl,
     if bulk or ready is not None:
         rf, rv, lpc = ready if ready is not None else (None, 0, 1)
         dc, pf = done if done is not None else (None, None)
-        _lib.call("kvx_pull_dequant_scatter_paged", *args, rf, rv, lpc, dc, pf, ctl,
-                  _lib.KVX_PULL_PDL if pdl else 0, _stream_ptr(stream))
+        flags = (_lib.KVX_PULL_PDL | (_lib.KVX_PULL_CHAINED if chained else 0)) if pdl else 0
+        _lib.call("kvx_pull_dequant_scatter_paged", *args, rf, rv, lpc, dc, pf, ctl, flags,
+                  _stream_ptr(stream))
     else:
         _lib.call("kvx_dequant_scatter_paged", *args, _stream_ptr(stream))
 
