@@ -1304,8 +1304,7 @@ int kvx_pull_dequant_scatter_paged_kivi(const void* payload, int64_t payload_lay
                                         void* peer_free_flag, void* ctl, int flags,
                                         void* stream) {
   if ((ready_flags && (!aligned(ready_flags, 4) || layers_per_chunk < 1)) || !aligned(ctl, 8) ||
-      (flags & ~(KVX_PULL_PDL | KVX_PULL_CHAINED)) ||
-      ((flags & KVX_PULL_CHAINED) && !(flags & KVX_PULL_PDL)))
+      (flags & ~KVX_PULL_PDL))  // the kivi pull has no chained variant
     return KVX_ERR_INVALID_ARG;
   if ((done_counter != nullptr) != (peer_free_flag != nullptr) ||
       (done_counter && (!ready_flags || !aligned(done_counter, 4) || !aligned(peer_free_flag, 4))))
